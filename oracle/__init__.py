@@ -1,0 +1,167 @@
+"""CPU oracle for the SMC-SD verification hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_2604_15672_b200`` never imports it, and the C source here shares no code with
+``paper_2604_15672_b200/csrc``.
+
+The arithmetic lives in ``smcsd_oracle.c`` (plain fp64 loops, built with
+``-ffp-contract=off``); this module only builds it and marshals numpy arrays.
+Every function cites the PAPER.md passage it follows (see the C file).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "smcsd_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+ST_DEGENERATE = 1
+ST_NOT_ABSCONT = 2
+ST_BAD_TOKEN = 4
+ST_NONFINITE = 8
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+               "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        vp, i64, i32, dbl, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_uint64
+        L.orc_philox4x32_10.argtypes = [vp, vp, vp]
+        L.orc_row_logprob.argtypes = [vp, i32, i64, dbl, i64, vp]
+        L.orc_row_logprob.restype = dbl
+        L.orc_row_partial.argtypes = [vp, i32, i64, i64, dbl, i64, vp]
+        L.orc_row_partial.restype = i32
+        L.orc_combine_partials.argtypes = [vp, i32, i64, vp]
+        L.orc_combine_partials.restype = dbl
+        L.orc_weights.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp, i32, i32, i32, i64,
+                                  dbl, dbl, dbl, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_resample.argtypes = [vp, i32, i32, i64, dbl, u64, u64, vp, vp, vp, vp, vp, vp, vp,
+                                   vp, vp, vp, vp, vp, vp, vp]
+        L.orc_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _dtype_code(arr: np.ndarray) -> int:
+    if arr.dtype == np.float32:
+        return 0
+    if arr.dtype == np.uint16:   # bf16 bit patterns
+        return 1
+    raise TypeError(f"logits must be float32 or uint16 (bf16 bits), got {arr.dtype}")
+
+
+def philox4x32_10(ctr, key):
+    c = np.ascontiguousarray(np.asarray(ctr, dtype=np.uint32))
+    k = np.ascontiguousarray(np.asarray(key, dtype=np.uint32))
+    out = np.zeros(4, dtype=np.uint32)
+    lib().orc_philox4x32_10(_ptr(c), _ptr(k), _ptr(out))
+    return out
+
+
+def row_logprob(row: np.ndarray, d: int, tau: float = 1.0):
+    """ell = log-softmax(tau*z)[d] in fp64.  Returns (ell, flag)."""
+    row = np.ascontiguousarray(row)
+    flag = np.zeros(1, dtype=np.uint32)
+    ell = lib().orc_row_logprob(_ptr(row), _dtype_code(row), row.shape[-1], float(tau), int(d), _ptr(flag))
+    return ell, int(flag[0])
+
+
+def row_partial(row_shard: np.ndarray, v_begin: int, d: int, tau: float = 1.0):
+    """(m, s, x) of one vocab shard, natural-log domain; returns (array[3], has_nan_or_posinf)."""
+    row_shard = np.ascontiguousarray(row_shard)
+    out = np.zeros(3, dtype=np.float64)
+    bad = lib().orc_row_partial(_ptr(row_shard), _dtype_code(row_shard), int(v_begin),
+                                row_shard.shape[-1], float(tau), int(d), _ptr(out))
+    return out, bool(bad)
+
+
+def combine_partials(parts: np.ndarray):
+    """Merge [G][3] shard partials in rank order -> (ell, flag)."""
+    parts = np.ascontiguousarray(parts, dtype=np.float64)
+    flag = np.zeros(1, dtype=np.uint32)
+    ell = lib().orc_combine_partials(_ptr(parts), parts.shape[0], 3, _ptr(flag))
+    return ell, int(flag[0])
+
+
+def weights(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=None,
+            alpha=1.0, tau_p=1.0, tau_q=1.0):
+    """S1-S4 oracle.  logits_p: [P][N][rpp_p][ld], logits_q: [P][N][rpp_q][ld] (float32 or
+    uint16 bf16 bits), tokens: [P][N][K] int32.  Returns a dict of numpy outputs."""
+    lp = np.ascontiguousarray(logits_p)
+    lq = np.ascontiguousarray(logits_q)
+    assert lp.dtype == lq.dtype
+    tok = np.ascontiguousarray(tokens, dtype=np.int32)
+    P, N, K = tok.shape
+    ld_p, rpp_p = lp.shape[-1], lp.shape[-2]
+    ld_q, rpp_q = lq.shape[-1], lq.shape[-2]
+    V = ld_p if V is None else V
+    nd = None if n_drafted is None else np.ascontiguousarray(n_drafted, dtype=np.int32)
+    lw = None if logw_prev is None else np.ascontiguousarray(logw_prev, dtype=np.float32)
+    out = dict(logw=np.zeros((P, N), np.float32), logp_tok=np.zeros((P, N, K)),
+               logq_tok=np.zeros((P, N, K)), lse=np.zeros(P), ess=np.zeros(P),
+               wnorm=np.zeros((P, N)), status=np.zeros(P, np.uint32))
+    scratch = np.zeros(2 * N)
+    lib().orc_weights(_ptr(lp), ld_p, rpp_p, _ptr(lq), ld_q, rpp_q, _dtype_code(lp), _ptr(tok),
+                      _ptr(nd), _ptr(lw), P, N, K, V, float(alpha), float(tau_p), float(tau_q),
+                      _ptr(out["logw"]), _ptr(out["logp_tok"]), _ptr(out["logq_tok"]),
+                      _ptr(out["lse"]), _ptr(out["ess"]), _ptr(out["wnorm"]), _ptr(out["status"]),
+                      _ptr(scratch))
+    return out
+
+
+def resample(logw, *, eta=float("inf"), seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None):
+    """S4-S7 oracle from fp32 log-weights [P][N]."""
+    lw = np.ascontiguousarray(logw, dtype=np.float32)
+    P, N = lw.shape
+    un = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.uint32)
+    out = dict(ancestors=np.zeros((P, N), np.int32), offspring=np.zeros((P, N), np.int32),
+               slot_src=np.zeros((P, N), np.int32), logw=np.zeros((P, N), np.float32),
+               resampled=np.zeros(P, np.uint8), ess=np.zeros(P), lse=np.zeros(P),
+               n_ties=np.zeros(P, np.int32), status=np.zeros(P, np.uint32),
+               wnorm=np.zeros((P, N)), cdf=np.zeros((P, N)))
+    scratch = np.zeros(4 * N)
+    iscratch = np.zeros(3 * N, np.int32)
+    lib().orc_resample(_ptr(lw), P, N, int(prompt_base), float(eta), int(seed) & (2**64 - 1),
+                       int(step) & (2**64 - 1), _ptr(un), _ptr(out["ancestors"]),
+                       _ptr(out["offspring"]), _ptr(out["slot_src"]), _ptr(out["logw"]),
+                       _ptr(out["resampled"]), _ptr(out["ess"]), _ptr(out["lse"]),
+                       _ptr(out["n_ties"]), _ptr(out["status"]), _ptr(out["wnorm"]),
+                       _ptr(out["cdf"]), _ptr(scratch), _ptr(iscratch))
+    return out
+
+
+def kv_reindex(dst: np.ndarray, src: np.ndarray, src_index: np.ndarray, *, n_outer, outer_stride,
+               prompt_stride, particle_stride, seg_count, seg_bytes, seg_stride):
+    """S8/S9 oracle: byte copies (strides in bytes).  dst is src for in-place."""
+    idx = np.ascontiguousarray(src_index, dtype=np.int32)
+    P, N = idx.shape
+    lib().orc_kv_reindex(_ptr(dst), _ptr(src), n_outer, outer_stride, prompt_stride,
+                         particle_stride, seg_count, seg_bytes, seg_stride, _ptr(idx), P, N)
+
+
+def neg_log_n(N: int) -> np.float32:
+    """The S7 reset value fl32(-ln N) as the oracle computes it (via one resample call)."""
+    out = resample(np.zeros((1, N), np.float32), eta=float("inf"))
+    return out["logw"][0, 0]

@@ -1,0 +1,421 @@
+/*
+ * smcsd_oracle.c -- plain, slow, single-threaded fp64 CPU oracle for the SMC-SD
+ * verification hot path (arxiv 2604.15672, "Sequential Monte Carlo Speculative Decoding").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2604_15672_b200/, libsmcsd.so) never calls, links or imports it, and this
+ * file shares no source, header, table or constant generator with csrc/.
+ *
+ * Every function follows the paper's definitions in the paper's order, with no
+ * blocking, fusion or reordering.  Citations are PAPER.md line numbers (LaTeX source
+ * in /root/reference) plus the algorithm / equation they fall in; readings of
+ * ambiguous passages are the G-numbers listed in DESIGN.md section 3.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -shared -fPIC -lm
+ * (-ffp-contract=off: no fused multiply-add, so every fp64 op is one IEEE rounding.)
+ *
+ * Pinned by tests/test_oracle_*.py (see DESIGN.md section 4 for the pin table).
+ * Parity unpinned: nothing here -- multi-round trajectories are not part of the oracle.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+/* Status bits (the ABI contract, retyped here from DESIGN.md section 2; no shared header). */
+#define ORC_ST_DEGENERATE  1u  /* every log-weight of the prompt is -inf           */
+#define ORC_ST_NOT_ABSCONT 2u  /* log q(d) = -inf at a drafted token, p << q violated */
+#define ORC_ST_BAD_TOKEN   4u  /* drafted token outside [0,V), or n_drafted outside [0,K]         */
+#define ORC_ST_NONFINITE   8u  /* NaN / +inf logit or log-weight, or a row whose max is -inf       */
+
+/* ------------------------------------------------------------------------------------ */
+/* Philox4x32-10 counter-based generator (Salmon et al., SC'11; the Random123 reference  */
+/* algorithm).  Not in the paper: reading G5/G10 in DESIGN.md (counter-based uniforms,   */
+/* north star).  Multipliers and Weyl key increments are the published constants.       */
+/* ------------------------------------------------------------------------------------ */
+void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {            /* key schedule: bump the key before rounds 2..10 */
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t prod0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t prod1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(prod0 >> 32), lo0 = (uint32_t)prod0;
+        uint32_t hi1 = (uint32_t)(prod1 >> 32), lo1 = (uint32_t)prod1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Decode one logit.  dtype 0 = fp32, 1 = bf16 (the top 16 bits of an fp32).  Both       */
+/* decodes are exact in fp64.                                                             */
+/* ------------------------------------------------------------------------------------ */
+static double decode_logit(const void *row, int dtype, int64_t v)
+{
+    if (dtype == 1) {
+        uint16_t bits16 = ((const uint16_t *)row)[v];
+        uint32_t bits32 = (uint32_t)bits16 << 16;
+        float f;
+        memcpy(&f, &bits32, sizeof f);
+        return (double)f;
+    }
+    return (double)((const float *)row)[v];
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* S1 over a column range.  For y_v = tau * z_v (temperature, reading G9):               */
+/*   m = max_v y_v,  s = sum_v exp(y_v - m) (ascending v),  x = y_d if d is in range.    */
+/* This is the log-sum-exp decomposition of the next-token conditional                    */
+/* p(y|x) = p(xy)/p(x) (Eq. 1a) for a softmax-parameterised model.          */
+/* `row` points at column v_begin; d_local = d - v_begin.  Returns 1 when a NaN or +inf   */
+/* logit is present.  When every y is -inf, m = -inf and s = 0.                          */
+/* ------------------------------------------------------------------------------------ */
+static int row_stats_range(const void *row, int dtype, int64_t v_len, double tau,
+                           int64_t d_local, double *m_out, double *s_out, double *x_out)
+{
+    int bad = 0;
+    double m = -INFINITY;
+    for (int64_t v = 0; v < v_len; ++v) {
+        double z = decode_logit(row, dtype, v);
+        if (isnan(z) || z == INFINITY) bad = 1;
+        double y = tau * z;
+        if (y > m) m = y;
+    }
+    double s = 0.0;
+    if (m != -INFINITY && !bad) {
+        for (int64_t v = 0; v < v_len; ++v) {
+            double y = tau * decode_logit(row, dtype, v);
+            s = s + exp(y - m);
+        }
+    }
+    double x = -INFINITY;
+    if (d_local >= 0 && d_local < v_len) x = tau * decode_logit(row, dtype, d_local);
+    *m_out = m;
+    *s_out = s;
+    *x_out = x;
+    return bad;
+}
+
+/* S1+S2 for a whole row: ell = y_d - m - ln s, the log-softmax at the drafted token,   */
+/* i.e. log p(d_j | x d_<j) of Alg. 1 line "Score".  Sets *flag to       */
+/* ORC_ST_NONFINITE when the row has a NaN/+inf logit or its max is -inf.               */
+double orc_row_logprob(const void *row, int dtype, int64_t V, double tau, int64_t d, uint32_t *flag)
+{
+    double m, s, x;
+    int bad = row_stats_range(row, dtype, V, tau, d, &m, &s, &x);
+    *flag = 0;
+    if (bad || m == -INFINITY) {
+        *flag = ORC_ST_NONFINITE;
+        return NAN;
+    }
+    return x - m - log(s);
+}
+
+/* TP reference pieces (north star: vocab-sharded logits, per-row max/sum-exp exchange).
+ * orc_row_partial: S1 on the shard of columns [v_begin, v_begin+v_len) -> (m, s, x),
+ * natural-log domain.  orc_combine_partials: merge G shards in rank order,
+ * M = max m_g, S = sum_g s_g exp(m_g - M), X = max_g x_g, ell = X - M - ln S.        */
+int orc_row_partial(const void *row_shard, int dtype, int64_t v_begin, int64_t v_len,
+                    double tau, int64_t d, double out3[3])
+{
+    return row_stats_range(row_shard, dtype, v_len, tau, d - v_begin, &out3[0], &out3[1], &out3[2]);
+}
+
+double orc_combine_partials(const double *parts /*[G][3]*/, int G, int64_t row_stride3,
+                            uint32_t *flag)
+{
+    double M = -INFINITY, X = -INFINITY;
+    for (int g = 0; g < G; ++g) {
+        const double *pg = parts + (int64_t)g * row_stride3;
+        if (pg[0] > M) M = pg[0];
+        if (pg[2] > X) X = pg[2];
+    }
+    *flag = 0;
+    if (M == -INFINITY || isnan(M) || M == INFINITY) {
+        *flag = ORC_ST_NONFINITE;
+        return NAN;
+    }
+    double S = 0.0;
+    for (int g = 0; g < G; ++g) {
+        const double *pg = parts + (int64_t)g * row_stride3;
+        if (pg[0] == -INFINITY) continue;
+        S = S + pg[1] * exp(pg[0] - M);
+    }
+    return X - M - log(S);
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* S4: normalise + ESS (Alg. 1 lines "normalize" / "effective sample size",             */
+/* PAPER.md:323-324; Eq. 3), in log space.              */
+/* From fp32 log-weights lam[0..N): M = max lam; e_n = exp(lam_n - M);                  */
+/* P_m = sum_{i<=m} e_i (sequential, reading G6); S = P_{N-1}; lse = M + ln S;          */
+/* ESS = S^2 / sum_n e_n^2 (sequential).  Returns 1 when degenerate (M = -inf).         */
+/* ------------------------------------------------------------------------------------ */
+static int s4_normalise(const float *lam, int N, double *e, double *Pcum,
+                        double *S_out, double *lse_out, double *ess_out)
+{
+    double M = -INFINITY;
+    for (int n = 0; n < N; ++n)
+        if ((double)lam[n] > M) M = (double)lam[n];
+    if (M == -INFINITY) return 1;
+    for (int n = 0; n < N; ++n) e[n] = exp((double)lam[n] - M);
+    double acc = 0.0;
+    for (int m = 0; m < N; ++m) {
+        acc = acc + e[m];
+        Pcum[m] = acc;
+    }
+    double S = Pcum[N - 1];
+    double sumsq = 0.0;
+    for (int n = 0; n < N; ++n) {
+        double sq = e[n] * e[n];
+        sumsq = sumsq + sq;
+    }
+    *S_out = S;
+    *lse_out = M + log(S);
+    *ess_out = (S * S) / sumsq;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* smcsd_weights oracle: S1-S4 for P prompts.                                            */
+/* Row (prompt p, particle n, draft position j) of a logits tensor lives at              */
+/*   base + ((p*N + n)*rows_per_particle + j)*ld   (elements).                           */
+/* S3 (Alg. 1 "Reweight"; power weight PAPER.md:1418, reading G11):        */
+/*   Delta_n = sum_{j<k_n} (alpha*ell^p_j - ell^q_j) in fp64, bonus row excluded          */
+/*   (PAPER.md:1168); lam'_n = fl32(lam_prev_n + Delta_n).                                */
+/* A particle with an invalid row (bad token, non-finite row, q(d)=0) gets lam' = -inf  */
+/* and its prompt's status bit is set (reading G13).                                     */
+/* logp_tok/logq_tok (optional, [P][N][K] fp64): ell per row; 0 for rows j >= k_n, NaN   */
+/* for invalid rows.  wnorm (optional [P][N] fp64): e_n / S.                              */
+/* ------------------------------------------------------------------------------------ */
+void orc_weights(const void *logits_p, int64_t ld_p, int rpp_p,
+                 const void *logits_q, int64_t ld_q, int rpp_q, int dtype,
+                 const int32_t *tokens, const int32_t *n_drafted, const float *logw_prev,
+                 int P, int N, int K, int64_t V, double alpha, double tau_p, double tau_q,
+                 float *logw_out, double *logp_tok, double *logq_tok,
+                 double *lse_out, double *ess_out, double *wnorm, uint32_t *status,
+                 double *scratch /* 2*N doubles */)
+{
+    size_t esz = dtype == 1 ? 2 : 4;
+    for (int p = 0; p < P; ++p) {
+        uint32_t st = 0;
+        for (int n = 0; n < N; ++n) {
+            int64_t pn = (int64_t)p * N + n;
+            int k_n = n_drafted ? n_drafted[pn] : K;
+            int bad = 0;
+            if (k_n < 0 || k_n > K) {
+                st |= ORC_ST_BAD_TOKEN;
+                bad = 1;
+                k_n = 0;
+            }
+            double delta = 0.0;
+            for (int j = 0; j < K; ++j) {
+                double lp = 0.0, lq = 0.0;
+                if (j < k_n) {
+                    int64_t d = tokens[pn * K + j];
+                    if (d < 0 || d >= V) {
+                        st |= ORC_ST_BAD_TOKEN;
+                        bad = 1;
+                        lp = NAN;
+                        lq = NAN;
+                    } else {
+                        const char *rp = (const char *)logits_p + ((pn * rpp_p + j) * ld_p) * (int64_t)esz;
+                        const char *rq = (const char *)logits_q + ((pn * rpp_q + j) * ld_q) * (int64_t)esz;
+                        uint32_t fp, fq;
+                        lp = orc_row_logprob(rp, dtype, V, tau_p, d, &fp);
+                        lq = orc_row_logprob(rq, dtype, V, tau_q, d, &fq);
+                        if (fp | fq) {
+                            st |= ORC_ST_NONFINITE;
+                            bad = 1;
+                        } else if (lq == -INFINITY) {
+                            st |= ORC_ST_NOT_ABSCONT;
+                            bad = 1;
+                        } else {
+                            delta = delta + (alpha * lp - lq);
+                        }
+                    }
+                }
+                if (logp_tok) logp_tok[pn * K + j] = lp;
+                if (logq_tok) logq_tok[pn * K + j] = lq;
+            }
+            float prev = logw_prev ? logw_prev[pn] : (float)(-log((double)N));
+            if (isnan(prev) || prev == INFINITY) {
+                st |= ORC_ST_NONFINITE;
+                bad = 1;
+            }
+            logw_out[pn] = bad ? -INFINITY : (float)((double)prev + delta);
+        }
+        /* S4 on the fp32 log-weights just stored */
+        double S, lse, ess;
+        double *e = scratch, *Pc = scratch + N;
+        if (s4_normalise(logw_out + (int64_t)p * N, N, e, Pc, &S, &lse, &ess)) {
+            st |= ORC_ST_DEGENERATE;
+            if (lse_out) lse_out[p] = -INFINITY;
+            if (ess_out) ess_out[p] = 0.0;
+            if (wnorm) for (int n = 0; n < N; ++n) wnorm[(int64_t)p * N + n] = 0.0;
+        } else {
+            if (lse_out) lse_out[p] = lse;
+            if (ess_out) ess_out[p] = ess;
+            if (wnorm) for (int n = 0; n < N; ++n) wnorm[(int64_t)p * N + n] = e[n] / S;
+        }
+        if (status) status[p] = st;
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* smcsd_resample oracle: S4-S7 for P prompts from fp32 log-weights.                    */
+/* S5: resample iff ESS < eta (strict; reading G3).                        */
+/* S6: systematic resampling (north star; reading G1) by inverse CDF:      */
+/*   U = word0(Philox4x32-10(key=(seed_lo,seed_hi), ctr=(step_lo,step_hi,prompt,0)))     */
+/*       * 2^-32   (or uniforms[p] * 2^-32 when the override is given),                  */
+/*   C_m = P_m / S,  u_n = (n + U) / N,  a_n = #{m : C_m <= u_n}                         */
+/*   (= min{m : u_n < C_m}; zero-weight particles are never chosen),        */
+/*   o_m = #{n : a_n = m},  ties = #{(n,m) : |u_n - C_m| <= 2^-40} (reading G7).          */
+/*   In-place slot plan (reading G14): survivors keep their slot; the list E of extra    */
+/*   copies (m repeated o_m - 1 times, ascending m) fills the dead slots D (o_m = 0,      */
+/*   ascending): slot_src[D_i] = E_i, slot_src[m] = m for survivors.                      */
+/* S7: after a resample every log-weight is reset to fl32(-ln N) (G8).     */
+/* Without a resample: ancestors = identity, offspring = 1, lam kept.                    */
+/* Degenerate prompt: lse = -inf, ESS = 0, identity ancestry, resampled = 0.             */
+/* NaN / +inf input log-weights are flagged NONFINITE and treated as -inf (G13).         */
+/* ------------------------------------------------------------------------------------ */
+void orc_resample(const float *logw, int P, int N, int64_t prompt_base, double eta,
+                  uint64_t seed, uint64_t step, const uint32_t *uniforms,
+                  int32_t *ancestors, int32_t *offspring, int32_t *slot_src, float *logw_out,
+                  uint8_t *resampled, double *ess_out, double *lse_out, int32_t *n_ties,
+                  uint32_t *status, double *wnorm, double *cdf_out,
+                  double *scratch /* 4*N doubles */, int32_t *iscratch /* 3*N ints */)
+{
+    const double two_m32 = 1.0 / 4294967296.0;
+    const double tie_delta = 1.0 / 1099511627776.0; /* 2^-40 */
+    float *lam = (float *)(iscratch + 0);          /* reuse int scratch as float storage */
+    int32_t *a = iscratch + N;
+    int32_t *o = iscratch + 2 * N;
+    double *e = scratch, *Pc = scratch + N, *C = scratch + 2 * N, *u = scratch + 3 * N;
+    float reset = (float)(-log((double)N));
+
+    for (int p = 0; p < P; ++p) {
+        uint32_t st = 0;
+        const float *lw = logw + (int64_t)p * N;
+        for (int n = 0; n < N; ++n) {
+            float v = lw[n];
+            if (isnan(v) || v == INFINITY) {
+                st |= ORC_ST_NONFINITE;
+                v = -INFINITY;
+            }
+            lam[n] = v;
+        }
+        double S, lse, ess;
+        int degenerate = s4_normalise(lam, N, e, Pc, &S, &lse, &ess);
+        int do_resample = 0;
+        int ties = 0;
+        if (degenerate) {
+            st |= ORC_ST_DEGENERATE;
+            lse = -INFINITY;
+            ess = 0.0;
+        } else {
+            do_resample = ess < eta;
+        }
+        if (do_resample) {
+            double U;
+            if (uniforms) {
+                U = (double)uniforms[p] * two_m32;
+            } else {
+                uint64_t prompt = (uint64_t)(prompt_base + p);
+                uint32_t ctr[4] = {(uint32_t)step, (uint32_t)(step >> 32), (uint32_t)prompt, 0u};
+                uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+                uint32_t r[4];
+                orc_philox4x32_10(ctr, key, r);
+                U = (double)r[0] * two_m32;
+            }
+            for (int m = 0; m < N; ++m) C[m] = Pc[m] / S;
+            for (int n = 0; n < N; ++n) u[n] = ((double)n + U) / (double)N;
+            for (int n = 0; n < N; ++n) {
+                int count = 0;
+                for (int m = 0; m < N; ++m)
+                    if (C[m] <= u[n]) count++;
+                a[n] = count;
+            }
+            for (int m = 0; m < N; ++m) o[m] = 0;
+            for (int n = 0; n < N; ++n) o[a[n]]++;
+            for (int n = 0; n < N; ++n)
+                for (int m = 0; m < N; ++m)
+                    if (fabs(u[n] - C[m]) <= tie_delta) ties++;
+            if (ancestors) for (int n = 0; n < N; ++n) ancestors[(int64_t)p * N + n] = a[n];
+            if (offspring) for (int m = 0; m < N; ++m) offspring[(int64_t)p * N + m] = o[m];
+            if (slot_src) {
+                /* E: extra copies, ascending source; D: dead slots, ascending. */
+                int32_t *plan = slot_src + (int64_t)p * N;
+                int n_dead = 0;
+                for (int m = 0; m < N; ++m) plan[m] = m;
+                /* walk the dead slots and the extra list in step */
+                int src = 0, left = 0;
+                for (int m = 0; m < N; ++m) {
+                    if (o[m] != 0) continue;
+                    while (left == 0) {         /* advance to the next source with an extra copy */
+                        if (o[src] >= 2) left = o[src] - 1;
+                        if (left == 0) src++;
+                    }
+                    plan[m] = src;
+                    n_dead++;
+                    left--;
+                    if (left == 0) src++;
+                }
+                (void)n_dead;
+            }
+            for (int n = 0; n < N; ++n) logw_out[(int64_t)p * N + n] = reset;
+            if (cdf_out) for (int m = 0; m < N; ++m) cdf_out[(int64_t)p * N + m] = C[m];
+        } else {
+            for (int n = 0; n < N; ++n) {
+                if (ancestors) ancestors[(int64_t)p * N + n] = n;
+                if (offspring) offspring[(int64_t)p * N + n] = 1;
+                if (slot_src) slot_src[(int64_t)p * N + n] = n;
+                logw_out[(int64_t)p * N + n] = lam[n];
+            }
+            if (cdf_out) for (int m = 0; m < N; ++m)
+                cdf_out[(int64_t)p * N + m] = degenerate ? 0.0 : Pc[m] / S;
+        }
+        if (wnorm) for (int n = 0; n < N; ++n)
+            wnorm[(int64_t)p * N + n] = degenerate ? 0.0 : e[n] / S;
+        if (resampled) resampled[p] = (uint8_t)do_resample;
+        if (ess_out) ess_out[p] = ess;
+        if (lse_out) lse_out[p] = lse;
+        if (n_ties) n_ties[p] = ties;
+        if (status) status[p] = st;
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* S8/S9: reindex per-particle state to the ancestor's (Alg. 1: x^(n) <- x^(a_n) d^(a_n) */
+/* x+_(a_n)).  Block (o, p, n) = seg_count segments of seg_bytes bytes at  */
+/* base + o*outer_stride + p*prompt_stride + n*particle_stride + s*seg_stride.           */
+/* Out-of-place (dst != src): dst block n <- src block src_index[n] for every n.         */
+/* In-place (dst == src): for every n with src_index[n] != n, block n <- block           */
+/* src_index[n] (the slot plan guarantees sources are never destinations).              */
+/* ------------------------------------------------------------------------------------ */
+void orc_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_stride,
+                    int64_t prompt_stride, int64_t particle_stride, int64_t seg_count,
+                    int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index, int P, int N)
+{
+    int in_place = (dst == src);
+    for (int64_t o = 0; o < n_outer; ++o)
+        for (int p = 0; p < P; ++p)
+            for (int n = 0; n < N; ++n) {
+                int s = src_index[(int64_t)p * N + n];
+                if (in_place && s == n) continue;
+                for (int64_t g = 0; g < seg_count; ++g) {
+                    char *d = (char *)dst + o * outer_stride + p * prompt_stride + n * particle_stride + g * seg_stride;
+                    const char *sp = (const char *)src + o * outer_stride + p * prompt_stride + (int64_t)s * particle_stride + g * seg_stride;
+                    memcpy(d, sp, (size_t)seg_bytes);
+                }
+            }
+}
