@@ -1,0 +1,456 @@
+#!/usr/bin/env python
+"""bench.py -- SMC-SD verify + resample hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg1|cfg3|cfg4|cfg5]
+                    [--impl ours|reference]
+
+A step is one pass of the whole hot path over one batch of
+synthetic input.  Default workload (configs[1] of BASELINE.json, one prompt per GPU):
+  verify + resample  V=128256, N=16, K=8, bf16 logits   (smcsd_step: S1-S7, one launch)
+  + KV reindex of Llama-3.1-70B-shaped per-particle KV caches (80 L x 2 x 8 KV heads x
+    seq 2048 x d 128 bf16 = 640 MiB per particle) with the in-place slot plan (S8)
+  + token-history reindex (S9).
+eta = +inf forces a resample every step (worst case).  Logits come from a ring of 6 input
+sets (394 MB > 126 MB L2); the KV caches (10.7 GB) exceed L2.  Timing: W untimed steps, then K
+steps bracketed by barrier + synchronize, CUDA events on the launching stream, max over ranks.
+For N > 1 (torchrun) each rank runs its own prompt (global prompt index = rank): weak scaling,
+no data-path collective (cfg5 is the tensor-parallel variant with the NCCL exchange).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SMC verify+resample steps/s; achieved HBM GB/s vs B200 peak"
+NORTH_STAR_TBS = 8.0
+KV70B = dict(L=80, H=8, S=2048, d=128)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def traffic_table():
+    """dram bytes per launch per kernel from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and clocks-event reasons with NVML while the timed region runs."""
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x100: "display_clock_setting"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            h = None
+            try:
+                uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU") else uuid)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.h, self.nv = h, pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        names = [n for b, n in self.NAMES.items() if self.reasons & b and b != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ env
+def dist_env(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "reference":
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------------------ workloads
+class Cfg2Step:
+    """configs[1]: verify+resample (N=16, K=8, V=128256 bf16) + 70B-KV in-place reindex."""
+    name = "cfg2"
+
+    def __init__(self, dev, rank, args, N=16, K=8, V=128256, P=1, ring=6, kv=True):
+        import torch
+        import paper_2604_15672_b200 as smc
+        import synth
+        self.smc, self.torch = smc, torch
+        self.dev, self.N, self.K, self.V, self.P = dev, N, K, V, P
+        self.prompt_base = rank * P
+        self.ring = [synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, device=dev,
+                                     seed=synth.GEN_SEED_BASE + 2 + 1000 * r + 7 * rank)
+                     for r in range(ring)]
+        self.logw = synth.uniform_prior(P, N, device=dev)
+        total = args.warmup + args.steps + 4
+        mk = lambda dt: torch.zeros((total, P, N), dtype=dt, device=dev)
+        self.anc, self.off, self.slot = mk(torch.int32), mk(torch.int32), mk(torch.int32)
+        self.out = smc.Outputs(logw=self.logw, status=torch.zeros(P, dtype=torch.int32, device=dev),
+                               resampled=torch.zeros(P, dtype=torch.uint8, device=dev),
+                               ess=torch.zeros(P, dtype=torch.float64, device=dev),
+                               lse=torch.zeros(P, dtype=torch.float64, device=dev),
+                               n_ties=torch.zeros(P, dtype=torch.int32, device=dev))
+        self.ws = smc.Workspace(dev)
+        self.ws.get(P, N, K, V)
+        self.kv = None
+        if kv:
+            L, H, S, d = KV70B["L"], KV70B["H"], KV70B["S"], KV70B["d"]
+            self.kv = synth.kv_bits_fast((L, 2, P, N, H, S, d), seed=91 + rank, device=dev)
+            self.kv_geom = smc.kv_geometry(self.kv)
+            self.Bp = L * 2 * H * S * d * 2
+            self.T = 2048
+            self.hist = torch.randint(0, V, (P, N, self.T), dtype=torch.int32, device=dev)
+            self.hist_geom = dict(n_outer=1, outer_stride=0, prompt_stride=N * self.T * 4,
+                                  particle_stride=self.T * 4, seg_count=1, seg_bytes=self.T * 4,
+                                  seg_stride=self.T * 4)
+        self.kernels = ["k_rowstats(step)"] + (["k_kv_reindex(kv)", "k_kv_reindex(tokens)"] if kv else [])
+
+    def launches_per_step(self):
+        return len(self.kernels)
+
+    def step(self, i, events=None, inputs=None):
+        smc = self.smc
+        lp, lq, tok = inputs if inputs is not None else self.ring[i % len(self.ring)]
+        o = self.out
+        o.ancestors, o.offspring, o.slot_src = self.anc[i], self.off[i], self.slot[i]
+        if events: events[0].record()
+        smc.smcsd_step(lp, lq, tok, V=self.V, logw_prev=self.logw, eta=math.inf,
+                       seed=0x5EED5EED, step=i, prompt_base=self.prompt_base, out=o,
+                       fields=(), workspace=self.ws)
+        if events: events[1].record()
+        if self.kv is not None:
+            smc.smcsd_kv_reindex(self.kv, self.kv, self.slot[i], **self.kv_geom)
+            if events: events[2].record()
+            smc.smcsd_kv_reindex(self.hist, self.hist, self.slot[i], **self.hist_geom)
+            if events: events[3].record()
+
+    # algorithmic bytes
+    def logit_bytes(self):
+        P, N, K, V = self.P, self.N, self.K, self.V
+        return P * (2 * N * K * V * 2 + N * K * 4 + 3 * N * 4)
+
+    def kv_bytes(self, steps):
+        """Per-step in-place KV + token bytes: (R_src + W_dst) * block, from the recorded plans."""
+        off = self.off[steps].cpu()
+        kv, tok = [], []
+        for s in range(off.shape[0]):
+            r = int((off[s] >= 2).sum())
+            w = int((off[s] == 0).sum())
+            kv.append((r + w) * self.Bp)
+            tok.append((r + w) * self.T * 4)
+        return kv, tok
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_2604_15672_b200 as smc
+    from paper_2604_15672_b200.dist import max_over_ranks
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    hbm_peak, peak_src = peaks()
+    wl = Cfg2Step(dev, rank, args)
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- warm-up
+    for i in range(args.warmup):
+        wl.step(i)
+    torch.cuda.synchronize()
+
+    # ---- timed region (device time, CUDA events on the launching stream)
+    nk = wl.launches_per_step()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for k in range(args.steps):
+            wl.step(args.warmup + k, events=ev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    elapsed_ms = t0.elapsed_time(t1)
+    per_kernel_ms = [statistics.fmean(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps))
+                     for j in range(nk)]
+    elapsed_ms = max_over_ranks(elapsed_ms, dev)
+    ms_per_step = elapsed_ms / args.steps
+    value = world * wl.P * args.steps / (elapsed_ms / 1e3)
+
+    # ---- algorithmic bytes and roofline
+    timed = list(range(args.warmup, args.warmup + args.steps))
+    kvb, tokb = wl.kv_bytes(timed)
+    logit_b = wl.logit_bytes()
+    kv_avg, tok_avg = statistics.fmean(kvb), statistics.fmean(tokb)
+    step_bytes = logit_b + kv_avg + tok_avg
+    bytes_by_kernel = [logit_b, kv_avg, tok_avg]
+    kernels = []
+    traffic = traffic_table()
+    for name, ms, b in zip(wl.kernels, per_kernel_ms, bytes_by_kernel):
+        gbs = b / (ms / 1e3) / 1e9
+        kernels.append({"kernel": name, "avg_ms": round(ms, 5), "algorithmic_bytes": int(b),
+                        "achieved_gbs": round(gbs, 1), "frac_of_measured": round(gbs / hbm_peak, 4),
+                        "frac_of_8tbs": round(gbs / (NORTH_STAR_TBS * 1e3), 4)})
+    dom = max(range(len(kernels)), key=lambda j: per_kernel_ms[j])
+    dk = kernels[dom]
+    tr = traffic.get(dk["kernel"])
+    roofline = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(dk["achieved_gbs"] / hbm_peak, 4),
+                "traffic": tr, "kernel": dk["kernel"], "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": dk["algorithmic_bytes"]}
+    step_gbs = step_bytes / (ms_per_step / 1e3) / 1e9
+    anc = wl.anc[timed].cpu()
+    dead = statistics.fmean(float((wl.off[s] == 0).sum()) for s in timed)
+
+    # ---- end to end through the public API with host buffers (H2D of inputs, D2H of result)
+    e2e = run_e2e(wl, args, dev, world)
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded LM-like logits, random KV bits; no models)",
+        "config": {
+            "workload": "cfg2: verify+resample V=128256 N=16 K=8 bf16 logits, 1 prompt/GPU "
+                        "+ in-place KV reindex of Llama-3.1-70B-shaped KV (80L x 8 KV heads x "
+                        "d128 x seq2048 bf16, 640 MiB/particle) + token-history reindex",
+            "P_per_gpu": wl.P, "N": wl.N, "K": wl.K, "V": wl.V, "logits_dtype": "bf16",
+            "eta": "inf (resample every step)", "parallelism": f"dp{world} (prompts)",
+            "l2": "logits ring of 6 sets (394 MB > 126 MB L2); KV 10.7 GB > L2",
+            "kv_mode": "in-place slot plan", "mean_dead_slots": round(dead, 2),
+        },
+        "hbm": {"algorithmic_bytes_per_step": int(step_bytes),
+                "achieved_gbs": round(step_gbs, 1),
+                "frac_of_measured": round(step_gbs / hbm_peak, 4),
+                "frac_of_8tbs": round(step_gbs / (NORTH_STAR_TBS * 1e3), 4)},
+        "roofline": roofline,
+        "kernels": kernels,
+        "breakdown": {"verify_resample_us": round(per_kernel_ms[0] * 1e3, 2),
+                      "verify_resample_steps_per_s": round(1e3 / per_kernel_ms[0], 1)},
+        "e2e": e2e,
+        "gpu_launches": nk * args.steps,
+        "clocks": clk.summary(),
+        "library": smc.smcsd_version(),
+        "ancestor_sample": anc[-1, 0].tolist(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(wl, args, dev, world):
+    """Same metric through smcsd_step / smcsd_kv_reindex with inputs from pinned host memory:
+    every step copies that step's logits + tokens + prior H2D and reads logw + ancestors D2H."""
+    import torch
+    host = [(lp.cpu().pin_memory(), lq.cpu().pin_memory(), tok.cpu().pin_memory())
+            for lp, lq, tok in wl.ring[:2]]
+    stage = [torch.empty_like(t) for t in wl.ring[0]]
+    prior_h = wl.logw.cpu().pin_memory()
+    res_w = torch.empty_like(prior_h).pin_memory()
+    res_a = torch.empty((wl.P, wl.N), dtype=torch.int32).pin_memory()
+    steps = max(3, min(args.steps, 50))
+    base = args.warmup + args.steps
+
+    def one(i):
+        h = host[i % len(host)]
+        for s, t in zip(stage, h):
+            s.copy_(t, non_blocking=True)
+        wl.logw.copy_(prior_h, non_blocking=True)
+        wl.step(base + (i % 4), inputs=stage)
+        res_w.copy_(wl.logw, non_blocking=True)
+        res_a.copy_(wl.anc[base + (i % 4)], non_blocking=True)
+
+    one(0)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    t0.record()
+    for i in range(steps):
+        one(i)
+    t1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    from paper_2604_15672_b200.dist import max_over_ranks
+    ms = max_over_ranks(t0.elapsed_time(t1), dev)
+    h2d = sum(t.numel() * t.element_size() for t in host[0]) + prior_h.numel() * 4
+    d2h = res_w.numel() * 4 + res_a.numel() * 4
+    return {"value": round(world * wl.P * steps / (ms / 1e3), 3), "unit": "steps/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": steps, "wall_s": round(wall, 4)}
+
+
+# ------------------------------------------------------------------------------ CPU legs
+def oracle_step_sample(N=16, K=8, V=128256, kv_layers=1, seed=None, logits=None):
+    """One bounded sample of the cfg2 step on the host with the oracle: full S1-S7 on one
+    prompt's logits, plus the in-place KV reindex of `kv_layers` of the 80 layers (scaled).
+    Returns (seconds for S1-S7, seconds for the KV sample, scale factor for the KV)."""
+    import numpy as np
+    import torch
+    import oracle
+    import synth
+    if logits is None:
+        lp, lq, tok = synth.lm_logits(1, N, K, V, dtype=torch.bfloat16,
+                                      seed=seed or synth.GEN_SEED_BASE + 2)
+        logits = (lp.view(torch.int16).numpy().view(np.uint16),
+                  lq.view(torch.int16).numpy().view(np.uint16), tok.numpy())
+    lp, lq, tok = logits
+    prior = np.full((1, N), np.float32(-math.log(N)), np.float32)
+    t0 = time.perf_counter()
+    w = oracle.weights(lp, lq, tok, V=V, logw_prev=prior)
+    r = oracle.resample(w["logw"], eta=math.inf, seed=0x5EED5EED, step=0)
+    t1 = time.perf_counter()
+    H, S, d = KV70B["H"], KV70B["S"], KV70B["d"]
+    kv = np.empty((kv_layers, 2, 1, N, H, S, d), np.int16)
+    kv.view(np.uint8)[...] = 7
+    geom = dict(n_outer=kv_layers * 2, outer_stride=N * H * S * d * 2, prompt_stride=N * H * S * d * 2,
+                particle_stride=H * S * d * 2, seg_count=H, seg_bytes=S * d * 2, seg_stride=S * d * 2)
+    t2 = time.perf_counter()
+    oracle.kv_reindex(kv, kv, r["slot_src"], **geom)
+    t3 = time.perf_counter()
+    return t1 - t0, t3 - t2, KV70B["L"] / kv_layers, logits
+
+
+def cpu_baseline(wl, budget_s=12.0):
+    """The oracle as it stands, single-threaded, on this host, on a bounded sample."""
+    import numpy as np
+    import torch
+    lp, lq, tok = wl.ring[0]
+    logits = (lp.cpu().view(torch.int16).numpy().view(np.uint16),
+              lq.cpu().view(torch.int16).numpy().view(np.uint16), tok.cpu().numpy())
+    reps, t_w, t_kv = 0, [], []
+    start = time.perf_counter()
+    scale = 80.0
+    while reps < 1 or (time.perf_counter() - start < budget_s and reps < 20):
+        a, b, scale, logits = oracle_step_sample(logits=logits, kv_layers=2)
+        t_w.append(a); t_kv.append(b)
+        reps += 1
+    step_s = statistics.fmean(t_w) + statistics.fmean(t_kv) * scale
+    return {"value": round(1.0 / step_s, 4), "unit": "steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"{reps} x (full S1-S7 of one cfg2 prompt, 256 rows x 128256 bf16; "
+                      f"+ in-place KV reindex of 2 of 80 layers, scaled x{scale:.0f})",
+            "s1_s7_s": round(statistics.fmean(t_w), 4),
+            "kv_per_layer_s": round(statistics.fmean(t_kv) / 2, 5),
+            "host_cores_available": os.cpu_count()}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle, as it stands, on this host's cores (rank 0 only)."""
+    if rank != 0:
+        return
+    t_steps = []
+    logits = None
+    for i in range(args.warmup + args.steps):
+        a, b, scale, logits = oracle_step_sample(logits=logits, kv_layers=1)
+        if i >= args.warmup:
+            t_steps.append(a + b * scale)
+    step_s = statistics.fmean(t_steps)
+    value = 1.0 / step_s
+    line = {"metric": METRIC, "impl": "reference", "value": round(value, 4), "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(step_s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2 (see ours); oracle: full S1-S7 per step + 1 of 80 KV "
+                                   "layers reindexed and scaled x80",
+                       "P_per_gpu": 1, "N": 16, "K": 8, "V": 128256},
+            "cpu_baseline": {"value": round(value, 4), "unit": "steps/s", "cores": 1,
+                             "kind": "oracle",
+                             "sample": "per step: S1-S7 of one cfg2 prompt + KV reindex of 1 "
+                                       "layer of 80 (scaled)"},
+            "e2e": {"value": round(value, 4), "unit": "steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * smcsd.h -- C ABI of libsmcsd.so, the B200 (sm_100a) verification hot path of
+ * Sequential Monte Carlo Speculative Decoding (arxiv 2604.15672; PAPER.md = its LaTeX
+ * source, cited by line number).
+ *
+ * One SMC-SD round (Alg. 1) after the target forward pass:
+ *   S1/S2  score:     ell^p_j = log p(d_j | x d_<j), ell^q_j = log q(d_j | x d_<j) from logits
+ *                     (Alg. 1 "Score"; Eq. 1a)
+ *   S3     reweight:  lam'_n = lam_n + sum_{j<k_n} (alpha ell^p_j - ell^q_j)
+ *                     (Alg. 1 "Reweight"; power target PAPER.md:1418)
+ *   S4     normalise, ESS = (sum w)^2 / sum w^2   (Eq. 3)
+ *   S5-S7  if ESS < eta: draw ancestors, reset weights to 1/N
+ *   S8/S9  x^(n) <- x^(a_n): per-particle KV cache and token history reindex
+ *   S10    (tensor parallel) per-row max / sum-exp exchange across vocab shards (north star)
+ * Readings of the paper where it is silent (G1..G18) are listed in DESIGN.md section 3; the
+ * ones that shape this ABI are cited inline.
+ *
+ * Conventions (all entry points):
+ *  - Pointers are DEVICE pointers unless marked "host".  Every call only enqueues work on
+ *    `stream` (a cudaStream_t passed as void*, NULL = legacy default stream): no call
+ *    synchronises, allocates or frees.  All buffers are caller-owned.
+ *  - Layouts are row-major.  Logit row (prompt p, particle n, draft position j) of a logits
+ *    tensor starts at element  base + ((p*N + n)*rows_per_particle + j)*ld ; the first V
+ *    elements are read, and the buffer must hold  P*N*rows_per_particle*ld  elements.
+ *    Base pointers must be 16-byte aligned and ld a multiple of 16 bytes (8 bf16 / 4 fp32).
+ *  - Synchronous argument errors return SMCSD_EINVAL and enqueue nothing.  A failed launch
+ *    returns SMCSD_ECUDA.  There is no CPU fallback and no silent layout fallback.
+ *  - Data-dependent conditions cannot be returned synchronously; they are written to
+ *    status[p] (uint32 per prompt, overwritten by each call) as SMCSD_ST_* bits.  A particle
+ *    with an invalid row (bad token, non-finite row, q(d) = 0) gets lam' = -inf and the
+ *    prompt is flagged (reading G13).
+ *  - Ancestor indices are local to the prompt (0..N-1).  Philox counters use the GLOBAL
+ *    prompt index prompt_base + p, so prompt-sharded (data-parallel) runs are bit-identical
+ *    to a single-GPU run.
+ *  - The library keeps no global state.  A workspace may not be shared by concurrent calls.
+ */
+#ifndef SMCSD_H
+#define SMCSD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SMCSD_API __attribute__((visibility("default")))
+#else
+#define SMCSD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SMCSD_OK = 0,
+    SMCSD_EINVAL = 1,   /* invalid argument (synchronous; nothing enqueued)          */
+    SMCSD_ECUDA = 2,    /* a CUDA launch / runtime call failed                       */
+    SMCSD_ENOSYS = 3    /* valid request that this build does not implement          */
+} smcsd_rc;
+
+typedef enum { SMCSD_F32 = 0, SMCSD_BF16 = 1 } smcsd_dtype;
+
+/* Resampling scheme.  Systematic is the north star's choice (reading G1); the paper's
+ * multinomial draw is NEXT (returns SMCSD_ENOSYS in this build). */
+typedef enum { SMCSD_SYSTEMATIC = 0, SMCSD_MULTINOMIAL = 1 } smcsd_scheme;
+
+/* Per-prompt status bits (asynchronous, data-dependent). */
+#define SMCSD_ST_DEGENERATE  1u  /* every log-weight of the prompt is -inf           */
+#define SMCSD_ST_NOT_ABSCONT 2u  /* q(d) = 0 at a drafted token: p << q violated     */
+#define SMCSD_ST_BAD_TOKEN   4u  /* drafted token outside [0,V), or n_drafted outside [0,K]         */
+#define SMCSD_ST_NONFINITE   8u  /* NaN/+inf logit or log-weight, or a row whose max is -inf        */
+
+/* Segment length (elements) of the fixed in-row split used by every logit row (G17). */
+#define SMCSD_SEGMENT 8192
+
+/* Bytes of device workspace needed by smcsd_weights / smcsd_step / smcsd_weights_partial /
+ * smcsd_weights_combine for P prompts, N particles, K drafted tokens and v_len vocabulary
+ * columns per row (V, or the shard width for the partial call). */
+SMCSD_API size_t smcsd_workspace_bytes(int P, int N, int K, int64_t v_len);
+
+/* Zero a workspace (enqueued).  Required once after allocation: the kernels use per-prompt
+ * completion counters inside the workspace and leave them zero on exit, so a workspace
+ * stays valid across calls and CUDA-graph replays. */
+SMCSD_API smcsd_rc smcsd_workspace_init(void *workspace, size_t workspace_bytes, void *stream);
+
+/* S1-S4.
+ *  logits_p: target logits, rows_per_particle_p >= K (K+1 when the bonus row is present; the
+ *            bonus row is never read: it cancels in the weight).
+ *  logits_q: draft logits, rows_per_particle_q >= K.  dtype: SMCSD_F32 or SMCSD_BF16 (both).
+ *  tokens:   [P][N][K] int32 drafted tokens d_j (global vocabulary ids).
+ *  n_drafted:[P][N] int32 drafted length k_n in [0,K] (EOS inside a block, reading G10), or
+ *            NULL for k_n = K.  Rows j >= k_n are not read.
+ *  logw_prev:[P][N] fp32 prior log-weights lam_n, or NULL for -ln N.  May alias logw_out.
+ *  alpha:    power-target exponent (1 = plain SMC-SD), > 0.
+ *  inv_temp_p/q: inverse temperatures applied to logits before the log-softmax (G9), > 0.
+ *  Outputs (NULL allowed except logw_out and status):
+ *    logw_out [P][N] fp32 lam'_n;  logp_tok/logq_tok [P][N][K] fp32 ell (0 for j >= k_n,
+ *    NaN for invalid rows);  lse_out [P] fp64 log sum_n exp(lam'_n);  ess_out [P] fp64;
+ *    wnorm_out [P][N] fp32 normalised weights;  status [P].
+ *  Any N >= 1 is accepted (N > 1024 uses a slower serial normalisation). */
+SMCSD_API smcsd_rc smcsd_weights(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
+                       const void *logits_q, int64_t ld_q, int rows_per_particle_q,
+                       int dtype, const int32_t *tokens, const int32_t *n_drafted,
+                       const float *logw_prev, int P, int N, int K, int64_t V,
+                       float alpha, float inv_temp_p, float inv_temp_q,
+                       float *logw_out, float *logp_tok, float *logq_tok,
+                       double *lse_out, double *ess_out, float *wnorm_out, uint32_t *status,
+                       void *workspace, size_t workspace_bytes, void *stream);
+
+/* S4-S7 from fp32 log-weights, N <= 1024.
+ *  eta:       resample iff ESS < eta (strict); +INFINITY forces, 0 never.
+ *  seed/step: Philox4x32-10 key and counter high words: U = word0(Philox(key = seed,
+ *             ctr = (step_lo, step_hi, prompt_base + p, 0))) * 2^-32 (reading G5).
+ *  uniforms:  optional [P] raw 32-bit words replacing the Philox draw (tests), or NULL.
+ *  Systematic ancestors: C_m = P_m / S (fp64 sequential prefix), u_n = (n + U)/N,
+ *  a_n = #{m : C_m <= u_n}; offspring o_m; slot_src = the in-place plan (survivors keep their
+ *  slot, dead slots take the extra copies in ascending order; reading G14); n_ties counts
+ *  pairs |u_n - C_m| <= 2^-40 (reading G7).  Without a resample: identity, o = 1, lam kept.
+ *  logw_out [P][N]: fl32(-ln N) after a resample, else lam.  May alias logw.
+ *  Outputs other than ancestors, logw_out, resampled and status may be NULL. */
+SMCSD_API smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t prompt_base, float eta,
+                        int scheme, uint64_t seed, uint64_t step, const uint32_t *uniforms,
+                        int32_t *ancestors, int32_t *offspring, int32_t *slot_src,
+                        float *logw_out, uint8_t *resampled, double *ess_out, double *lse_out,
+                        float *wnorm_out, int32_t *n_ties, uint32_t *status, void *stream);
+
+/* Fused S1-S7 in one enqueue (one launch: row statistics + last-CTA-per-prompt tail), the
+ * performance path.  Arguments as smcsd_weights + smcsd_resample; N <= 1024.
+ *  logw_pre [P][N] (optional): lam' before the S7 reset -- the exact fp32 values the
+ *  resampling consumed (staged parity).  logw_out receives the S7 output. */
+SMCSD_API smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
+                    const void *logits_q, int64_t ld_q, int rows_per_particle_q,
+                    int dtype, const int32_t *tokens, const int32_t *n_drafted,
+                    const float *logw_prev, int P, int N, int K, int64_t V,
+                    float alpha, float inv_temp_p, float inv_temp_q,
+                    float eta, int scheme, uint64_t seed, uint64_t step, int64_t prompt_base,
+                    const uint32_t *uniforms,
+                    float *logw_out, float *logw_pre, float *logp_tok, float *logq_tok,
+                    double *lse_out, double *ess_out, float *wnorm_out, uint32_t *status,
+                    int32_t *ancestors, int32_t *offspring, int32_t *slot_src,
+                    uint8_t *resampled, int32_t *n_ties,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* S1 on this rank's vocabulary shard (tensor-parallel, north star).  Row pointers address
+ * only the shard: logits_* row r holds columns [v_begin, v_begin + v_len) of the full row
+ * (ld >= v_len).  tokens are GLOBAL ids.  partials: [P][2][N][K][4] fp32 per row
+ * {m, s, x, 0} in the log2 domain of the scaled logits t = inv_temp * z * log2(e):
+ *   m = max t over the shard, s = sum 2^(t - m), x = t_d if d is in the shard else -inf.
+ * Rows are ordered (prompt, model p then q, particle, position).  Rows j >= k_n hold
+ * {-inf, 0, -inf, 0}. */
+SMCSD_API smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
+                               const void *logits_q, int64_t ld_q, int rows_per_particle_q,
+                               int dtype, const int32_t *tokens, const int32_t *n_drafted,
+                               int P, int N, int K, int64_t v_begin, int64_t v_len,
+                               float inv_temp_p, float inv_temp_q, float *partials,
+                               void *workspace, size_t workspace_bytes, void *stream);
+
+/* S2-S4 after the exchange: gathered = [G][P][2][N][K][4] (the all_gather_into_tensor layout
+ * of G smcsd_weights_partial outputs in rank order).  Shards are merged in rank order, so
+ * every rank obtains bit-identical results.  V (full vocabulary) is used for the token range
+ * check.  Outputs as smcsd_weights.  workspace: smcsd_workspace_bytes(P, N, K, 1) bytes. */
+SMCSD_API smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int32_t *tokens,
+                               const int32_t *n_drafted, const float *logw_prev,
+                               int P, int N, int K, int64_t V, float alpha,
+                               float *logw_out, float *logp_tok, float *logq_tok,
+                               double *lse_out, double *ess_out, float *wnorm_out,
+                               uint32_t *status, void *workspace, size_t workspace_bytes,
+                               void *stream);
+
+/* S8/S9: reindex per-particle state blocks (dense analogue of the paged
+ * pointer copy of PAPER.md:489).  Block (o, p, n), o < n_outer (e.g. L*2 layer K/V planes),
+ * is seg_count segments of seg_bytes bytes at
+ *   base + o*outer_stride + p*prompt_stride + n*particle_stride + s*seg_stride   (bytes),
+ * e.g. the filled rows [0, seq_len) of each KV head (reading G12).
+ *  dst != src (out of place): dst block n <- src block src_index[n] for every n
+ *                             (src_index = ancestors).
+ *  dst == src (in place):     block n <- block src_index[n] where src_index[n] != n
+ *                             (src_index = slot_src; precondition: no index is both a source
+ *                             and a destination, which slot_src guarantees).
+ * Copies are bitwise (16-byte integer vectors; NaN payloads survive) and source-major: each
+ * source chunk is read once and written to all of its destinations.  seg_bytes, all strides
+ * and both base pointers must be multiples of 16; N <= 1024. */
+SMCSD_API smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_stride,
+                          int64_t prompt_stride, int64_t particle_stride, int64_t seg_count,
+                          int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index,
+                          int P, int N, void *stream);
+
+/* Human-readable name of a return code (static storage). */
+SMCSD_API const char *smcsd_strerror(smcsd_rc rc);
+
+/* Library build identifier, e.g. "smcsd 0.1 sm_100a" (static storage). */
+SMCSD_API const char *smcsd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SMCSD_H */

@@ -1,0 +1,317 @@
+"""paper_2604_15672_b200 -- B200-native verification hot path of SMC-SD (arxiv 2604.15672).
+
+Thin Python binding of ``libsmcsd.so`` (C ABI in ``include/smcsd.h``).  Every function here
+only marshals ``torch.Tensor`` arguments into pointers and sizes and calls the entry point of
+the same name; every step of the path runs in the library's sm_100a kernels.  PyTorch is used
+for device memory, streams and process groups only.  There is no CPU fallback: importing
+the package without the built library raises, and CPU tensors are rejected.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import torch
+
+__all__ = [
+    "SMCSD_F32", "SMCSD_BF16", "SMCSD_SYSTEMATIC", "SMCSD_MULTINOMIAL", "SEGMENT",
+    "ST_DEGENERATE", "ST_NOT_ABSCONT", "ST_BAD_TOKEN", "ST_NONFINITE",
+    "SmcsdError", "Workspace", "lib_path",
+    "smcsd_workspace_bytes", "smcsd_workspace_init", "smcsd_weights", "smcsd_step",
+    "smcsd_resample", "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
+    "smcsd_version", "kv_geometry",
+]
+
+SMCSD_F32, SMCSD_BF16 = 0, 1
+SMCSD_SYSTEMATIC, SMCSD_MULTINOMIAL = 0, 1
+SEGMENT = 8192
+ST_DEGENERATE, ST_NOT_ABSCONT, ST_BAD_TOKEN, ST_NONFINITE = 1, 2, 4, 8
+_RC = {0: "ok", 1: "invalid argument", 2: "CUDA launch or runtime error", 3: "not implemented"}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libsmcsd.so")
+
+
+class SmcsdError(RuntimeError):
+    def __init__(self, name, rc):
+        super().__init__(f"{name} failed: rc={rc} ({_RC.get(rc, 'unknown')})")
+        self.rc = rc
+
+
+def _load():
+    if not os.path.exists(lib_path):
+        raise ImportError(f"{lib_path} is missing: run `python -m paper_2604_15672_b200.build` "
+                          "(or __graft_entry__.build()) -- there is no fallback path")
+    L = ctypes.CDLL(lib_path)
+    vp, i32, i64, f32, u64, sz = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float,
+                                  ctypes.c_uint64, ctypes.c_size_t)
+    L.smcsd_workspace_bytes.argtypes = [i32, i32, i32, i64]
+    L.smcsd_workspace_bytes.restype = sz
+    L.smcsd_workspace_init.argtypes = [vp, sz, vp]
+    L.smcsd_weights.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp, i32, i32, i32, i64,
+                                f32, f32, f32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.smcsd_resample.argtypes = [vp, i32, i32, i64, f32, i32, u64, u64, vp, vp, vp, vp, vp, vp,
+                                 vp, vp, vp, vp, vp, vp]
+    L.smcsd_step.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp, i32, i32, i32, i64,
+                             f32, f32, f32, f32, i32, u64, u64, i64, vp,
+                             vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.smcsd_weights_partial.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, i32, i32, i32,
+                                        i64, i64, f32, f32, vp, vp, sz, vp]
+    L.smcsd_weights_combine.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i64, f32, vp, vp, vp,
+                                        vp, vp, vp, vp, vp, sz, vp]
+    L.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
+    for name in ("smcsd_workspace_init", "smcsd_weights", "smcsd_resample", "smcsd_step",
+                 "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex"):
+        getattr(L, name).restype = i32
+    L.smcsd_version.restype = ctypes.c_char_p
+    L.smcsd_strerror.restype = ctypes.c_char_p
+    L.smcsd_strerror.argtypes = [i32]
+    return L
+
+
+_lib = _load()
+
+
+def _check(name, rc):
+    if rc != 0:
+        raise SmcsdError(name, rc)
+
+
+def _p(t):
+    """Device pointer of a CUDA tensor (None -> NULL).  CPU tensors are rejected."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libsmcsd takes device tensors only (no CPU fallback)")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream
+
+
+def _dtype_code(t):
+    if t.dtype == torch.bfloat16:
+        return SMCSD_BF16
+    if t.dtype == torch.float32:
+        return SMCSD_F32
+    raise TypeError(f"logits must be bfloat16 or float32, got {t.dtype}")
+
+
+def _logits_geom(t, name):
+    if t.dim() != 4:
+        raise ValueError(f"{name} must be [P][N][rows_per_particle][ld]")
+    if t.stride(3) != 1 or t.stride(2) != t.shape[3] or t.stride(1) != t.shape[2] * t.shape[3] \
+            or t.stride(0) != t.shape[1] * t.shape[2] * t.shape[3]:
+        raise ValueError(f"{name} must be contiguous (row pitch = last dim)")
+    return t.shape[3], t.shape[2]
+
+
+def _empty(shape, dtype, device):
+    return torch.empty(shape, dtype=dtype, device=device)
+
+
+def smcsd_version() -> str:
+    return _lib.smcsd_version().decode()
+
+
+def smcsd_workspace_bytes(P: int, N: int, K: int, v_len: int) -> int:
+    return int(_lib.smcsd_workspace_bytes(P, N, K, v_len))
+
+
+def smcsd_workspace_init(ws: torch.Tensor, stream=None):
+    _check("smcsd_workspace_init", _lib.smcsd_workspace_init(_p(ws), ws.numel(), _stream(stream)))
+
+
+class Workspace:
+    """A zero-initialised device workspace that grows on demand (plumbing only)."""
+
+    def __init__(self, device=None):
+        self.device = torch.device("cuda" if device is None else device)
+        self.buf = None
+
+    def get(self, P, N, K, v_len, stream=None):
+        need = smcsd_workspace_bytes(P, N, K, v_len)
+        if self.buf is None or self.buf.numel() < need:
+            self.buf = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+            smcsd_workspace_init(self.buf, stream)
+        return self.buf
+
+
+_default_ws = {}
+
+
+def _ws(ws, device, P, N, K, v_len, stream):
+    if ws is None:
+        key = (device.type, device.index)
+        ws = _default_ws.setdefault(key, Workspace(device))
+    if isinstance(ws, Workspace):
+        return ws.get(P, N, K, v_len, stream)
+    return ws
+
+
+@dataclass
+class Outputs:
+    logw: torch.Tensor = None
+    logw_pre: torch.Tensor = None
+    logp_tok: torch.Tensor = None
+    logq_tok: torch.Tensor = None
+    lse: torch.Tensor = None
+    ess: torch.Tensor = None
+    wnorm: torch.Tensor = None
+    status: torch.Tensor = None
+    ancestors: torch.Tensor = None
+    offspring: torch.Tensor = None
+    slot_src: torch.Tensor = None
+    resampled: torch.Tensor = None
+    n_ties: torch.Tensor = None
+    partials: torch.Tensor = None
+
+
+def _alloc(out: Outputs, dev, P, N, K, fields):
+    shapes = dict(logw=((P, N), torch.float32), logw_pre=((P, N), torch.float32),
+                  logp_tok=((P, N, K), torch.float32), logq_tok=((P, N, K), torch.float32),
+                  lse=((P,), torch.float64), ess=((P,), torch.float64),
+                  wnorm=((P, N), torch.float32), status=((P,), torch.int32),
+                  ancestors=((P, N), torch.int32), offspring=((P, N), torch.int32),
+                  slot_src=((P, N), torch.int32), resampled=((P,), torch.uint8),
+                  n_ties=((P,), torch.int32))
+    for f in fields:
+        if getattr(out, f) is None:
+            shp, dt = shapes[f]
+            setattr(out, f, _empty(shp, dt, dev))
+    return out
+
+
+_ALL_W = ("logw", "logp_tok", "logq_tok", "lse", "ess", "wnorm", "status")
+_ALL_S = _ALL_W + ("logw_pre", "ancestors", "offspring", "slot_src", "resampled", "n_ties")
+
+
+def smcsd_weights(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=None,
+                  alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, out: Outputs | None = None,
+                  fields=_ALL_W, workspace=None, stream=None) -> Outputs:
+    """S1-S4.  logits_*: [P][N][rows][ld] bf16/fp32 CUDA tensors; tokens [P][N][K] int32."""
+    ld_p, rpp_p = _logits_geom(logits_p, "logits_p")
+    ld_q, rpp_q = _logits_geom(logits_q, "logits_q")
+    if logits_p.dtype != logits_q.dtype:
+        raise TypeError("logits_p and logits_q must share a dtype")
+    P, N, K = tokens.shape
+    V = ld_p if V is None else V
+    dev = logits_p.device
+    out = _alloc(out or Outputs(), dev, P, N, K, ("logw", "status") + tuple(fields))
+    ws = _ws(workspace, dev, P, N, K, V, stream)
+    rc = _lib.smcsd_weights(_p(logits_p), ld_p, rpp_p, _p(logits_q), ld_q, rpp_q,
+                            _dtype_code(logits_p), _p(tokens), _p(n_drafted), _p(logw_prev),
+                            P, N, K, V, alpha, inv_temp_p, inv_temp_q, _p(out.logw),
+                            _p(out.logp_tok), _p(out.logq_tok), _p(out.lse), _p(out.ess),
+                            _p(out.wnorm), _p(out.status), _p(ws), ws.numel(), _stream(stream))
+    _check("smcsd_weights", rc)
+    return out
+
+
+def smcsd_step(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=None,
+               alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, eta=math.inf,
+               scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
+               out: Outputs | None = None, fields=_ALL_S, workspace=None,
+               stream=None) -> Outputs:
+    """Fused S1-S7 (one launch)."""
+    ld_p, rpp_p = _logits_geom(logits_p, "logits_p")
+    ld_q, rpp_q = _logits_geom(logits_q, "logits_q")
+    if logits_p.dtype != logits_q.dtype:
+        raise TypeError("logits_p and logits_q must share a dtype")
+    P, N, K = tokens.shape
+    V = ld_p if V is None else V
+    dev = logits_p.device
+    out = _alloc(out or Outputs(), dev, P, N, K,
+                 ("logw", "status", "ancestors", "resampled") + tuple(fields))
+    ws = _ws(workspace, dev, P, N, K, V, stream)
+    rc = _lib.smcsd_step(_p(logits_p), ld_p, rpp_p, _p(logits_q), ld_q, rpp_q,
+                         _dtype_code(logits_p), _p(tokens), _p(n_drafted), _p(logw_prev),
+                         P, N, K, V, alpha, inv_temp_p, inv_temp_q, eta, scheme,
+                         seed & (2 ** 64 - 1), step & (2 ** 64 - 1), prompt_base, _p(uniforms),
+                         _p(out.logw), _p(out.logw_pre), _p(out.logp_tok), _p(out.logq_tok),
+                         _p(out.lse), _p(out.ess), _p(out.wnorm), _p(out.status),
+                         _p(out.ancestors), _p(out.offspring), _p(out.slot_src),
+                         _p(out.resampled), _p(out.n_ties), _p(ws), ws.numel(), _stream(stream))
+    _check("smcsd_step", rc)
+    return out
+
+
+def smcsd_resample(logw, *, eta=math.inf, scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0,
+                   prompt_base=0, uniforms=None, out: Outputs | None = None,
+                   fields=("offspring", "slot_src", "ess", "lse", "wnorm", "n_ties"),
+                   stream=None) -> Outputs:
+    """S4-S7 from fp32 log-weights [P][N]."""
+    P, N = logw.shape
+    out = _alloc(out or Outputs(), logw.device, P, N, 1,
+                 ("ancestors", "logw", "resampled", "status") + tuple(fields))
+    rc = _lib.smcsd_resample(_p(logw), P, N, prompt_base, eta, scheme, seed & (2 ** 64 - 1),
+                             step & (2 ** 64 - 1), _p(uniforms), _p(out.ancestors),
+                             _p(out.offspring), _p(out.slot_src), _p(out.logw), _p(out.resampled),
+                             _p(out.ess), _p(out.lse), _p(out.wnorm), _p(out.n_ties),
+                             _p(out.status), _stream(stream))
+    _check("smcsd_resample", rc)
+    return out
+
+
+def smcsd_weights_partial(logits_p, logits_q, tokens, *, v_begin, v_len=None, n_drafted=None,
+                          inv_temp_p=1.0, inv_temp_q=1.0, partials=None, workspace=None,
+                          stream=None) -> torch.Tensor:
+    """S1 on a vocab shard: rows of logits_* hold columns [v_begin, v_begin + v_len)
+    (v_len defaults to the row pitch).  Returns partials [P][2][N][K][4] (log2 domain)."""
+    ld_p, rpp_p = _logits_geom(logits_p, "logits_p")
+    ld_q, rpp_q = _logits_geom(logits_q, "logits_q")
+    P, N, K = tokens.shape
+    v_len = ld_p if v_len is None else v_len
+    dev = logits_p.device
+    if partials is None:
+        partials = _empty((P, 2, N, K, 4), torch.float32, dev)
+    ws = _ws(workspace, dev, P, N, K, v_len, stream)
+    rc = _lib.smcsd_weights_partial(_p(logits_p), ld_p, rpp_p, _p(logits_q), ld_q, rpp_q,
+                                    _dtype_code(logits_p), _p(tokens), _p(n_drafted), P, N, K,
+                                    v_begin, v_len, inv_temp_p, inv_temp_q, _p(partials), _p(ws),
+                                    ws.numel(), _stream(stream))
+    _check("smcsd_weights_partial", rc)
+    return partials
+
+
+def smcsd_weights_combine(gathered, tokens, *, V, n_drafted=None, logw_prev=None, alpha=1.0,
+                          out: Outputs | None = None, fields=_ALL_W, workspace=None,
+                          stream=None) -> Outputs:
+    """S2-S4 from G gathered shard partials [G][P][2][N][K][4] (rank order)."""
+    G = gathered.shape[0]
+    P, N, K = tokens.shape
+    dev = gathered.device
+    out = _alloc(out or Outputs(), dev, P, N, K, ("logw", "status") + tuple(fields))
+    ws = _ws(workspace, dev, P, N, K, 1, stream)
+    rc = _lib.smcsd_weights_combine(_p(gathered), G, _p(tokens), _p(n_drafted), _p(logw_prev),
+                                    P, N, K, V, alpha, _p(out.logw), _p(out.logp_tok),
+                                    _p(out.logq_tok), _p(out.lse), _p(out.ess), _p(out.wnorm),
+                                    _p(out.status), _p(ws), ws.numel(), _stream(stream))
+    _check("smcsd_weights_combine", rc)
+    return out
+
+
+def kv_geometry(kv: torch.Tensor, seq_len: int | None = None) -> dict:
+    """Strides for a dense KV cache laid out [L][2][P][N][H][S][d] (any element type)."""
+    if kv.dim() != 7 or not kv.is_contiguous():
+        raise ValueError("kv must be a contiguous [L][2][P][N][H][S][d] tensor")
+    L, C, P, N, H, S, d = kv.shape
+    e = kv.element_size()
+    seq_len = S if seq_len is None else seq_len
+    return dict(n_outer=L * C, outer_stride=P * N * H * S * d * e, prompt_stride=N * H * S * d * e,
+                particle_stride=H * S * d * e, seg_count=H, seg_bytes=seq_len * d * e,
+                seg_stride=S * d * e)
+
+
+def smcsd_kv_reindex(dst, src, src_index, *, n_outer, outer_stride, prompt_stride,
+                     particle_stride, seg_count, seg_bytes, seg_stride, stream=None):
+    """S8/S9 block gather; pass dst is src for the in-place slot plan."""
+    P, N = src_index.shape
+    rc = _lib.smcsd_kv_reindex(_p(dst), _p(src), n_outer, outer_stride, prompt_stride,
+                               particle_stride, seg_count, seg_bytes, seg_stride, _p(src_index),
+                               P, N, _stream(stream))
+    _check("smcsd_kv_reindex", rc)

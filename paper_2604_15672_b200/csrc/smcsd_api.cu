@@ -1,0 +1,299 @@
+// smcsd_api.cu -- extern "C" entry points of libsmcsd.so (declared in include/smcsd.h):
+// synchronous argument validation, workspace carve-up, launch configuration.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <cuda_runtime.h>
+
+#include "smcsd.h"
+#include "smcsd_kernels.cuh"
+
+using namespace smcsd;
+
+namespace {
+
+constexpr double kLog2e = 1.442695040888963407359924681001892137;
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+struct WsLayout {
+    size_t counters, parts, ell, lam, e, c, total;
+};
+
+WsLayout ws_layout(int P, int N, int K, int64_t v_len) {
+    WsLayout L{};
+    const size_t rows = 2ull * (size_t)P * (size_t)N * (size_t)K;
+    const size_t nseg = (size_t)cdiv(v_len < 1 ? 1 : v_len, kSeg);
+    size_t off = 0;
+    L.counters = off; off += align256((size_t)P * sizeof(unsigned));
+    L.parts = off;    off += align256(rows * nseg * sizeof(float4));
+    L.ell = off;      off += align256(rows * sizeof(double));
+    L.lam = off;      off += align256((size_t)P * N * sizeof(float));
+    L.e = off;        off += align256((size_t)P * N * sizeof(double));
+    L.c = off;        off += align256((size_t)P * N * sizeof(double));
+    L.total = off;
+    return L;
+}
+
+void bind_workspace(Params &prm, void *ws, const WsLayout &L) {
+    char *b = static_cast<char *>(ws);
+    prm.counters = reinterpret_cast<unsigned *>(b + L.counters);
+    prm.part_ws = reinterpret_cast<float4 *>(b + L.parts);
+    prm.ell_ws = reinterpret_cast<double *>(b + L.ell);
+    prm.lam_ws = reinterpret_cast<float *>(b + L.lam);
+    prm.e_ws = reinterpret_cast<double *>(b + L.e);
+    prm.c_ws = reinterpret_cast<double *>(b + L.c);
+}
+
+bool valid_temp(float t) { return std::isfinite(t) && t > 0.0f; }
+
+// Validation shared by weights / step / partial.  Returns SMCSD_OK or SMCSD_EINVAL.
+smcsd_rc check_logits(const void *lp, int64_t ld_p, int rpp_p, const void *lq, int64_t ld_q,
+                      int rpp_q, int dtype, const int32_t *tokens, int P, int N, int K,
+                      int64_t v_len) {
+    if (!lp || !lq || !tokens) return SMCSD_EINVAL;
+    if (P < 1 || N < 1 || K < 1 || v_len < 1) return SMCSD_EINVAL;
+    if (dtype != SMCSD_F32 && dtype != SMCSD_BF16) return SMCSD_EINVAL;
+    const int64_t vec = dtype == SMCSD_BF16 ? 8 : 4;
+    if (ld_p < v_len || ld_q < v_len || ld_p % vec || ld_q % vec) return SMCSD_EINVAL;
+    if (rpp_p < K || rpp_q < K) return SMCSD_EINVAL;
+    if (!aligned16(lp) || !aligned16(lq)) return SMCSD_EINVAL;
+    const int64_t items = 2ll * P * N * K * cdiv(v_len, kSeg);
+    if (items >= (1ll << 31)) return SMCSD_EINVAL;
+    return SMCSD_OK;
+}
+
+smcsd_rc launched() { return cudaGetLastError() == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA; }
+
+template <int MODE>
+void launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st) {
+    if (dtype == SMCSD_BF16) k_rowstats<1, MODE><<<(unsigned)items, kThreads, 0, st>>>(prm);
+    else                     k_rowstats<0, MODE><<<(unsigned)items, kThreads, 0, st>>>(prm);
+}
+
+// Common Params for the logits entry points.
+Params logits_params(const void *lp, int64_t ld_p, int rpp_p, const void *lq, int64_t ld_q,
+                     int rpp_q, const int32_t *tokens, const int32_t *n_drafted, int P, int N,
+                     int K, int64_t V, int64_t v_begin, int64_t v_len, float tp, float tq) {
+    Params prm;
+    std::memset(&prm, 0, sizeof prm);
+    prm.lp = static_cast<const char *>(lp); prm.ld_p = ld_p; prm.rpp_p = rpp_p;
+    prm.lq = static_cast<const char *>(lq); prm.ld_q = ld_q; prm.rpp_q = rpp_q;
+    prm.tokens = tokens; prm.n_drafted = n_drafted;
+    prm.P = P; prm.N = N; prm.K = K; prm.V = V;
+    prm.v_begin = v_begin; prm.v_len = v_len;
+    prm.nseg = (int)cdiv(v_len, kSeg);
+    prm.c_p = (float)((double)tp * kLog2e);
+    prm.c_q = (float)((double)tq * kLog2e);
+    prm.alpha = 1.0;
+    return prm;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t smcsd_workspace_bytes(int P, int N, int K, int64_t v_len) {
+    if (P < 1 || N < 1 || K < 1) return 0;
+    return ws_layout(P, N, K, v_len).total;
+}
+
+smcsd_rc smcsd_workspace_init(void *workspace, size_t workspace_bytes, void *stream) {
+    if (!workspace) return SMCSD_EINVAL;
+    return cudaMemsetAsync(workspace, 0, workspace_bytes, as_stream(stream)) == cudaSuccess
+               ? SMCSD_OK : SMCSD_ECUDA;
+}
+
+smcsd_rc smcsd_weights(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
+                       const void *logits_q, int64_t ld_q, int rows_per_particle_q, int dtype,
+                       const int32_t *tokens, const int32_t *n_drafted, const float *logw_prev,
+                       int P, int N, int K, int64_t V, float alpha, float inv_temp_p,
+                       float inv_temp_q, float *logw_out, float *logp_tok, float *logq_tok,
+                       double *lse_out, double *ess_out, float *wnorm_out, uint32_t *status,
+                       void *workspace, size_t workspace_bytes, void *stream) {
+    smcsd_rc rc = check_logits(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
+                               rows_per_particle_q, dtype, tokens, P, N, K, V);
+    if (rc != SMCSD_OK) return rc;
+    if (!logw_out || !status || !workspace) return SMCSD_EINVAL;
+    if (!(std::isfinite(alpha) && alpha > 0.0f) || !valid_temp(inv_temp_p) || !valid_temp(inv_temp_q))
+        return SMCSD_EINVAL;
+    const WsLayout L = ws_layout(P, N, K, V);
+    if (workspace_bytes < L.total || !aligned16(workspace)) return SMCSD_EINVAL;
+    Params prm = logits_params(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
+                               rows_per_particle_q, tokens, n_drafted, P, N, K, V, 0, V,
+                               inv_temp_p, inv_temp_q);
+    prm.alpha = (double)alpha;
+    prm.logw_prev = logw_prev;
+    prm.logw_out = logw_out; prm.logp_tok = logp_tok; prm.logq_tok = logq_tok;
+    prm.lse = lse_out; prm.ess = ess_out; prm.wnorm = wnorm_out; prm.status = status;
+    bind_workspace(prm, workspace, L);
+    prm.parts = prm.part_ws; prm.part_row_stride = prm.nseg; prm.part_seg_stride = 1;
+    prm.nparts = prm.nseg;
+    const int64_t items = 2ll * P * N * K * prm.nseg;
+    cudaStream_t st = as_stream(stream);
+    if (N <= kTailMaxN) {
+        launch_rowstats<MODE_WEIGHTS>(prm, dtype, items, st);
+    } else {
+        launch_rowstats<MODE_ROWS_ONLY>(prm, dtype, items, st);
+        if (launched() != SMCSD_OK) return SMCSD_ECUDA;
+        k_tail_large<<<P, kThreads, 0, st>>>(prm);
+    }
+    return launched();
+}
+
+smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t prompt_base, float eta,
+                        int scheme, uint64_t seed, uint64_t step, const uint32_t *uniforms,
+                        int32_t *ancestors, int32_t *offspring, int32_t *slot_src,
+                        float *logw_out, uint8_t *resampled, double *ess_out, double *lse_out,
+                        float *wnorm_out, int32_t *n_ties, uint32_t *status, void *stream) {
+    if (!logw || !ancestors || !logw_out || !resampled || !status) return SMCSD_EINVAL;
+    if (P < 1 || N < 1 || N > kTailMaxN || std::isnan(eta)) return SMCSD_EINVAL;
+    if (scheme == SMCSD_MULTINOMIAL) return SMCSD_ENOSYS;
+    if (scheme != SMCSD_SYSTEMATIC) return SMCSD_EINVAL;
+    Params prm;
+    std::memset(&prm, 0, sizeof prm);
+    prm.P = P; prm.N = N;
+    prm.logw_prev = logw;
+    prm.eta = (double)eta; prm.seed = seed; prm.step = step; prm.prompt_base = prompt_base;
+    prm.uniforms = uniforms;
+    prm.ancestors = ancestors; prm.offspring = offspring; prm.slot_src = slot_src;
+    prm.logw_out = logw_out; prm.resampled = resampled; prm.ess = ess_out; prm.lse = lse_out;
+    prm.wnorm = wnorm_out; prm.n_ties = n_ties; prm.status = status;
+    k_resample<<<P, kThreads, 0, as_stream(stream)>>>(prm);
+    return launched();
+}
+
+smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
+                    const void *logits_q, int64_t ld_q, int rows_per_particle_q, int dtype,
+                    const int32_t *tokens, const int32_t *n_drafted, const float *logw_prev,
+                    int P, int N, int K, int64_t V, float alpha, float inv_temp_p,
+                    float inv_temp_q, float eta, int scheme, uint64_t seed, uint64_t step,
+                    int64_t prompt_base, const uint32_t *uniforms, float *logw_out,
+                    float *logw_pre, float *logp_tok, float *logq_tok, double *lse_out,
+                    double *ess_out, float *wnorm_out, uint32_t *status, int32_t *ancestors,
+                    int32_t *offspring, int32_t *slot_src, uint8_t *resampled, int32_t *n_ties,
+                    void *workspace, size_t workspace_bytes, void *stream) {
+    smcsd_rc rc = check_logits(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
+                               rows_per_particle_q, dtype, tokens, P, N, K, V);
+    if (rc != SMCSD_OK) return rc;
+    if (!logw_out || !status || !ancestors || !resampled || !workspace) return SMCSD_EINVAL;
+    if (N > kTailMaxN || std::isnan(eta)) return SMCSD_EINVAL;
+    if (!(std::isfinite(alpha) && alpha > 0.0f) || !valid_temp(inv_temp_p) || !valid_temp(inv_temp_q))
+        return SMCSD_EINVAL;
+    if (scheme == SMCSD_MULTINOMIAL) return SMCSD_ENOSYS;
+    if (scheme != SMCSD_SYSTEMATIC) return SMCSD_EINVAL;
+    const WsLayout L = ws_layout(P, N, K, V);
+    if (workspace_bytes < L.total || !aligned16(workspace)) return SMCSD_EINVAL;
+    // logw_prev may alias logw_out: the tail reads lam_prev[n] before any S7 write.
+    Params prm = logits_params(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
+                               rows_per_particle_q, tokens, n_drafted, P, N, K, V, 0, V,
+                               inv_temp_p, inv_temp_q);
+    prm.alpha = (double)alpha;
+    prm.logw_prev = logw_prev;
+    prm.eta = (double)eta; prm.seed = seed; prm.step = step; prm.prompt_base = prompt_base;
+    prm.uniforms = uniforms;
+    prm.logw_out = logw_out; prm.logw_pre = logw_pre; prm.logp_tok = logp_tok;
+    prm.logq_tok = logq_tok; prm.lse = lse_out; prm.ess = ess_out; prm.wnorm = wnorm_out;
+    prm.status = status; prm.ancestors = ancestors; prm.offspring = offspring;
+    prm.slot_src = slot_src; prm.resampled = resampled; prm.n_ties = n_ties;
+    bind_workspace(prm, workspace, L);
+    prm.parts = prm.part_ws; prm.part_row_stride = prm.nseg; prm.part_seg_stride = 1;
+    prm.nparts = prm.nseg;
+    launch_rowstats<MODE_STEP>(prm, dtype, 2ll * P * N * K * prm.nseg, as_stream(stream));
+    return launched();
+}
+
+smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
+                               const void *logits_q, int64_t ld_q, int rows_per_particle_q,
+                               int dtype, const int32_t *tokens, const int32_t *n_drafted,
+                               int P, int N, int K, int64_t v_begin, int64_t v_len,
+                               float inv_temp_p, float inv_temp_q, float *partials,
+                               void *workspace, size_t workspace_bytes, void *stream) {
+    smcsd_rc rc = check_logits(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
+                               rows_per_particle_q, dtype, tokens, P, N, K, v_len);
+    if (rc != SMCSD_OK) return rc;
+    if (!partials || !workspace || v_begin < 0 || !aligned16(partials)) return SMCSD_EINVAL;
+    if (!valid_temp(inv_temp_p) || !valid_temp(inv_temp_q)) return SMCSD_EINVAL;
+    const WsLayout L = ws_layout(P, N, K, v_len);
+    if (workspace_bytes < L.total || !aligned16(workspace)) return SMCSD_EINVAL;
+    Params prm = logits_params(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
+                               rows_per_particle_q, tokens, n_drafted, P, N, K,
+                               v_begin + v_len, v_begin, v_len, inv_temp_p, inv_temp_q);
+    prm.partials_out = reinterpret_cast<float4 *>(partials);
+    bind_workspace(prm, workspace, L);
+    launch_rowstats<MODE_PARTIAL>(prm, dtype, 2ll * P * N * K * prm.nseg, as_stream(stream));
+    return launched();
+}
+
+smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int32_t *tokens,
+                               const int32_t *n_drafted, const float *logw_prev, int P, int N,
+                               int K, int64_t V, float alpha, float *logw_out, float *logp_tok,
+                               float *logq_tok, double *lse_out, double *ess_out,
+                               float *wnorm_out, uint32_t *status, void *workspace,
+                               size_t workspace_bytes, void *stream) {
+    if (!gathered || !tokens || !logw_out || !status || !workspace) return SMCSD_EINVAL;
+    if (G < 1 || P < 1 || N < 1 || K < 1 || V < 1 || N > kTailMaxN) return SMCSD_EINVAL;
+    if (!(std::isfinite(alpha) && alpha > 0.0f) || !aligned16(gathered)) return SMCSD_EINVAL;
+    const WsLayout L = ws_layout(P, N, K, 1);
+    if (workspace_bytes < L.total || !aligned16(workspace)) return SMCSD_EINVAL;
+    Params prm;
+    std::memset(&prm, 0, sizeof prm);
+    prm.tokens = tokens; prm.n_drafted = n_drafted; prm.logw_prev = logw_prev;
+    prm.P = P; prm.N = N; prm.K = K; prm.V = V; prm.alpha = (double)alpha;
+    prm.logw_out = logw_out; prm.logp_tok = logp_tok; prm.logq_tok = logq_tok;
+    prm.lse = lse_out; prm.ess = ess_out; prm.wnorm = wnorm_out; prm.status = status;
+    bind_workspace(prm, workspace, L);
+    prm.parts = reinterpret_cast<const float4 *>(gathered);
+    prm.part_row_stride = 1;
+    prm.part_seg_stride = 2ll * P * N * K;
+    prm.nparts = G;
+    k_tail<<<P, kThreads, 0, as_stream(stream)>>>(prm, 0);
+    return launched();
+}
+
+smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_stride,
+                          int64_t prompt_stride, int64_t particle_stride, int64_t seg_count,
+                          int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index,
+                          int P, int N, void *stream) {
+    if (!dst || !src || !src_index) return SMCSD_EINVAL;
+    if (P < 1 || N < 1 || N > kTailMaxN || n_outer < 1 || seg_count < 1 || seg_bytes < 16)
+        return SMCSD_EINVAL;
+    if (!aligned16(dst) || !aligned16(src)) return SMCSD_EINVAL;
+    if ((seg_bytes | outer_stride | prompt_stride | particle_stride | seg_stride) & 15)
+        return SMCSD_EINVAL;
+    if (outer_stride < 0 || prompt_stride < 0 || particle_stride < 0 || seg_stride < 0)
+        return SMCSD_EINVAL;
+    const uint64_t vps = (uint64_t)seg_bytes / 16;
+    if (vps >= (1ull << 32)) return SMCSD_EINVAL;
+    KvParams prm;
+    prm.dst = static_cast<char *>(dst);
+    prm.src = static_cast<const char *>(src);
+    prm.outer_stride = outer_stride; prm.prompt_stride = prompt_stride;
+    prm.particle_stride = particle_stride; prm.seg_stride = seg_stride;
+    prm.vps = (uint32_t)vps;
+    prm.vecs = (uint64_t)seg_count * vps;
+    prm.nchunks = (int64_t)cdiv((int64_t)prm.vecs, kKvChunkVec);
+    prm.idx = src_index; prm.P = P; prm.N = N; prm.in_place = dst == src;
+    const int64_t items = n_outer * P * prm.nchunks;
+    if (items >= (1ll << 31)) return SMCSD_EINVAL;
+    k_kv_reindex<<<(unsigned)items, kThreads, 0, as_stream(stream)>>>(prm);
+    return launched();
+}
+
+const char *smcsd_strerror(smcsd_rc rc) {
+    switch (rc) {
+        case SMCSD_OK: return "ok";
+        case SMCSD_EINVAL: return "invalid argument";
+        case SMCSD_ECUDA: return "CUDA launch or runtime error";
+        case SMCSD_ENOSYS: return "not implemented in this build";
+    }
+    return "unknown smcsd_rc";
+}
+
+const char *smcsd_version(void) { return "smcsd 0.1 sm_100a"; }
+
+}  // extern "C"

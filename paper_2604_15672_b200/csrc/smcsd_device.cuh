@@ -1,0 +1,97 @@
+// smcsd_device.cuh -- device helpers for libsmcsd (sm_100a).  No host code, no torch.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace smcsd {
+
+constexpr int kThreads = 256;            // CTA size of every kernel in the library
+constexpr int kWarps = kThreads / 32;
+constexpr int kSeg = 8192;               // SMCSD_SEGMENT: fixed in-row segment (G17)
+constexpr int kTailMaxN = 1024;          // fused tail / resample keep per-prompt state in smem
+
+// ---- scalars -------------------------------------------------------------------------
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// Streaming 16-byte load: read-only path, no L1 allocation (each logit byte is read once).
+__device__ __forceinline__ uint4 ld_stream(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_stream(void *p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Butterfly sum: every lane ends with the same bits (x+y == y+x at each level).
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ---- Philox4x32-10 (Salmon et al. SC'11), own implementation (reading G5) ---------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint2 key) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) {
+            key.x += 0x9E3779B9u;
+            key.y += 0xBB67AE85u;
+        }
+        const uint32_t lo0 = 0xD2511F53u * ctr.x, hi0 = __umulhi(0xD2511F53u, ctr.x);
+        const uint32_t lo1 = 0xCD9E8D57u * ctr.z, hi1 = __umulhi(0xCD9E8D57u, ctr.z);
+        ctr = make_uint4(hi1 ^ ctr.y ^ key.x, lo1, hi0 ^ ctr.w ^ key.y, lo0);
+    }
+    return ctr;
+}
+
+// ---- block-wide exclusive scan of int over n <= kTailMaxN entries held in smem -------------
+// Returns the total.  All threads of the CTA must call it.  `wtot` is kWarps+1 ints of smem.
+__device__ __forceinline__ int block_exclusive_scan(int *data, int n, int *wtot) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int carry = 0;
+    for (int base = 0; base < n; base += kThreads) {
+        const int i = base + tid;
+        const int v = i < n ? data[i] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wtot[warp] = x;
+        __syncthreads();
+        if (tid == 0) {
+            int acc = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                const int t = wtot[w];
+                wtot[w] = acc;
+                acc += t;
+            }
+            wtot[kWarps] = acc;
+        }
+        __syncthreads();
+        if (i < n) data[i] = carry + wtot[warp] + x - v;
+        carry += wtot[kWarps];
+        __syncthreads();
+    }
+    return carry;
+}
+
+}  // namespace smcsd

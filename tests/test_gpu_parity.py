@@ -1,0 +1,356 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Bars (north star): log-weights within 1e-4 absolute; ancestors,
+offspring, slot plans, resampled flags, reset values and KV bytes bit-exact (ties flagged);
+ESS / lse within 1e-12 relative when both sides start from the same fp32 log-weights."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from gpu_util import max_abs, np_, to_host
+
+pytestmark = pytest.mark.gpu
+
+TOL_LOGW = 1e-4          # north star: log-weights within 1e-4 absolute
+TOL_ELL = 2e-5           # per-row log-prob (fp32 kernel vs fp64 oracle)
+
+
+@pytest.fixture(scope="module")
+def smc():
+    import paper_2604_15672_b200 as m          # raises if libsmcsd.so is missing (no fallback)
+    assert torch.cuda.is_available()
+    return m
+
+
+def _run_weights(smc, orc, lp, lq, tok, V, **kw):
+    dev = torch.device("cuda")
+    g = dict(n_drafted=kw.get("n_drafted"), logw_prev=kw.get("logw_prev"))
+    gpu = smc.smcsd_weights(lp.to(dev), lq.to(dev), tok.to(dev), V=V,
+                            n_drafted=None if g["n_drafted"] is None else g["n_drafted"].to(dev),
+                            logw_prev=None if g["logw_prev"] is None else g["logw_prev"].to(dev),
+                            alpha=kw.get("alpha", 1.0), inv_temp_p=kw.get("tp", 1.0),
+                            inv_temp_q=kw.get("tq", 1.0))
+    torch.cuda.synchronize()
+    ref = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, n_drafted=np_(g["n_drafted"]),
+                      logw_prev=np_(g["logw_prev"]), alpha=kw.get("alpha", 1.0),
+                      tau_p=kw.get("tp", 1.0), tau_q=kw.get("tq", 1.0))
+    return gpu, ref
+
+
+CASES = [
+    # (P, N, K, V, dtype, sigma_d)       -- tiles: 8192-element segments; ragged tails
+    (1, 4, 4, 1000, torch.float32, 0.5),          # cfg1 tiny
+    (1, 16, 8, 128256, torch.bfloat16, 0.5),      # cfg2 (full size, every row checked)
+    (3, 5, 3, 8192, torch.bfloat16, 0.5),         # exactly one segment
+    (2, 3, 2, 8193, torch.float32, 1.5),          # one element into a second segment
+    (2, 7, 5, 20001, torch.bfloat16, 1.5),        # odd V (bf16 vector straddles V)
+    (1, 1, 1, 3, torch.float32, 0.5),             # V < one vector, N = 1, K = 1
+    (2, 33, 2, 50000, torch.float32, 0.5),        # N not a multiple of 32
+]
+
+
+@pytest.mark.parametrize("P,N,K,V,dtype,sd", CASES)
+def test_weights_parity(smc, orc, P, N, K, V, dtype, sd):
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=dtype, sigma_d=sd, seed=1000 + V + N)
+    prev = synth.random_logw(P, N, seed=7, sigma=0.5)
+    gpu, ref = _run_weights(smc, orc, lp, lq, tok, V, logw_prev=prev)
+    assert np.array_equal(np_(gpu.status).astype(np.uint32), ref["status"])
+    assert max_abs(np_(gpu.logp_tok), ref["logp_tok"]) <= TOL_ELL
+    assert max_abs(np_(gpu.logq_tok), ref["logq_tok"]) <= TOL_ELL
+    assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW
+    assert np.allclose(np_(gpu.lse), ref["lse"], rtol=0, atol=TOL_LOGW)
+    assert np.allclose(np_(gpu.ess), ref["ess"], rtol=1e-3)
+    assert np.allclose(np_(gpu.wnorm), ref["wnorm"], rtol=1e-3, atol=1e-6)
+
+
+def test_temperature_and_power(smc, orc):
+    lp, lq, tok = synth.lm_logits(2, 8, 4, 30000, dtype=torch.bfloat16, seed=5, tau_q=0.7)
+    gpu, ref = _run_weights(smc, orc, lp, lq, tok, 30000, alpha=2.5, tp=1.0 / 0.6, tq=0.7)
+    assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW
+    assert max_abs(np_(gpu.logp_tok), ref["logp_tok"]) <= TOL_ELL * 2
+
+
+def test_identical_models_exact_zero(smc):
+    # p == q bitwise, tau_p == tau_q, alpha = 1  =>  Delta == 0.0 exactly and ESS == N exactly
+    # (requires the fixed in-row reduction order, reading G17)
+    lp, _, tok = synth.lm_logits(2, 16, 8, 128256, dtype=torch.bfloat16, seed=3)
+    dev = torch.device("cuda")
+    lpd = lp.to(dev)
+    lqd = lpd[:, :, :8, :].contiguous()
+    prev = torch.full((2, 16), -math.log(16), device=dev)
+    out = smc.smcsd_weights(lpd, lqd, tok.to(dev), V=128256, logw_prev=prev)
+    assert torch.equal(out.logw, prev)
+    assert torch.equal(out.logp_tok, out.logq_tok)
+    assert torch.all(out.ess == 16.0)
+
+
+def test_status_flags_match_oracle(smc, orc):
+    lp, lq, tok = synth.lm_logits(4, 4, 3, 9000, dtype=torch.float32, seed=9)
+    tok[0, 1, 0] = 9000                                   # BAD_TOKEN
+    lq[1, 2, 1, tok[1, 2, 1]] = -float("inf")             # NOT_ABSCONT
+    lp[2, 3, 0, 8500] = float("nan")                      # NONFINITE (second segment)
+    lp[3, 0, 2, tok[3, 0, 2]] = -float("inf")             # p(d) = 0: allowed, weight -inf
+    nd = torch.tensor([[3, 3, 3, 3], [3, 3, 3, 3], [3, 3, 3, 3], [3, 3, 3, 3]], dtype=torch.int32)
+    gpu, ref = _run_weights(smc, orc, lp, lq, tok, 9000, n_drafted=nd)
+    assert np_(gpu.status).astype(np.uint32).tolist() == ref["status"].tolist() == [4, 2, 8, 0]
+    assert np.array_equal(np.isneginf(np_(gpu.logw)), np.isneginf(ref["logw"]))
+    assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW
+    # all particles dead -> DEGENERATE
+    dead = torch.full((4, 4), -float("inf"))
+    gpu, ref = _run_weights(smc, orc, lp, lq, tok, 9000, logw_prev=dead)
+    assert np.array_equal(np_(gpu.status).astype(np.uint32), ref["status"])
+    assert np.all(np_(gpu.lse) == -np.inf) and np.all(np_(gpu.ess) == 0.0)
+
+
+def test_n_drafted_rows_never_read(smc, orc):
+    lp, lq, tok = synth.lm_logits(2, 5, 4, 10000, dtype=torch.bfloat16, seed=12)
+    nd = torch.tensor([[4, 0, 2, 1, 3], [4, 4, 4, 4, 4]], dtype=torch.int32)
+    for p in range(2):
+        for n in range(5):
+            k = int(nd[p, n])
+            lp[p, n, k:, :] = float("nan")
+            lq[p, n, k:, :] = float("nan")
+            tok[p, n, k:] = 10 ** 6
+    gpu, ref = _run_weights(smc, orc, lp, lq, tok, 10000, n_drafted=nd)
+    assert np.all(np_(gpu.status) == 0) and np.all(ref["status"] == 0)
+    assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW
+    assert np_(gpu.logw)[0, 1] == np.float32(-math.log(5))
+
+
+def test_large_n_weights_path(smc, orc):
+    # N > 1024 takes the serial-normalisation tail; ESS-rate fixture from SPEC.md:203
+    N = 4000
+    rng = np.random.default_rng(31)
+    row_p = torch.tensor([math.log(0.5), math.log(0.5), float("nan"), float("nan")])
+    row_q = torch.tensor([math.log(0.25), math.log(0.75), float("nan"), float("nan")])
+    lp = row_p.expand(1, N, 3, 4).contiguous()
+    lq = row_q.expand(1, N, 2, 4).contiguous()
+    tok = torch.from_numpy((rng.random((1, N, 2)) < 0.75).astype(np.int32))
+    gpu, ref = _run_weights(smc, orc, lp, lq, tok, 2, logw_prev=torch.zeros(1, N))
+    assert max_abs(np_(gpu.logw), ref["logw"]) <= 1e-6
+    assert np_(gpu.ess)[0] == pytest.approx(ref["ess"][0], rel=1e-6)
+    assert np_(gpu.ess)[0] / N == pytest.approx(0.5625, abs=0.03)
+
+
+# ----------------------------------------------------------------------------- resampling
+def _resample_both(smc, orc, lw, **kw):
+    dev = torch.device("cuda")
+    un = kw.get("uniforms")
+    gpu = smc.smcsd_resample(torch.from_numpy(lw).to(dev), eta=kw.get("eta", math.inf),
+                             seed=kw.get("seed", synth.PHILOX_SEED), step=kw.get("step", 0),
+                             prompt_base=kw.get("prompt_base", 0),
+                             uniforms=None if un is None else torch.from_numpy(un.view(np.int32)).to(dev))
+    torch.cuda.synchronize()
+    ref = orc.resample(lw, eta=kw.get("eta", math.inf), seed=kw.get("seed", synth.PHILOX_SEED),
+                       step=kw.get("step", 0), prompt_base=kw.get("prompt_base", 0), uniforms=un)
+    return gpu, ref
+
+
+def _assert_resample_equal(gpu, ref):
+    assert np.array_equal(np_(gpu.resampled), ref["resampled"])
+    assert np.array_equal(np_(gpu.status).astype(np.uint32), ref["status"])
+    assert np.array_equal(np_(gpu.n_ties), ref["n_ties"])
+    ok = ref["n_ties"] == 0
+    assert np.array_equal(np_(gpu.ancestors)[ok], ref["ancestors"][ok])
+    assert np.array_equal(np_(gpu.offspring)[ok], ref["offspring"][ok])
+    assert np.array_equal(np_(gpu.slot_src)[ok], ref["slot_src"][ok])
+    assert np_(gpu.logw)[ok].tobytes() == ref["logw"][ok].tobytes()
+    fin = np.isfinite(ref["lse"])
+    assert np.allclose(np_(gpu.lse)[fin], ref["lse"][fin], rtol=1e-12, atol=0)
+    assert np.allclose(np_(gpu.ess), ref["ess"], rtol=1e-12, atol=0)
+    assert np.array_equal(np_(gpu.lse)[~fin], ref["lse"][~fin])
+
+
+@pytest.mark.parametrize("N", [1, 2, 16, 32, 64, 100, 1024])
+def test_resample_bit_exact(smc, orc, N):
+    P = 64
+    lw = synth.random_logw(P, N, seed=N, sigma=2.0, neg_inf_frac=0.2).numpy()
+    lw[0, :] = -np.inf                                    # degenerate prompt
+    lw[1, :] = 0.0                                        # uniform: ESS = N
+    lw[2, :] = -np.inf; lw[2, N // 2] = 1.5               # single survivor
+    if N > 3:
+        lw[3, 3] = np.nan                                 # non-finite input -> flagged, -inf
+    for step in (0, 1, (1 << 40) + 3):
+        gpu, ref = _resample_both(smc, orc, lw, step=step, prompt_base=1000)
+        _assert_resample_equal(gpu, ref)
+    gpu, ref = _resample_both(smc, orc, lw, eta=N / 2)    # threshold path: some prompts kept
+    _assert_resample_equal(gpu, ref)
+
+
+def test_resample_worked_examples(smc, orc):
+    from conftest import read_golden
+    for line in read_golden("systematic_worked.txt"):
+        w, x, anc, off = [s.strip() for s in line.split(";")]
+        lw = np.log(np.array([float(v) for v in w.split(",")]))[None, :].astype(np.float32)
+        gpu, ref = _resample_both(smc, orc, lw, uniforms=np.array([int(x)], np.uint32))
+        assert np_(gpu.ancestors)[0].tolist() == [int(v) for v in anc.split(",")]
+        assert np_(gpu.offspring)[0].tolist() == [int(v) for v in off.split(",")]
+
+
+def test_reset_value_table(smc):
+    # fl32(-ln N), N = 1..1024, bitwise equal to the oracle's and Python's
+    dev = torch.device("cuda")
+    for N in range(1, 1025):
+        out = smc.smcsd_resample(torch.zeros(1, N, device=dev), eta=math.inf)
+        got = out.logw[0, 0].item()
+        assert np.float32(got).tobytes() == np.float32(-math.log(N)).tobytes(), N
+
+
+def test_systematic_unbiased_sweep(smc):
+    # deterministic exactness: mean over a stratified U sweep of o_m equals N*wbar_m to 2/M
+    dev = torch.device("cuda")
+    N, M = 32, 4096
+    lw = synth.random_logw(1, N, seed=77, sigma=1.5).to(dev).expand(M, N).contiguous()
+    xs = ((np.arange(M) + 0.5) / M * 2 ** 32).astype(np.uint64).astype(np.uint32)
+    out = smc.smcsd_resample(lw, eta=math.inf, uniforms=torch.from_numpy(xs.view(np.int32)).to(dev))
+    mean = out.offspring.double().mean(0).cpu().numpy()
+    wbar = out.wnorm[0].double().cpu().numpy()
+    assert np.max(np.abs(mean - N * wbar)) <= 2.0 / M + 1e-6
+
+
+def test_step_staged_parity(smc, orc):
+    # fused S1-S7: logw_pre feeds the oracle's S4-S7 -> bit-exact ancestry (staged protocol)
+    P, N, K, V = 4, 32, 8, 40000
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=21)
+    dev = torch.device("cuda")
+    prev = synth.uniform_prior(P, N)
+    out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, logw_prev=prev.to(dev),
+                         eta=math.inf, seed=123, step=9, prompt_base=40)
+    torch.cuda.synchronize()
+    ref_w = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, logw_prev=prev.numpy())
+    assert max_abs(np_(out.logw_pre), ref_w["logw"]) <= TOL_LOGW
+    staged = orc.resample(np_(out.logw_pre), eta=math.inf, seed=123, step=9, prompt_base=40)
+    _assert_resample_equal(out, staged)
+    # determinism: a second run is bitwise identical
+    out2 = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, logw_prev=prev.to(dev),
+                          eta=math.inf, seed=123, step=9, prompt_base=40)
+    for f in ("logw", "logw_pre", "ancestors", "slot_src", "ess", "lse", "logp_tok"):
+        assert torch.equal(getattr(out, f), getattr(out2, f)), f
+
+
+def test_step_end_to_end_vs_oracle(smc, orc):
+    # soft protocol: oracle from the logits; ancestor mismatches only where |u - C| is within
+    # the CDF disagreement (none expected at these sizes)
+    P, N, K, V = 2, 16, 8, 128256
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=22)
+    dev = torch.device("cuda")
+    out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, eta=math.inf, seed=5, step=1)
+    torch.cuda.synchronize()
+    ref_w = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V)
+    ref = orc.resample(ref_w["logw"], eta=math.inf, seed=5, step=1)
+    assert max_abs(np_(out.logw_pre), ref_w["logw"]) <= TOL_LOGW
+    assert np.allclose(np_(out.ess), ref["ess"], rtol=1e-3)
+    assert np.array_equal(np_(out.ancestors), ref["ancestors"])
+
+
+def test_n_equals_one(smc):
+    # N = 1 reduces to plain proposal sampling: a = [0], ESS = 1
+    lp, lq, tok = synth.lm_logits(3, 1, 4, 5000, dtype=torch.bfloat16, seed=2)
+    dev = torch.device("cuda")
+    out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=5000, eta=math.inf)
+    assert torch.all(out.ancestors == 0) and torch.all(out.ess == 1.0)
+    assert torch.all(out.logw == 0.0)
+
+
+def test_dp_prompt_sharding_is_bit_identical(smc):
+    # prompt-sharded (data-parallel) runs use the global prompt index for Philox
+    P, N, K, V = 8, 32, 8, 30000
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=33)
+    dev = torch.device("cuda")
+    lp, lq, tok = lp.to(dev), lq.to(dev), tok.to(dev)
+    full = smc.smcsd_step(lp, lq, tok, V=V, eta=math.inf, seed=99, step=4)
+    for G in (2, 4, 8):
+        per = P // G
+        for g in range(G):
+            sl = slice(g * per, (g + 1) * per)
+            part = smc.smcsd_step(lp[sl].contiguous(), lq[sl].contiguous(), tok[sl].contiguous(),
+                                  V=V, eta=math.inf, seed=99, step=4, prompt_base=g * per)
+            for f in ("logw", "ancestors", "slot_src", "ess", "lse"):
+                assert torch.equal(getattr(part, f), getattr(full, f)[sl]), (G, g, f)
+
+
+# ----------------------------------------------------------------------------- TP (cfg5)
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_tp_vocab_sharded_simulated(smc, orc, G):
+    # cfg5 shapes: V = 128256 split G-way, N = 64, K = 8; shards run one after another on
+    # one GPU, gathered in rank order, combined (bit-identical on every rank by construction)
+    P, N, K, V = 1, 64, 8, 128256
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=55)
+    dev = torch.device("cuda")
+    lpd, lqd, tokd = lp.to(dev), lq.to(dev), tok.to(dev)
+    bounds = [V * g // G // 8 * 8 for g in range(G)] + [V]
+    parts = []
+    for g in range(G):
+        b0, b1 = bounds[g], bounds[g + 1]
+        w = (b1 - b0 + 7) // 8 * 8
+        sp = torch.full((P, N, K + 1, w), float("nan"), dtype=torch.bfloat16, device=dev)
+        sq = torch.full((P, N, K, w), float("nan"), dtype=torch.bfloat16, device=dev)
+        sp[..., :b1 - b0] = lpd[..., b0:b1]
+        sq[..., :b1 - b0] = lqd[..., b0:b1]
+        parts.append(smc.smcsd_weights_partial(sp, sq, tokd, v_begin=b0, v_len=b1 - b0))
+    gathered = torch.stack(parts).contiguous()
+    c1 = smc.smcsd_weights_combine(gathered, tokd, V=V)
+    c2 = smc.smcsd_weights_combine(gathered.clone(), tokd, V=V)
+    assert torch.equal(c1.logw, c2.logw) and torch.equal(c1.ess, c2.ess)
+    full = smc.smcsd_weights(lpd, lqd, tokd, V=V)
+    assert (c1.logw - full.logw).abs().max().item() <= 1e-5
+    ref = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V)
+    assert max_abs(np_(c1.logw), ref["logw"]) <= TOL_LOGW
+    assert np.array_equal(np_(c1.status).astype(np.uint32), ref["status"])
+
+
+# ----------------------------------------------------------------------------- KV (S8/S9)
+def _kv_case(smc, orc, L, P, N, H, S, d, seq_len, in_place, seed):
+    dev = torch.device("cuda")
+    kv = synth.kv_bits((L, 2, P, N, H, S, d), seed=seed)
+    lw = synth.random_logw(P, N, seed=seed, sigma=2.0).numpy()
+    r = orc.resample(lw, eta=np.inf, seed=seed)
+    idx = r["slot_src"] if in_place else r["ancestors"]
+    geom = smc.kv_geometry(kv, seq_len)
+    src = kv.to(dev)
+    dst = src if in_place else torch.zeros_like(src)
+    smc.smcsd_kv_reindex(dst, src, torch.from_numpy(idx).to(dev), **geom)
+    torch.cuda.synchronize()
+    want = kv.numpy().copy()
+    want_dst = want if in_place else np.zeros_like(want)
+    orc.kv_reindex(want_dst, want, idx, **geom)
+    assert np.array_equal(dst.cpu().numpy(), want_dst)
+
+
+@pytest.mark.parametrize("in_place", [False, True])
+def test_kv_reindex_toy_cfg1(smc, orc, in_place):
+    _kv_case(smc, orc, L=2, P=1, N=4, H=2, S=64, d=16, seq_len=64, in_place=in_place, seed=1)
+
+
+@pytest.mark.parametrize("in_place", [False, True])
+def test_kv_reindex_ragged(smc, orc, in_place):
+    # several chunks, partial fill of each head, P > 1, N not a power of two
+    _kv_case(smc, orc, L=3, P=3, N=37, H=4, S=256, d=64, seq_len=200, in_place=in_place, seed=2)
+    _kv_case(smc, orc, L=1, P=2, N=1024, H=1, S=8, d=8, seq_len=8, in_place=in_place, seed=3)
+
+
+def test_token_history_reindex(smc, orc):
+    # S9: tok'[p][n][:] = tok[p][a_n][:], int32 rows through the same entry point
+    dev = torch.device("cuda")
+    P, N, T = 4, 16, 100
+    tok = torch.randint(0, 128256, (P, N, T), dtype=torch.int32)
+    lw = synth.random_logw(P, N, seed=4, sigma=2.0).numpy()
+    r = orc.resample(lw, eta=np.inf, seed=4)
+    geom = dict(n_outer=1, outer_stride=0, prompt_stride=N * T * 4, particle_stride=T * 4,
+                seg_count=1, seg_bytes=T * 4, seg_stride=T * 4)
+    src = tok.to(dev)
+    dst = torch.zeros_like(src)
+    smc.smcsd_kv_reindex(dst, src, torch.from_numpy(r["ancestors"]).to(dev), **geom)
+    want = np.stack([tok.numpy()[p][r["ancestors"][p]] for p in range(P)])
+    assert np.array_equal(dst.cpu().numpy(), want)
+
+
+def test_kv_identity_is_noop(smc):
+    dev = torch.device("cuda")
+    kv = synth.kv_bits((2, 2, 1, 8, 2, 32, 16), seed=5).to(dev)
+    before = kv.clone()
+    smc.smcsd_kv_reindex(kv, kv, torch.arange(8, dtype=torch.int32, device=dev)[None],
+                         **smc.kv_geometry(kv))
+    assert torch.equal(kv, before)
