@@ -119,7 +119,10 @@ def dist_env(args):
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if args.impl == "reference":
+        backend = os.environ.get("SMCSD_BENCH_BACKEND", "nccl")   # gloo: functional test only
+        if args.impl == "reference" or backend == "gloo":
+            if args.impl != "reference":
+                torch.cuda.set_device(local % torch.cuda.device_count())
             dist.init_process_group("gloo")
         else:
             torch.cuda.set_device(local)
@@ -170,7 +173,7 @@ class Cfg2Step:
             self.hist_geom = dict(n_outer=1, outer_stride=0, prompt_stride=N * self.T * 4,
                                   particle_stride=self.T * 4, seg_count=1, seg_bytes=self.T * 4,
                                   seg_stride=self.T * 4)
-        self.kernels = ["k_rowstats(step)"] + (["k_kv_reindex(kv)", "k_kv_reindex(tokens)"] if kv else [])
+        self.kernels = ["smcsd_step(k_rowstats+k_tail)"] + (["k_kv_reindex(kv)", "k_kv_reindex(tokens)"] if kv else [])
 
     def launches_per_step(self):
         return len(self.kernels)
@@ -213,7 +216,7 @@ def run_ours(args, rank, world, local):
     import paper_2604_15672_b200 as smc
     from paper_2604_15672_b200.dist import max_over_ranks
 
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     hbm_peak, peak_src = peaks()
     wl = Cfg2Step(dev, rank, args)
@@ -271,6 +274,14 @@ def run_ours(args, rank, world, local):
 
     # ---- end to end through the public API with host buffers (H2D of inputs, D2H of result)
     e2e = run_e2e(wl, args, dev, world)
+    secondary = {}
+    if not args.no_secondary:
+        del wl.kv
+        wl.kv = None
+        torch.cuda.empty_cache()
+        secondary["cfg4"] = measure_cfg4(dev, rank, world, hbm_peak)
+        if world == 1:
+            secondary["cfg3"] = measure_cfg3(dev, hbm_peak)
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
@@ -295,6 +306,7 @@ def run_ours(args, rank, world, local):
         "breakdown": {"verify_resample_us": round(per_kernel_ms[0] * 1e3, 2),
                       "verify_resample_steps_per_s": round(1e3 / per_kernel_ms[0], 1)},
         "e2e": e2e,
+        "secondary": secondary,
         "gpu_launches": nk * args.steps,
         "clocks": clk.summary(),
         "library": smc.smcsd_version(),
@@ -304,6 +316,99 @@ def run_ours(args, rank, world, local):
         line["cpu_baseline"] = cpu_baseline(wl, budget_s=args.cpu_budget)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _time_steps(fn, steps, warmup, world, dev):
+    """Device time per step (CUDA events on the current stream), max over ranks."""
+    import torch
+    from paper_2604_15672_b200.dist import max_over_ranks
+    for i in range(warmup):
+        fn(i)
+    barrier(world)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for i in range(steps):
+        fn(warmup + i)
+    t1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(t0.elapsed_time(t1), dev) / steps
+
+
+def measure_cfg4(dev, rank, world, hbm_peak, steps=20, warmup=3):
+    """configs[3]: 64 prompts x N=32 x K=8, V=128256 bf16, prompt-sharded over the ranks
+    (strong scaling: 64/G prompts per rank, global prompt index for Philox).  S1-S7 per step
+    (the dense KV of 64 x 32 70B particles, 1.3 TB, does not fit: S8 is measured in cfg3)."""
+    import torch
+    import paper_2604_15672_b200 as smc
+    import synth
+    from paper_2604_15672_b200.dist import prompt_shard
+    P_all, N, K, V = 64, 32, 8, 128256
+    b, e = prompt_shard(P_all, world, rank)
+    P = e - b
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, device=dev,
+                                  seed=synth.GEN_SEED_BASE + 4 + 101 * rank)
+    logw = synth.uniform_prior(P, N, device=dev)
+    ws = smc.Workspace(dev)
+    out = smc.Outputs(logw=logw)
+    fn = lambda i: smc.smcsd_step(lp, lq, tok, V=V, logw_prev=logw, eta=math.inf, step=i,
+                                  prompt_base=b, out=out, fields=(), workspace=ws)
+    ms = _time_steps(fn, steps, warmup, world, dev)
+    byts = P * (2 * N * K * V * 2 + N * K * 4 + 3 * N * 4)
+    gbs = byts / (ms / 1e3) / 1e9
+    del lp, lq, tok
+    torch.cuda.empty_cache()
+    return {"workload": f"cfg4: {P_all} prompts x N={N} x K={K}, V={V} bf16, {P} prompts/rank, "
+                        f"smcsd_step (S1-S7); 8.4 GB/step at G=1 (> L2)",
+            "steps_per_s": round(P_all / (ms / 1e3) if world > 1 else P / (ms / 1e3), 1),
+            "unit": "prompt-steps/s", "ms_per_step": round(ms, 4), "bytes_per_rank": int(byts),
+            "achieved_gbs_per_rank": round(gbs, 1), "frac_of_measured": round(gbs / hbm_peak, 4),
+            "frac_of_8tbs": round(gbs / 8000.0, 4)}
+
+
+def measure_cfg3(dev, hbm_peak, steps=5, warmup=2):
+    """configs[2]: Llama-3.1-70B KV (80 L x 2 x 8 heads x 2048 x 128 bf16 = 640 MiB/particle),
+    N=32, pinned ancestor pattern (lam = 0 on even n, -inf on odd n: 16 sources x 2 offspring).
+    One step = smcsd_resample + smcsd_kv_reindex, out of place and in place."""
+    import torch
+    import paper_2604_15672_b200 as smc
+    import synth
+    N = 32
+    L, H, S, d = KV70B["L"], KV70B["H"], KV70B["S"], KV70B["d"]
+    lw = torch.zeros((1, N), device=dev)
+    lw[0, 1::2] = -float("inf")
+    res = {}
+    Bp = L * 2 * H * S * d * 2
+    src = synth.kv_bits_fast((L, 2, 1, N, H, S, d), seed=7, device=dev)
+    geom = smc.kv_geometry(src)
+    dst = torch.empty_like(src)
+    o = smc.smcsd_resample(lw.clone(), eta=math.inf)
+    torch.cuda.synchronize()
+    off = o.offspring[0].cpu()
+    distinct, dead = int((off >= 1).sum()), int((off == 0).sum())
+    multi = int((off >= 2).sum())
+    for mode in ("out_of_place", "in_place"):
+        lwb = lw.clone()
+
+        def fn(i, mode=mode):
+            lwb.copy_(lw)
+            r = smc.smcsd_resample(lwb, eta=math.inf, step=i, out=o)
+            if mode == "out_of_place":
+                smc.smcsd_kv_reindex(dst, src, r.ancestors, **geom)
+            else:
+                smc.smcsd_kv_reindex(src, src, r.slot_src, **geom)
+        ms = _time_steps(fn, steps, warmup, 1, dev)
+        byts = ((distinct + N) if mode == "out_of_place" else (multi + dead)) * Bp
+        gbs = byts / (ms / 1e3) / 1e9
+        res[mode] = {"steps_per_s": round(1e3 / ms, 2), "ms_per_step": round(ms, 4),
+                     "algorithmic_bytes": int(byts), "achieved_gbs": round(gbs, 1),
+                     "frac_of_measured": round(gbs / hbm_peak, 4), "frac_of_8tbs": round(gbs / 8000.0, 4)}
+    del src, dst
+    torch.cuda.empty_cache()
+    res["workload"] = ("cfg3: 70B KV, N=32, pinned pattern (16 sources x 2 offspring, 16 dead slots); "
+                       "step = smcsd_resample + smcsd_kv_reindex")
+    return res
 
 
 def run_e2e(wl, args, dev, world):
@@ -439,6 +544,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the cfg3/cfg4 measurements")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

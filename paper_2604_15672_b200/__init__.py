@@ -31,7 +31,7 @@ ST_DEGENERATE, ST_NOT_ABSCONT, ST_BAD_TOKEN, ST_NONFINITE = 1, 2, 4, 8
 _RC = {0: "ok", 1: "invalid argument", 2: "CUDA launch or runtime error", 3: "not implemented"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "libsmcsd.so")
+lib_path = os.environ.get("SMCSD_LIB_OVERRIDE") or os.path.join(_HERE, "libsmcsd.so")  # debug builds only
 
 
 class SmcsdError(RuntimeError):

@@ -35,21 +35,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(f) > t for f in files)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """Build libsmcsd.so (or, with trace=True, the %globaltimer-instrumented debug variant
+    libsmcsd_trace.so used only by scripts/trace_tail.py)."""
+    lib = LIB.replace(".so", "_trace.so") if trace else LIB
+    if not force and not trace and not _stale():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-o", tmp,
-           *[os.path.join(CSRC, s) for s in SOURCES]]
+    tmp = lib + ".tmp"
+    extra = ["-DSMCSD_TRACE"] if trace else []
+    if trace and os.environ.get("SMCSD_TRACE_TWICE"):
+        extra.append("-DSMCSD_TRACE_TWICE")
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC,
+           "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libsmcsd.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, trace="--trace" in sys.argv))

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "smcsd.h"
@@ -21,7 +22,7 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 struct WsLayout {
-    size_t counters, parts, ell, lam, e, c, total;
+    size_t ctr, parts, ell, lam, e, c, rowstat, total;
 };
 
 WsLayout ws_layout(int P, int N, int K, int64_t v_len) {
@@ -29,24 +30,26 @@ WsLayout ws_layout(int P, int N, int K, int64_t v_len) {
     const size_t rows = 2ull * (size_t)P * (size_t)N * (size_t)K;
     const size_t nseg = (size_t)cdiv(v_len < 1 ? 1 : v_len, kSeg);
     size_t off = 0;
-    L.counters = off; off += align256((size_t)P * sizeof(unsigned));
+    L.ctr = off;      off += 256;
     L.parts = off;    off += align256(rows * nseg * sizeof(float4));
     L.ell = off;      off += align256(rows * sizeof(double));
     L.lam = off;      off += align256((size_t)P * N * sizeof(float));
     L.e = off;        off += align256((size_t)P * N * sizeof(double));
     L.c = off;        off += align256((size_t)P * N * sizeof(double));
+    L.rowstat = off;  off += align256(rows * sizeof(float4));
     L.total = off;
     return L;
 }
 
 void bind_workspace(Params &prm, void *ws, const WsLayout &L) {
     char *b = static_cast<char *>(ws);
-    prm.counters = reinterpret_cast<unsigned *>(b + L.counters);
     prm.part_ws = reinterpret_cast<float4 *>(b + L.parts);
     prm.ell_ws = reinterpret_cast<double *>(b + L.ell);
     prm.lam_ws = reinterpret_cast<float *>(b + L.lam);
     prm.e_ws = reinterpret_cast<double *>(b + L.e);
     prm.c_ws = reinterpret_cast<double *>(b + L.c);
+    prm.rowstat_ws = reinterpret_cast<float4 *>(b + L.rowstat);
+    prm.work_ctr = reinterpret_cast<unsigned *>(b + L.ctr);
 }
 
 bool valid_temp(float t) { return std::isfinite(t) && t > 0.0f; }
@@ -67,12 +70,68 @@ smcsd_rc check_logits(const void *lp, int64_t ld_p, int rpp_p, const void *lq, i
     return SMCSD_OK;
 }
 
-smcsd_rc launched() { return cudaGetLastError() == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA; }
+// Launch with programmatic stream serialization (PDL): the kernel may start while its
+// predecessor in the stream drains; it calls griddepcontrol.wait before touching that
+// predecessor's outputs.
+template <typename... KArgs, typename... Args>
+smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaStream_t st,
+                    Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...) == cudaSuccess
+               ? SMCSD_OK : SMCSD_ECUDA;
+}
 
-template <int MODE>
-void launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st) {
-    if (dtype == SMCSD_BF16) k_rowstats<1, MODE><<<(unsigned)items, kThreads, 0, st>>>(prm);
-    else                     k_rowstats<0, MODE><<<(unsigned)items, kThreads, 0, st>>>(prm);
+// K1 persistent grid: SMs x resident CTAs, capped by the number of work items.
+template <int DT>
+smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
+    static int ctas[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
+    if (ctas[dev] == 0) {
+        int occ = 0, sms = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT>, kThreads, 0) != cudaSuccess ||
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || occ < 1)
+            return SMCSD_ECUDA;
+        ctas[dev] = occ * sms;
+    }
+    const int64_t grid = items < ctas[dev] ? items : ctas[dev];
+    return launch_pdl(k_rowstats<DT>, (unsigned)grid, 0, st, prm);
+}
+
+// K2 tail: one CTA per prompt; the per-row S2 statistics live in dynamic shared memory when
+// they fit (k_tail<true>), else in the workspace (k_tail<false>).
+smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
+    if (!attr_set[dev]) {
+        const int big = (int)(kStageBytes + kRowStatSmem * sizeof(float4));
+        if (cudaFuncSetAttribute(k_tail<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tail<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tail_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes) != cudaSuccess)
+            return SMCSD_ECUDA;
+        attr_set[dev] = true;
+    }
+    const int64_t rows = 2ll * prm.N * prm.K;
+    if (prm.N > kTailMaxN) return launch_pdl(k_tail_large, (unsigned)prm.P, kStageBytes, st, prm);
+    if (rows <= kRowStatSmem && prm.N * (int64_t)prm.K <= 2 * kTailMaxN)
+        return launch_pdl(k_tail<true>, (unsigned)prm.P, kStageBytes + (size_t)rows * sizeof(float4), st,
+                          prm, resample_mode);
+    return launch_pdl(k_tail<false>, (unsigned)prm.P, kStageBytes, st, prm, resample_mode);
+}
+
+smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st) {
+    return dtype == SMCSD_BF16 ? launch_rowstats_dt<1>(prm, items, st)
+                               : launch_rowstats_dt<0>(prm, items, st);
 }
 
 // Common Params for the logits entry points.
@@ -135,14 +194,9 @@ smcsd_rc smcsd_weights(const void *logits_p, int64_t ld_p, int rows_per_particle
     prm.nparts = prm.nseg;
     const int64_t items = 2ll * P * N * K * prm.nseg;
     cudaStream_t st = as_stream(stream);
-    if (N <= kTailMaxN) {
-        launch_rowstats<MODE_WEIGHTS>(prm, dtype, items, st);
-    } else {
-        launch_rowstats<MODE_ROWS_ONLY>(prm, dtype, items, st);
-        if (launched() != SMCSD_OK) return SMCSD_ECUDA;
-        k_tail_large<<<P, kThreads, 0, st>>>(prm);
-    }
-    return launched();
+    rc = launch_rowstats(prm, dtype, items, st);
+    if (rc != SMCSD_OK) return rc;
+    return launch_tail(prm, 0, st);
 }
 
 smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t prompt_base, float eta,
@@ -163,8 +217,7 @@ smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t prompt_base, fl
     prm.ancestors = ancestors; prm.offspring = offspring; prm.slot_src = slot_src;
     prm.logw_out = logw_out; prm.resampled = resampled; prm.ess = ess_out; prm.lse = lse_out;
     prm.wnorm = wnorm_out; prm.n_ties = n_ties; prm.status = status;
-    k_resample<<<P, kThreads, 0, as_stream(stream)>>>(prm);
-    return launched();
+    return launch_pdl(k_resample, (unsigned)P, 0, as_stream(stream), prm);
 }
 
 smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
@@ -203,8 +256,10 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
     bind_workspace(prm, workspace, L);
     prm.parts = prm.part_ws; prm.part_row_stride = prm.nseg; prm.part_seg_stride = 1;
     prm.nparts = prm.nseg;
-    launch_rowstats<MODE_STEP>(prm, dtype, 2ll * P * N * K * prm.nseg, as_stream(stream));
-    return launched();
+    cudaStream_t st = as_stream(stream);
+    rc = launch_rowstats(prm, dtype, 2ll * P * N * K * prm.nseg, st);
+    if (rc != SMCSD_OK) return rc;
+    return launch_tail(prm, 1, st);
 }
 
 smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
@@ -225,8 +280,10 @@ smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_
                                v_begin + v_len, v_begin, v_len, inv_temp_p, inv_temp_q);
     prm.partials_out = reinterpret_cast<float4 *>(partials);
     bind_workspace(prm, workspace, L);
-    launch_rowstats<MODE_PARTIAL>(prm, dtype, 2ll * P * N * K * prm.nseg, as_stream(stream));
-    return launched();
+    cudaStream_t st = as_stream(stream);
+    rc = launch_rowstats(prm, dtype, 2ll * P * N * K * prm.nseg, st);
+    if (rc != SMCSD_OK) return rc;
+    return launch_pdl(k_merge_rows, (unsigned)P, 0, st, prm);
 }
 
 smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int32_t *tokens,
@@ -251,8 +308,7 @@ smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int32_t *toke
     prm.part_row_stride = 1;
     prm.part_seg_stride = 2ll * P * N * K;
     prm.nparts = G;
-    k_tail<<<P, kThreads, 0, as_stream(stream)>>>(prm, 0);
-    return launched();
+    return launch_tail(prm, 0, as_stream(stream));
 }
 
 smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_stride,
@@ -280,8 +336,7 @@ smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t o
     prm.idx = src_index; prm.P = P; prm.N = N; prm.in_place = dst == src;
     const int64_t items = n_outer * P * prm.nchunks;
     if (items >= (1ll << 31)) return SMCSD_EINVAL;
-    k_kv_reindex<<<(unsigned)items, kThreads, 0, as_stream(stream)>>>(prm);
-    return launched();
+    return launch_pdl(k_kv_reindex, (unsigned)items, 0, as_stream(stream), prm);
 }
 
 const char *smcsd_strerror(smcsd_rc rc) {
@@ -295,5 +350,11 @@ const char *smcsd_strerror(smcsd_rc rc) {
 }
 
 const char *smcsd_version(void) { return "smcsd 0.1 sm_100a"; }
+
+#ifdef SMCSD_TRACE
+SMCSD_API int smcsd_trace_read(unsigned long long *host, int n) {
+    return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * (n > 4096 ? 4096 : n)) == cudaSuccess ? 0 : 2;
+}
+#endif
 
 }  // extern "C"

@@ -1,12 +1,13 @@
 // smcsd_kernels.cuh -- the sm_100a kernels of libsmcsd.
 //
-//  K1  k_rowstats<DT, MODE>  S1: per (logit row, fixed 8192-element segment) work item, one
+//  K1  k_rowstats<DT>       S1: per (logit row, fixed 8192-element segment) work item, one
 //                            streaming pass: m = max t, s = sum 2^(t - m), x = t_d, with
 //                            t = inv_temp * z * log2(e)  (Eq. 1a).
-//                            MODE_WEIGHTS / MODE_STEP: the last CTA of each prompt (completion
-//                            counter) runs the tail below in the same launch.
-//  K2  tail_prompt           S2 merge segments in fixed order -> ell, S3 reweight, S4 fp64
-//                            normalise + ESS, S5-S7 systematic resampling from Philox, reset.
+//                            Persistent CTAs over contiguous item ranges, 16-byte streaming
+//                            loads with a one-item register prefetch.
+//  K2  k_tail                one CTA per prompt, PDL-launched behind K1: S2 merge segments in
+//                            fixed order -> ell, S3 reweight, S4 fp64 normalise + ESS, S5-S7
+//                            systematic resampling from Philox, reset.
 //  K3  k_kv_reindex          S8/S9 source-major bitwise gather of per-particle blocks.
 //
 // Determinism (reading G17): every row uses the same segment boundaries and the same
@@ -20,10 +21,13 @@
 
 namespace smcsd {
 
-enum { MODE_WEIGHTS = 0, MODE_STEP = 1, MODE_PARTIAL = 2, MODE_ROWS_ONLY = 3 };
 
 constexpr uint32_t ST_DEGENERATE = 1u, ST_NOT_ABSCONT = 2u, ST_BAD_TOKEN = 4u, ST_NONFINITE = 8u;
+#ifndef SMCSD_PHASE
+#define SMCSD_PHASE(i) do { } while (0)
+#endif
 constexpr double kLn2 = 0.693147180559945309417232121458176568;
+constexpr int kRowStatSmem = 2048;                           // rows whose S2 stats fit in smem
 
 struct Params {
     // ---- inputs (S1)
@@ -55,67 +59,83 @@ struct Params {
     int64_t part_row_stride, part_seg_stride;
     int nparts;
     // ---- workspace
-    unsigned *counters;                         // [P]
     float4 *part_ws;                            // [P*2*N*K*nseg]
     double *ell_ws;                             // [P*2*N*K]
     float *lam_ws;                              // [P*N]   (N > kTailMaxN path)
     double *e_ws, *c_ws;                        // [P*N]
+    float4 *rowstat_ws;                         // [P*2*N*K] (rows > kRowStatSmem)
+    unsigned *work_ctr;                         // K1 dynamic work counter (re-armed by K2)
 };
 
 // ------------------------------------------------------------------------------------------
-// S1 for one (row, segment).  Returns {m, s, x, 0} at thread 0 (log2 domain).
+// Programmatic dependent launch (PDL): the tail / gather kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, start while their predecessor drains,
+// and block in griddepcontrol.wait until its memory is visible.
 // ------------------------------------------------------------------------------------------
-template <int DT>  // 0 = fp32, 1 = bf16
-__device__ __forceinline__ float4 segment_stats(const char *row, int64_t v_len, int seg, float c,
-                                                int64_t d_local, float2 *red) {
-    constexpr int kEsz = DT == 1 ? 2 : 4;
-    constexpr int kVec = 16 / kEsz;                          // elements per 16-byte load
-    constexpr int kLoads = kSeg / (kThreads * kVec);         // 4 (bf16) or 8 (fp32)
-    constexpr uint32_t kNegInf = DT == 1 ? 0xFF80FF80u : 0xFF800000u;
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ------------------------------------------------------------------------------------------
+// K1: S1 over (row, 8192-column segment) work items.  Persistent CTAs own contiguous item
+// ranges; every thread keeps the NEXT item's 16-byte loads in flight (register double
+// buffer) while it reduces the current one, so the per-item block merge never drains the
+// memory pipe.  One CTA-wide barrier per item; warp 0 merges the 8 warp partials with a
+// fixed-order shuffle tree and stores {m, s, x, 0}.
+// ------------------------------------------------------------------------------------------
+template <int DT>
+struct ItemTraits {
+    static constexpr int kEsz = DT == 1 ? 2 : 4;
+    static constexpr int kVec = 16 / kEsz;                   // elements per 16-byte vector
+    static constexpr int kLoads = kSeg / (kThreads * kVec);  // vectors per thread: 4 / 8
+    static constexpr uint32_t kNegInf = DT == 1 ? 0xFF80FF80u : 0xFF800000u;
+};
+
+__device__ __forceinline__ int drafted_len(const Params &prm, int64_t pn) {
+    return prm.n_drafted ? prm.n_drafted[pn] : prm.K;
+}
+
+// Reduce one item held in registers: lane 0 of each warp writes red[warp] = {m_w, s_w}; the
+// thread holding the drafted token (local index dl) writes *xs = t_d.
+template <int DT>
+__device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], int nv, float c,
+                                            int dl, float2 *red, float *xs) {
+    using T = ItemTraits<DT>;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t v0 = (int64_t)seg * kSeg;
-
-    // drafted-token logit: issued first so its latency hides under the stream
-    float zd = -INFINITY;
-    const bool has_d = tid == 0 && d_local >= v0 && d_local < v0 + kSeg && d_local < v_len;
-    if (has_d) {
-        if (DT == 1) zd = bf16lo((uint32_t)__ldg((const unsigned short *)row + d_local));
-        else         zd = __ldg((const float *)row + d_local);
-    }
-
-    uint4 v[kLoads];
-    if (v0 + kSeg <= v_len) {
+    if (nv < kSeg) {                                          // ragged last segment: mask >= V
 #pragma unroll
-        for (int i = 0; i < kLoads; ++i)
-            v[i] = ld_stream(row + (v0 + (int64_t)(i * kThreads + tid) * kVec) * kEsz);
-    } else {
+        for (int i = 0; i < T::kLoads; ++i) {
+            const int e = (i * kThreads + tid) * T::kVec;
+            uint32_t *w = reinterpret_cast<uint32_t *>(&v[i]);
 #pragma unroll
-        for (int i = 0; i < kLoads; ++i) {
-            const int64_t e = v0 + (int64_t)(i * kThreads + tid) * kVec;
-            if (e < v_len) {
-                v[i] = ld_stream(row + e * kEsz);
-                uint32_t *w = reinterpret_cast<uint32_t *>(&v[i]);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (DT == 1) {
-                        if (e + 2 * k >= v_len)     w[k] = (w[k] & 0xffff0000u) | 0x0000FF80u;
-                        if (e + 2 * k + 1 >= v_len) w[k] = (w[k] & 0x0000ffffu) | 0xFF800000u;
-                    } else {
-                        if (e + k >= v_len) w[k] = kNegInf;
-                    }
+            for (int k = 0; k < 4; ++k) {
+                if (DT == 1) {
+                    if (e + 2 * k >= nv)     w[k] = (w[k] & 0xffff0000u) | 0x0000FF80u;
+                    if (e + 2 * k + 1 >= nv) w[k] = (w[k] & 0x0000ffffu) | 0xFF800000u;
+                } else {
+                    if (e + k >= nv) w[k] = T::kNegInf;
                 }
-            } else {
-                v[i] = make_uint4(kNegInf, kNegInf, kNegInf, kNegInf);
             }
         }
     }
-
-    // ---- max over the warp's 1024 elements (raw logits; c > 0 so max(z)*c = max(z*c))
+    if (dl >= 0 && dl < nv) {                                 // drafted token of this segment
+        const int vi = dl / T::kVec, k = dl % T::kVec;
+        if ((vi % kThreads) == tid) {
+            const int i = vi / kThreads;
+            uint4 w = v[0];
+#pragma unroll
+            for (int q = 1; q < T::kLoads; ++q) if (q == i) w = v[q];
+            const uint32_t word = (DT == 1 ? k >> 1 : k) == 0 ? w.x : (DT == 1 ? k >> 1 : k) == 1 ? w.y
+                                : (DT == 1 ? k >> 1 : k) == 2 ? w.z : w.w;
+            const float z = DT == 1 ? ((k & 1) ? bf16hi(word) : bf16lo(word)) : __uint_as_float(word);
+            *xs = z * c;
+        }
+    }
+    // max over the warp's elements (raw logits; c > 0 so max(z)*c = max(z*c))
     float mt;
     if (DT == 1) {
         uint32_t acc = v[0].x;
 #pragma unroll
-        for (int i = 0; i < kLoads; ++i) {
+        for (int i = 0; i < T::kLoads; ++i) {
             const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) asm("max.bf16x2 %0, %0, %1;" : "+r"(acc) : "r"(w4[k]));
@@ -124,18 +144,16 @@ __device__ __forceinline__ float4 segment_stats(const char *row, int64_t v_len, 
     } else {
         mt = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < kLoads; ++i) {
+        for (int i = 0; i < T::kLoads; ++i)
             mt = fmaxf(mt, fmaxf(fmaxf(__uint_as_float(v[i].x), __uint_as_float(v[i].y)),
                                  fmaxf(__uint_as_float(v[i].z), __uint_as_float(v[i].w))));
-        }
     }
     const float mw = warp_max(mt) * c;                       // warp max of t = z*c
     const float off = mw == -INFINITY ? 0.0f : mw;           // all -inf: sum(2^-inf) = 0, NaN kept
-
-    // ---- sum of 2^(t - m): exactly one ex2 per element
-    float s_acc[kLoads];
+    // sum of 2^(t - m): exactly one ex2 per element
+    float s_acc[T::kLoads];
 #pragma unroll
-    for (int i = 0; i < kLoads; ++i) {
+    for (int i = 0; i < T::kLoads; ++i) {
         const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
         float a = 0.0f;
         if (DT == 1) {
@@ -152,31 +170,179 @@ __device__ __forceinline__ float4 segment_stats(const char *row, int64_t v_len, 
     }
     float s = s_acc[0];
 #pragma unroll
-    for (int i = 1; i < kLoads; ++i) s += s_acc[i];
+    for (int i = 1; i < T::kLoads; ++i) s += s_acc[i];
     s = warp_sum(s);
     if (lane == 0) red[warp] = make_float2(mw, s);
-    __syncthreads();
-    float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (tid == 0) {
-        float M = red[0].x;
-#pragma unroll
-        for (int w = 1; w < kWarps; ++w) M = fmaxf(M, red[w].x);
-        float S = 0.0f;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const float mwv = red[w].x;
-            S += red[w].y * (mwv == M ? 1.0f : ex2_approx(mwv - M));
-        }
-        out = make_float4(M, S, has_d ? zd * c : -INFINITY, 0.0f);
-    }
-    return out;
 }
 
-// Merge row parts in fixed index order: M = max m_i, S = sum s_i 2^(m_i - M), X = max x_i.
+// Decoded work item (thread 0 decodes, the CTA reads it from shared memory).
+struct ItemInfo {
+    const char *seg;        // first byte of the segment
+    long long item;         // global item index (>= total: no more work)
+    int nv;                 // valid elements in the segment
+    int dl;                 // drafted token's index inside the segment, or -1
+    float c;                // inv_temp * log2(e) of the row's model
+    int valid;              // row is read (j < k_n)
+};
+
+// Two-step decode on thread 0: start() does the index arithmetic and issues the token /
+// n_drafted loads; finish() (one iteration later) consumes them, so no load latency sits in
+// front of the per-item barrier.
+struct ItemDecode {
+    const char *seg;
+    long long item;
+    int nv, j, kn, tok;
+    float c;
+    template <int DT>
+    __device__ __forceinline__ void start(const Params &prm, long long it, long long total) {
+        item = it;
+        seg = nullptr;
+        nv = 0; j = 0; kn = 0; tok = -1; c = 0.0f;
+        if (it >= total) return;
+        const unsigned u = (unsigned)it;                    // total < 2^31 (validated)
+        const unsigned sg = u % (unsigned)prm.nseg;
+        unsigned row = u / (unsigned)prm.nseg;
+        j = (int)(row % (unsigned)prm.K); row /= (unsigned)prm.K;
+        const int n = (int)(row % (unsigned)prm.N); row /= (unsigned)prm.N;
+        const int model = (int)(row & 1u);
+        const int64_t pn = (int64_t)(row >> 1) * prm.N + n;
+        constexpr int kEsz = ItemTraits<DT>::kEsz;
+        const int64_t v0 = (int64_t)sg * kSeg;
+        const char *row_ptr = model == 0 ? prm.lp + ((pn * prm.rpp_p + j) * prm.ld_p) * kEsz
+                                         : prm.lq + ((pn * prm.rpp_q + j) * prm.ld_q) * kEsz;
+        seg = row_ptr + v0 * kEsz;
+        nv = (int)min((int64_t)kSeg, prm.v_len - v0);
+        c = model == 0 ? prm.c_p : prm.c_q;
+        kn = prm.n_drafted ? prm.n_drafted[pn] : prm.K;     // loads issued here ...
+        tok = prm.tokens[pn * prm.K + j] - (int)(prm.v_begin + v0);
+    }
+    __device__ __forceinline__ ItemInfo finish(const Params &prm) const {   // ... used here
+        ItemInfo f;
+        f.item = item;
+        f.seg = seg;
+        f.nv = nv;
+        f.c = c;
+        f.valid = seg != nullptr && kn >= 0 && kn <= prm.K && j < kn;
+        f.dl = (f.valid && tok >= 0 && tok < nv) ? tok : -1;
+        return f;
+    }
+};
+
+// Issue this thread's loads of one decoded item.
+template <int DT>
+__device__ __forceinline__ void load_seg(uint4 (&v)[ItemTraits<DT>::kLoads], const ItemInfo &f) {
+    using T = ItemTraits<DT>;
+    const int tid = threadIdx.x;
+    if (f.nv == kSeg) {
+#pragma unroll
+        for (int i = 0; i < T::kLoads; ++i) v[i] = ld_stream(f.seg + (size_t)(i * kThreads + tid) * 16);
+    } else {
+#pragma unroll
+        for (int i = 0; i < T::kLoads; ++i) {
+            const int e = (i * kThreads + tid) * T::kVec;
+            v[i] = e < f.nv ? ld_stream(f.seg + (size_t)(i * kThreads + tid) * 16)
+                            : make_uint4(T::kNegInf, T::kNegInf, T::kNegInf, T::kNegInf);
+        }
+    }
+}
+
+// grid = min(items, SMs x resident CTAs), block = kThreads; writes prm.part_ws[item].
+// Items are handed out dynamically (first three per CTA static, then an atomic counter read
+// two iterations ahead of use) so that CTAs finish together; every thread keeps the NEXT
+// item's loads in flight while it reduces the current one.
+template <int DT>
+__global__ void __launch_bounds__(kThreads, DT == 1 ? 4 : 2) k_rowstats(const __grid_constant__ Params prm) {
+    using T = ItemTraits<DT>;
+    __shared__ float2 red[2][kWarps];
+    __shared__ float xs[2];
+    __shared__ ItemInfo info[3];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const long long total = 2ll * prm.P * prm.N * prm.K * prm.nseg;
+    long long pending = 0;                                    // thread 0: fetched index
+    ItemDecode dec;                                           // thread 0: decode in flight
+    if (tid < 2) xs[tid] = -INFINITY;
+    if (tid == 0) {
+        SMCSD_TRACE_AT(blockIdx.x & 1023);                      // K1 CTA start
+        ItemDecode d0, d1;
+        d0.template start<DT>(prm, blockIdx.x, total);
+        d1.template start<DT>(prm, (long long)gridDim.x + blockIdx.x, total);
+        dec.template start<DT>(prm, 2ll * gridDim.x + blockIdx.x, total);
+        pending = 3ll * gridDim.x + atomicAdd(prm.work_ctr, 1u);
+        info[0] = d0.finish(prm);
+        info[1] = d1.finish(prm);
+    }
+    __syncthreads();
+    uint4 a[T::kLoads], b[T::kLoads];
+    if (info[0].valid) load_seg<DT>(a, info[0]);
+
+    for (int it = 0;; ++it) {
+        const ItemInfo &cur = info[it % 3];                   // slots it%3, (it+1)%3 are not
+        if (cur.item >= total) break;                         // written during this iteration
+        const ItemInfo &nxt = info[(it + 1) % 3];
+        if (nxt.valid) load_seg<DT>(b, nxt);                  // prefetch the next item
+        if (tid == 0) {                                       // scheduler pipeline
+            info[(it + 2) % 3] = dec.finish(prm);
+            dec.template start<DT>(prm, pending, total);
+            if (pending < total) pending = 3ll * gridDim.x + atomicAdd(prm.work_ctr, 1u);
+        }
+        const int par = it & 1;
+        if (cur.valid) reduce_item<DT>(a, cur.nv, cur.c, cur.dl, red[par], &xs[par]);
+        __syncthreads();
+        if (warp == 0) {
+            // fixed-order (tree) merge of the 8 warp partials on lanes 0..7
+            float4 out = make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
+            if (cur.valid) {
+                const float2 rw = lane < kWarps ? red[par][lane] : make_float2(-INFINITY, 0.0f);
+                float M = rw.x;
+                M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 4));
+                M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
+                M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
+                float t = lane < kWarps ? rw.y * (rw.x == M ? 1.0f : ex2_approx(rw.x - M)) : 0.0f;
+                t += __shfl_xor_sync(0xffffffffu, t, 4);
+                t += __shfl_xor_sync(0xffffffffu, t, 2);
+                t += __shfl_xor_sync(0xffffffffu, t, 1);
+                out = make_float4(M, t, xs[par], 0.0f);
+            }
+            if (lane == 0) {
+                xs[par] = -INFINITY;                          // re-armed for item it + 2
+                prm.part_ws[cur.item] = out;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < T::kLoads; ++i) a[i] = b[i];
+    }
+    if (tid == 0) SMCSD_TRACE_AT(1024 + (blockIdx.x & 1023));    // K1 CTA done
+    pdl_trigger();
+}
+
+// Merge a row's parts in fixed index order: M = max m_i, S = sum s_i 2^(m_i - M), X = max x_i.
+// Up to 16 parts are loaded at once (one L2 round trip).
 __device__ __forceinline__ float4 merge_parts(const float4 *parts, int64_t stride, int count) {
-    float M = -INFINITY;
+    constexpr int kC = 16;
+    float M = -INFINITY, S = 0.0f, X = -INFINITY;
+    if (count <= kC) {
+        float3 q[kC];
+#pragma unroll
+        for (int i = 0; i < kC; ++i) {
+            if (i < count) {
+                const float4 t = __ldcg(&parts[i * stride]);
+                q[i] = make_float3(t.x, t.y, t.z);
+            } else {
+                q[i] = make_float3(-INFINITY, 0.0f, -INFINITY);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kC; ++i) M = fmaxf(M, q[i].x);
+#pragma unroll
+        for (int i = 0; i < kC; ++i) {
+            if (i < count) {
+                S += q[i].y * (q[i].x == M ? 1.0f : ex2_approx(q[i].x - M));
+                X = fmaxf(X, q[i].z);
+            }
+        }
+        return make_float4(M, S, X, 0.0f);
+    }
     for (int i = 0; i < count; ++i) M = fmaxf(M, __ldcg(&parts[i * stride]).x);
-    float S = 0.0f, X = -INFINITY;
     for (int i = 0; i < count; ++i) {
         const float4 q = __ldcg(&parts[i * stride]);
         S += q.y * (q.x == M ? 1.0f : ex2_approx(q.x - M));
@@ -185,71 +351,116 @@ __device__ __forceinline__ float4 merge_parts(const float4 *parts, int64_t strid
     return make_float4(M, S, X, 0.0f);
 }
 
-__device__ __forceinline__ int drafted_len(const Params &prm, int64_t pn) {
-    return prm.n_drafted ? prm.n_drafted[pn] : prm.K;
+
+// S2, phase A: merged {M, S, X} of every row of prompt p into rowstat[0 .. 2NK).  Chunks of
+// 256 rows x 16 parts are read with coalesced 16-byte loads (16 per thread in flight), staged in
+// shared memory (row pitch 17 float4: conflict-free), then thread t merges row t of the chunk
+// in part order (online rescale across part chunks when a row has more than 16 parts).
+constexpr int kStagePitch = 17;
+constexpr size_t kStageBytes = (size_t)kThreads * kStagePitch * sizeof(float4);
+
+__device__ __forceinline__ void tail_rowstats(const Params &prm, int p, float4 *rowstat, float4 *stage) {
+    const int tid = threadIdx.x;
+    const int rows = 2 * prm.N * prm.K, np_all = prm.nparts;
+    const int64_t gbase = (int64_t)p * rows;
+    for (int r0 = 0; r0 < rows; r0 += kThreads) {
+        const int cr = min(kThreads, rows - r0);
+        float M = -INFINITY, S = 0.0f, X = -INFINITY;
+        for (int pc = 0; pc < np_all; pc += 16) {
+            const int np = min(16, np_all - pc);
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+                const int e = tid + kThreads * kk, r = e >> 4, i = e & 15;
+                if (r < cr && i < np)
+                    stage[r * kStagePitch + i] =
+                        __ldcg(&prm.parts[(gbase + r0 + r) * prm.part_row_stride + (int64_t)(pc + i) * prm.part_seg_stride]);
+            }
+            __syncthreads();
+            if (tid < cr) {
+                const float4 *row = stage + tid * kStagePitch;
+                float Mc = -INFINITY;
+                for (int i = 0; i < np; ++i) Mc = fmaxf(Mc, row[i].x);
+                const float Mn = fmaxf(M, Mc);
+                S = S * (M == Mn ? 1.0f : ex2_approx(M - Mn));
+                for (int i = 0; i < np; ++i) {
+                    const float4 q = row[i];
+                    S += q.y * (q.x == Mn ? 1.0f : ex2_approx(q.x - Mn));
+                    X = fmaxf(X, q.z);
+                }
+                M = Mn;
+            }
+            __syncthreads();
+        }
+        if (tid < cr) rowstat[r0 + tid] = make_float4(M, S, X, 0.0f);
+    }
 }
 
-// ------------------------------------------------------------------------------------------
-// Tail state in shared memory (N <= kTailMaxN) for the fused path and smcsd_resample.
-// ------------------------------------------------------------------------------------------
-struct TailSmem {
-    double e[kTailMaxN];
-    double C[kTailMaxN];
-    float lam[kTailMaxN];
-    int o[kTailMaxN];
-    float2 red[kWarps];
-    float fred[kWarps];
-    int wtot[kWarps + 1];
-    uint32_t st;
-    int do_res, degenerate, ties;
-    double S, U, M;
-};
-
-// S2 for every row of prompt p: ell -> ell_ws (+ optional fp32 outputs); flags into sh_st.
-__device__ void tail_rows(const Params &prm, int p, uint32_t *sh_st) {
-    const int N = prm.N, K = prm.K;
-    const int64_t rows = 2ll * N * K;
+// S2, phase B + per-row part of S3.  Thread pairs (2q, 2q+1) take the target and draft rows of
+// (particle n, position j), q = n*K + j: ell from rowstat, then term[q] = alpha*ell^p - ell^q
+// (fp64); NaN marks an invalid pair (flag already raised).  term is shared memory when
+// term_smem != nullptr, else prm.ell_ws (global, L2).
+__device__ __forceinline__ void tail_scores(const Params &prm, int p, const float4 *rowstat, double *term_smem,
+                                            uint32_t *sh_st) {
+    const int N = prm.N, K = prm.K, tid = threadIdx.x;
+    const int NK = N * K, rows = 2 * NK;
+    double *term_g = prm.ell_ws + (int64_t)p * NK;
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     uint32_t st = 0;
-    for (int64_t rl = threadIdx.x; rl < rows; rl += kThreads) {
-        const int j = (int)(rl % K);
-        const int n = (int)((rl / K) % N);
-        const int model = (int)(rl / ((int64_t)N * K));
+    for (int base = 0; base < rows; base += kThreads) {      // uniform trip count per warp
+        const int r2 = base + tid;
+        const bool active = r2 < rows;
+        const int model = r2 & 1;
+        const int q = r2 >> 1;
+        const int n = active ? q / K : 0, j = active ? q - (q / K) * K : 0;
         const int64_t pn = (int64_t)p * N + n;
-        const int64_t r = (int64_t)p * rows + rl;           // global row index
-        const int kn = drafted_len(prm, pn);
         double ell = 0.0;
-        if (kn >= 0 && kn <= K && j < kn) {
+        bool valid = false;
+        if (active) {
+            const int kn = drafted_len(prm, pn);
             const int64_t d = prm.tokens[pn * K + j];
-            if (d < 0 || d >= prm.V) {
+            const float4 m = rowstat[model * NK + q];
+            valid = kn >= 0 && kn <= K && j < kn;
+            if (!valid) {
+                ell = 0.0;
+            } else if (d < 0 || d >= prm.V) {
                 st |= ST_BAD_TOKEN;
-                ell = __longlong_as_double(0x7ff8000000000000ll);
+                ell = qnan;
+            } else if (!isfinite(m.x) || !isfinite(m.y)) {
+                st |= ST_NONFINITE;
+                ell = qnan;
             } else {
-                const float4 q = merge_parts(prm.parts + r * prm.part_row_stride,
-                                             prm.part_seg_stride, prm.nparts);
-                if (!isfinite(q.x) || !isfinite(q.y)) {
-                    st |= ST_NONFINITE;
-                    ell = __longlong_as_double(0x7ff8000000000000ll);
-                } else {
-                    // ell = (x - m - log2 s) * ln 2   (natural log of the softmax at d)
-                    ell = __dmul_rn(__dsub_rn(__dsub_rn((double)q.z, (double)q.x), log2((double)q.y)), kLn2);
-                }
+                // ell = (x - m - log2 s) * ln 2  (natural log of the softmax at d); s in [1, V]
+                ell = __dmul_rn(__dsub_rn(__dsub_rn((double)m.z, (double)m.x), (double)log2f(m.y)), kLn2);
             }
+            float *outp = model == 0 ? prm.logp_tok : prm.logq_tok;
+            if (outp) outp[pn * K + j] = (float)ell;
         }
-        __stcg(&prm.ell_ws[r], ell);
-        float *outp = model == 0 ? prm.logp_tok : prm.logq_tok;
-        if (outp) outp[pn * K + j] = (float)ell;
+        const double other = __shfl_xor_sync(0xffffffffu, ell, 1);
+        if (active && model == 0 && valid) {
+            const double lp = ell, lq = other;
+            double term;
+            if (isnan(lp) || isnan(lq)) {
+                term = qnan;
+            } else if (lq == -INFINITY) {
+                st |= ST_NOT_ABSCONT;
+                term = qnan;
+            } else {
+                term = __dsub_rn(__dmul_rn(prm.alpha, lp), lq);
+            }
+            if (term_smem) term_smem[q] = term;
+            else __stcg(&term_g[q], term);
+        }
     }
     if (st) atomicOr(sh_st, st);
 }
 
-// S3 for particle n of prompt p: returns lam' (fp32); flags OR-ed into *st.
-__device__ __forceinline__ float reweight_particle(const Params &prm, int p, int n, float neglogN,
-                                                   uint32_t *st) {
+// Rest of S3 for particle n: lam' = fl32(prev + sum_{j<k_n} term_j) in j order.
+__device__ __forceinline__ float tail_reweight(const Params &prm, int p, int n, const double *term_smem,
+                                               float prev, uint32_t *st) {
     const int N = prm.N, K = prm.K;
     const int64_t pn = (int64_t)p * N + n;
-    const int64_t rows = 2ll * N * K;
-    const double *ellp = prm.ell_ws + (int64_t)p * rows + (int64_t)n * K;
-    const double *ellq = ellp + (int64_t)N * K;
+    const double *tg = prm.ell_ws + (int64_t)p * N * K + (int64_t)n * K;
+    const double *ts = term_smem ? term_smem + (int64_t)n * K : nullptr;
     int kn = drafted_len(prm, pn);
     bool bad = false;
     if (kn < 0 || kn > K) {
@@ -258,18 +469,8 @@ __device__ __forceinline__ float reweight_particle(const Params &prm, int p, int
         kn = 0;
     }
     double delta = 0.0;
-    for (int j = 0; j < kn; ++j) {
-        const double lp = __ldcg(&ellp[j]), lq = __ldcg(&ellq[j]);
-        if (isnan(lp) || isnan(lq)) {
-            bad = true;                                      // flag already raised in S2
-        } else if (lq == -INFINITY) {
-            *st |= ST_NOT_ABSCONT;
-            bad = true;
-        } else {
-            delta = __dadd_rn(delta, __dsub_rn(__dmul_rn(prm.alpha, lp), lq));
-        }
-    }
-    const float prev = prm.logw_prev ? prm.logw_prev[pn] : neglogN;
+    for (int j = 0; j < kn; ++j) delta = __dadd_rn(delta, ts ? ts[j] : __ldcg(&tg[j]));
+    if (isnan(delta)) bad = true;                           // an invalid pair (flag raised in S2)
     if (isnan(prev) || prev == INFINITY) {
         *st |= ST_NONFINITE;
         bad = true;
@@ -277,25 +478,54 @@ __device__ __forceinline__ float reweight_particle(const Params &prm, int p, int
     return bad ? -INFINITY : (float)__dadd_rn((double)prev, delta);
 }
 
-// S4-S7 for prompt p from lam[0..N) (smem).  All threads call.  resample_mode = false: S4 only.
-__device__ void normalise_resample(const Params &prm, int p, bool resample_mode, TailSmem &sh) {
-    const int N = prm.N, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// ------------------------------------------------------------------------------------------
+// S4-S7 for prompt p from sh.lam[0..N), executed by warp 0 alone (warp-synchronous: no block
+// barriers on the critical path).  Lane l owns particles [l*B, min(N, (l+1)*B)), B = ceil(N/32).
+// All threads may call; warps other than 0 return at once.  The caller synchronises after.
+// ------------------------------------------------------------------------------------------
+struct TailSmem {
+    double e[kTailMaxN];
+    double C[kTailMaxN];
+    float lam[kTailMaxN];
+    int o[kTailMaxN];
+    int ex[kTailMaxN];          // E list: source of the i-th extra copy
+    uint32_t st;
+    double U;                   // systematic uniform (drawn before the predecessor finishes)
+    float reset;                // fl32(-ln N)
+};
+
+// Weight-independent tail inputs: U = word0(Philox4x32-10(...)) * 2^-32 and fl32(-ln N).
+// Called by thread 0 before griddepcontrol.wait so they overlap the predecessor kernel.
+__device__ __forceinline__ void tail_prologue(const Params &prm, int p, TailSmem &sh) {
+    uint32_t x;
+    if (prm.uniforms) {
+        x = prm.uniforms[p];
+    } else {
+        const uint64_t g = (uint64_t)(prm.prompt_base + p);
+        const uint4 r = philox4x32_10(
+            make_uint4((uint32_t)prm.step, (uint32_t)(prm.step >> 32), (uint32_t)g, 0u),
+            make_uint2((uint32_t)prm.seed, (uint32_t)(prm.seed >> 32)));
+        x = r.x;
+    }
+    sh.U = (double)x * 2.3283064365386962890625e-10;          // 2^-32, exact
+    sh.reset = (float)(-log((double)prm.N));
+}
+
+__device__ __forceinline__ void normalise_resample(const Params &prm, int p, bool resample_mode, TailSmem &sh) {
+    if (threadIdx.x >= 32) return;
+    const unsigned FULL = 0xffffffffu;
+    const int N = prm.N, lane = threadIdx.x;
+    const int B = (N + 31) >> 5;
+    const int b0 = min(N, lane * B), b1 = min(N, b0 + B);
     const int64_t base = (int64_t)p * N;
+    double U = sh.U;
+    SMCSD_PHASE(0);
     // ---- S4: M = max lam (order-free), e_n = exp(lam_n - M)
     float mloc = -INFINITY;
-    for (int n = tid; n < N; n += kThreads) mloc = fmaxf(mloc, sh.lam[n]);
-    mloc = warp_max(mloc);
-    if (lane == 0) sh.fred[warp] = mloc;
-    __syncthreads();
-    if (tid == 0) {
-        float M = sh.fred[0];
-        for (int w = 1; w < kWarps; ++w) M = fmaxf(M, sh.fred[w]);
-        sh.M = (double)M;
-        sh.degenerate = M == -INFINITY;
-    }
-    __syncthreads();
-    if (sh.degenerate) {
-        for (int n = tid; n < N; n += kThreads) {
+    for (int n = b0; n < b1; ++n) mloc = fmaxf(mloc, sh.lam[n]);
+    const double M = (double)warp_max(mloc);
+    if (M == -INFINITY) {                                     // degenerate prompt
+        for (int n = b0; n < b1; ++n) {
             if (prm.wnorm) prm.wnorm[base + n] = 0.0f;
             if (resample_mode) {
                 prm.ancestors[base + n] = n;
@@ -304,7 +534,7 @@ __device__ void normalise_resample(const Params &prm, int p, bool resample_mode,
                 prm.logw_out[base + n] = sh.lam[n];
             }
         }
-        if (tid == 0) {
+        if (lane == 0) {
             sh.st |= ST_DEGENERATE;
             if (prm.lse) prm.lse[p] = -INFINITY;
             if (prm.ess) prm.ess[p] = 0.0;
@@ -315,65 +545,58 @@ __device__ void normalise_resample(const Params &prm, int p, bool resample_mode,
         }
         return;
     }
-    for (int n = tid; n < N; n += kThreads) sh.e[n] = exp(__dsub_rn((double)sh.lam[n], sh.M));
-    __syncthreads();
-    if (tid == 0) {
-        // sequential fp64 prefix and sum of squares (reading G6): same order as the oracle
+    SMCSD_PHASE(1);
+    for (int n = b0; n < b1; ++n) sh.e[n] = exp(__dsub_rn((double)sh.lam[n], M));
+    __syncwarp();
+    SMCSD_PHASE(2);
+    // sequential fp64 prefix and sum of squares in particle order (reading G6): one lane
+    double S = 0.0, ess = 0.0;
+    int do_res = 0;
+    if (lane == 0) {
         double acc = 0.0, sq = 0.0;
         for (int m = 0; m < N; ++m) {
-            acc = __dadd_rn(acc, sh.e[m]);
+            const double e = sh.e[m];
+            acc = __dadd_rn(acc, e);
+            sq = __dadd_rn(sq, __dmul_rn(e, e));
             sh.C[m] = acc;
         }
-        for (int m = 0; m < N; ++m) sq = __dadd_rn(sq, __dmul_rn(sh.e[m], sh.e[m]));
-        const double S = acc;
-        const double ess = __ddiv_rn(__dmul_rn(S, S), sq);
-        sh.S = S;
-        if (prm.lse) prm.lse[p] = __dadd_rn(sh.M, log(S));
+        S = acc;
+        ess = __ddiv_rn(__dmul_rn(S, S), sq);
+        do_res = resample_mode && ess < prm.eta;
         if (prm.ess) prm.ess[p] = ess;
-        sh.do_res = resample_mode && ess < prm.eta;
-        if (sh.do_res) {
-            uint32_t x;
-            if (prm.uniforms) {
-                x = prm.uniforms[p];
-            } else {
-                const uint64_t g = (uint64_t)(prm.prompt_base + p);
-                const uint4 r = philox4x32_10(
-                    make_uint4((uint32_t)prm.step, (uint32_t)(prm.step >> 32), (uint32_t)g, 0u),
-                    make_uint2((uint32_t)prm.seed, (uint32_t)(prm.seed >> 32)));
-                x = r.x;
-            }
-            sh.U = (double)x * 2.3283064365386962890625e-10;   // 2^-32, exact
-        }
-        sh.ties = 0;
+        if (prm.lse) prm.lse[p] = __dadd_rn(M, log(S));
     }
-    __syncthreads();
-    const double S = sh.S;
+    SMCSD_PHASE(3);
+    S = __shfl_sync(FULL, S, 0);
+    do_res = __shfl_sync(FULL, do_res, 0);
+    __syncwarp();
     if (prm.wnorm)
-        for (int n = tid; n < N; n += kThreads) prm.wnorm[base + n] = (float)__ddiv_rn(sh.e[n], S);
+        for (int n = b0; n < b1; ++n) prm.wnorm[base + n] = (float)__ddiv_rn(sh.e[n], S);
     if (!resample_mode) return;
-    if (!sh.do_res) {
-        for (int n = tid; n < N; n += kThreads) {
+    if (!do_res) {
+        for (int n = b0; n < b1; ++n) {
             prm.ancestors[base + n] = n;
             if (prm.offspring) prm.offspring[base + n] = 1;
             if (prm.slot_src) prm.slot_src[base + n] = n;
             prm.logw_out[base + n] = sh.lam[n];
         }
-        if (tid == 0) {
+        if (lane == 0) {
             prm.resampled[p] = 0;
             if (prm.n_ties) prm.n_ties[p] = 0;
         }
         return;
     }
-    // ---- S6: systematic ancestors by inverse CDF
-    for (int m = tid; m < N; m += kThreads) {
+    SMCSD_PHASE(4);
+    // ---- S6: systematic ancestors by inverse CDF: C_m = P_m / S, u_n = (n + U) / N
+    for (int m = b0; m < b1; ++m) {
         sh.C[m] = __ddiv_rn(sh.C[m], S);
         sh.o[m] = 0;
     }
-    __syncthreads();
-    const double U = sh.U;
+    __syncwarp();
+    SMCSD_PHASE(5);
     const double tie = 9.094947017729282379150390625e-13;     // 2^-40
     int ties = 0;
-    for (int n = tid; n < N; n += kThreads) {
+    for (int n = b0; n < b1; ++n) {
         const double u = __ddiv_rn(__dadd_rn((double)n, U), (double)N);
         int lo = 0, hi = N;                                     // a = #{m : C_m <= u}
         while (lo < hi) {
@@ -386,125 +609,130 @@ __device__ void normalise_resample(const Params &prm, int p, bool resample_mode,
         for (int m = a - 1; m >= 0 && fabs(__dsub_rn(u, sh.C[m])) <= tie; --m) ++ties;
         for (int m = a; m < N && fabs(__dsub_rn(u, sh.C[m])) <= tie; ++m) ++ties;
     }
-    if (ties) atomicAdd(&sh.ties, ties);
-    __syncthreads();
-    // ---- S7 reset and per-particle outputs
-    const float reset = (float)(-log((double)N));
-    for (int n = tid; n < N; n += kThreads) {
-        if (prm.offspring) prm.offspring[base + n] = sh.o[n];
-        prm.logw_out[base + n] = reset;
+    __syncwarp();
+    SMCSD_PHASE(6);
+    // ---- in-place slot plan (G14): dead slots (o = 0, ascending) take the extra copies
+    // (source m repeated o_m - 1 times, ascending m).  Per-lane block totals + warp scans.
+    int dead_l = 0, extra_l = 0;
+    for (int m = b0; m < b1; ++m) {
+        const int o = sh.o[m];
+        dead_l += o == 0;
+        extra_l += o > 1 ? o - 1 : 0;
     }
-    if (tid == 0) {
+    int dead_x = dead_l, extra_x = extra_l;                     // inclusive scans
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        const int dv = __shfl_up_sync(FULL, dead_x, s), ev = __shfl_up_sync(FULL, extra_x, s);
+        if (lane >= s) { dead_x += dv; extra_x += ev; }
+    }
+    int d_rank = dead_x - dead_l, x_pos = extra_x - extra_l;   // exclusive
+    for (int m = b0; m < b1; ++m) {
+        const int o = sh.o[m];
+        for (int c = 1; c < o; ++c) sh.ex[x_pos++] = m;
+    }
+    ties = __reduce_add_sync(FULL, ties);
+    __syncwarp();
+    SMCSD_PHASE(7);
+    const float reset = sh.reset;                              // S7
+    for (int m = b0; m < b1; ++m) {
+        const int o = sh.o[m];
+        if (prm.offspring) prm.offspring[base + m] = o;
+        if (prm.slot_src) prm.slot_src[base + m] = o != 0 ? m : sh.ex[d_rank++];
+        prm.logw_out[base + m] = reset;
+    }
+    if (lane == 0) {
         prm.resampled[p] = 1;
-        if (prm.n_ties) prm.n_ties[p] = sh.ties;
-        if (prm.slot_src) {
-            // in-place plan (G14): dead slots ascending <- extra copies, ascending source
-            int32_t *plan = prm.slot_src + base;
-            int src = 0, left = 0;
-            for (int m = 0; m < N; ++m) {
-                if (sh.o[m] != 0) {
-                    plan[m] = m;
-                    continue;
-                }
-                while (left == 0) {
-                    if (sh.o[src] >= 2) left = sh.o[src] - 1;
-                    if (left == 0) ++src;
-                }
-                plan[m] = src;
-                if (--left == 0) ++src;
-            }
-        }
+        if (prm.n_ties) prm.n_ties[p] = ties;
     }
+    SMCSD_PHASE(8);
 }
 
-// Whole tail for prompt p: S2, S3, then S4 (MODE_WEIGHTS) or S4-S7 (MODE_STEP).  N <= kTailMaxN.
-__device__ void tail_prompt(const Params &prm, int p, bool resample_mode, TailSmem &sh) {
-    const int N = prm.N, tid = threadIdx.x;
-    if (tid == 0) sh.st = 0;
-    __syncthreads();
-    tail_rows(prm, p, &sh.st);
-    __syncthreads();
+// K2: tail for prompt p = blockIdx.x: S2, S3, then S4 (weights) or S4-S7 (step).
+// Launched with PDL after K1 (or after nothing, for the combine path): the prior weights are
+// prefetched before griddepcontrol.wait.  N <= kTailMaxN.  kSmem: the per-row statistics
+// (2NK <= kRowStatSmem) and S3 terms (NK <= 2 kTailMaxN) live in shared memory, so every
+// tail access has a compile-time address space; otherwise they go through the workspace.
+template <bool kSmem>
+__global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Params prm, int resample_mode) {
+    __shared__ TailSmem sh;
+    extern __shared__ float4 dyn_smem[];                      // [stage][rowstat (kSmem)]
+    float4 *stage = dyn_smem, *rowstat_smem = dyn_smem + kThreads * kStagePitch;
+    const int p = blockIdx.x, N = prm.N, tid = threadIdx.x;
     const float neglogN = (float)(-log((double)N));
+    float prev_v[kTailMaxN / kThreads];                       // prefetched before the wait
+#pragma unroll
+    for (int i = 0; i < kTailMaxN / kThreads; ++i) {
+        const int n = tid + i * kThreads;
+        prev_v[i] = (n < N && prm.logw_prev) ? prm.logw_prev[(int64_t)p * N + n] : neglogN;
+    }
+    if (tid == 0) {
+        sh.st = 0;
+        if (resample_mode) tail_prologue(prm, p, sh);
+    }
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2048);             // tail CTA resident
+    pdl_wait();
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2049);             // predecessor complete
+    if (tid == 0 && p == 0 && prm.work_ctr) *prm.work_ctr = 0u;   // re-arm K1's counter
+    __syncthreads();
+    const int rows = 2 * N * prm.K;
+    if (kSmem) tail_rowstats(prm, p, rowstat_smem, stage);
+    else       tail_rowstats(prm, p, prm.rowstat_ws + (int64_t)p * rows, stage);
+    __syncthreads();
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2053);             // S2 phase A done
+    if (kSmem) tail_scores(prm, p, rowstat_smem, sh.e, &sh.st);
+    else       tail_scores(prm, p, prm.rowstat_ws + (int64_t)p * rows, nullptr, &sh.st);
+    __syncthreads();
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);             // S2 done
     uint32_t st = 0;
-    for (int n = tid; n < N; n += kThreads) {
-        const float lam = reweight_particle(prm, p, n, neglogN, &st);
-        sh.lam[n] = lam;
-        const int64_t pn = (int64_t)p * N + n;
-        if (prm.logw_pre) prm.logw_pre[pn] = lam;
-        if (!resample_mode) prm.logw_out[pn] = lam;
+    float lam_v[kTailMaxN / kThreads];
+#pragma unroll
+    for (int i = 0; i < kTailMaxN / kThreads; ++i) {
+        const int n = tid + i * kThreads;
+        lam_v[i] = n < N ? tail_reweight(prm, p, n, kSmem ? sh.e : nullptr, prev_v[i], &st) : 0.0f;
+    }
+    __syncthreads();                                            // term (aliasing e/C) is dead now
+#pragma unroll
+    for (int i = 0; i < kTailMaxN / kThreads; ++i) {
+        const int n = tid + i * kThreads;
+        if (n < N) {
+            sh.lam[n] = lam_v[i];
+            const int64_t pn = (int64_t)p * N + n;
+            if (prm.logw_pre) prm.logw_pre[pn] = lam_v[i];
+            if (!resample_mode) prm.logw_out[pn] = lam_v[i];
+        }
     }
     if (st) atomicOr(&sh.st, st);
     __syncthreads();
-    normalise_resample(prm, p, resample_mode, sh);
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2051);             // S3 done
+    normalise_resample(prm, p, resample_mode != 0, sh);
     __syncthreads();
     if (tid == 0) prm.status[p] = sh.st;
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);             // S4-S7 done
+    pdl_trigger();
 }
 
-// ------------------------------------------------------------------------------------------
-// K1 (+ fused tail).  grid = P * 2 * N * K * nseg, block = kThreads.
-// ------------------------------------------------------------------------------------------
-template <int DT, int MODE>
-__global__ void __launch_bounds__(kThreads) k_rowstats(const __grid_constant__ Params prm) {
-    __shared__ float2 red[kWarps];
-    __shared__ int s_last;
-    const int64_t item = blockIdx.x;
-    const int seg = (int)(item % prm.nseg);
-    const int64_t row = item / prm.nseg;                    // ((p*2 + model)*N + n)*K + j
-    const int K = prm.K, N = prm.N;
-    const int j = (int)(row % K);
-    const int n = (int)((row / K) % N);
-    const int model = (int)((row / ((int64_t)K * N)) % 2);
-    const int p = (int)(row / (2ll * K * N));
-    const int64_t pn = (int64_t)p * N + n;
-    const int kn = drafted_len(prm, pn);
-    if (kn >= 0 && kn <= K && j < kn) {
-        const char *base = model == 0
-            ? prm.lp + ((pn * prm.rpp_p + j) * prm.ld_p) * (DT == 1 ? 2 : 4)
-            : prm.lq + ((pn * prm.rpp_q + j) * prm.ld_q) * (DT == 1 ? 2 : 4);
-        const float c = model == 0 ? prm.c_p : prm.c_q;
-        const int64_t d = prm.tokens[pn * K + j];
-        const float4 r = segment_stats<DT>(base, prm.v_len, seg, c, d - prm.v_begin, red);
-        if (threadIdx.x == 0) prm.part_ws[item] = r;
-    } else if (threadIdx.x == 0) {
-        prm.part_ws[item] = make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
+// K2 (TP partial path): merge each row's segment partials into one {m, s, x, 0}.  grid = P.
+__global__ void __launch_bounds__(kThreads) k_merge_rows(const __grid_constant__ Params prm) {
+    pdl_wait();
+    if (threadIdx.x == 0 && blockIdx.x == 0) *prm.work_ctr = 0u;   // re-arm K1's counter
+    const int64_t rows = 2ll * prm.N * prm.K;
+    const int64_t p = blockIdx.x;
+    for (int64_t rl = threadIdx.x; rl < rows; rl += kThreads) {
+        const int64_t r = p * rows + rl;
+        prm.partials_out[r] = merge_parts(prm.part_ws + r * prm.nseg, 1, prm.nseg);
     }
-    if constexpr (MODE == MODE_ROWS_ONLY) return;
-
-    // ---- completion counting: the last CTA of prompt p runs its tail (threadFenceReduction)
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const unsigned total = (unsigned)(2ll * N * K * prm.nseg);
-        const unsigned prev = atomicAdd(&prm.counters[p], 1u);
-        s_last = prev == total - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-
-    if constexpr (MODE == MODE_PARTIAL) {
-        const int64_t rows = 2ll * N * K;
-        for (int64_t rl = threadIdx.x; rl < rows; rl += kThreads) {
-            const int64_t r = (int64_t)p * rows + rl;
-            prm.partials_out[r] = merge_parts(prm.part_ws + r * prm.nseg, 1, prm.nseg);
-        }
-    } else {
-        __shared__ TailSmem sh;
-        tail_prompt(prm, p, MODE == MODE_STEP, sh);
-    }
-    if (threadIdx.x == 0) prm.counters[p] = 0u;             // graph-replay safe
-}
-
-// Tail-only kernel, grid = P: S2-S7 from prm.parts (combine path, N <= kTailMaxN).
-__global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Params prm, int resample_mode) {
-    __shared__ TailSmem sh;
-    tail_prompt(prm, blockIdx.x, resample_mode != 0, sh);
+    pdl_trigger();
 }
 
 // S4-S7 from fp32 log-weights, grid = P (smcsd_resample).
 __global__ void __launch_bounds__(kThreads) k_resample(const __grid_constant__ Params prm) {
     __shared__ TailSmem sh;
     const int p = blockIdx.x, N = prm.N;
-    if (threadIdx.x == 0) sh.st = 0;
+    if (threadIdx.x == 0) {
+        sh.st = 0;
+        tail_prologue(prm, p, sh);
+    }
+    pdl_wait();
     __syncthreads();
     uint32_t st = 0;
     for (int n = threadIdx.x; n < N; n += kThreads) {
@@ -520,6 +748,7 @@ __global__ void __launch_bounds__(kThreads) k_resample(const __grid_constant__ P
     normalise_resample(prm, p, true, sh);
     __syncthreads();
     if (threadIdx.x == 0) prm.status[p] = sh.st;
+    pdl_trigger();
 }
 
 // Large-N weights path (N > kTailMaxN): S2+S3 in parallel, S4 serial over global workspace.
@@ -530,14 +759,21 @@ __global__ void __launch_bounds__(kThreads) k_tail_large(const __grid_constant__
     const int p = blockIdx.x, N = prm.N, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)p * N;
     if (tid == 0) s_st = 0;
+    pdl_wait();
+    if (tid == 0 && p == 0) *prm.work_ctr = 0u;               // re-arm K1's counter
     __syncthreads();
-    tail_rows(prm, p, &s_st);
+    extern __shared__ float4 dyn_smem[];
+    float4 *rowstat = prm.rowstat_ws + (int64_t)p * 2 * N * prm.K;
+    tail_rowstats(prm, p, rowstat, dyn_smem);
+    __syncthreads();
+    tail_scores(prm, p, rowstat, nullptr, &s_st);
     __syncthreads();
     const float neglogN = (float)(-log((double)N));
     uint32_t st = 0;
     float mloc = -INFINITY;
     for (int n = tid; n < N; n += kThreads) {
-        const float lam = reweight_particle(prm, p, n, neglogN, &st);
+        const float lam = tail_reweight(prm, p, n, nullptr,
+                                        prm.logw_prev ? prm.logw_prev[base + n] : neglogN, &st);
         __stcg(&prm.lam_ws[base + n], lam);
         prm.logw_out[base + n] = lam;
         if (prm.logw_pre) prm.logw_pre[base + n] = lam;
@@ -568,9 +804,9 @@ __global__ void __launch_bounds__(kThreads) k_tail_large(const __grid_constant__
     __syncthreads();
     if (tid == 0) {
         double acc = 0.0, sq = 0.0;
-        for (int m = 0; m < N; ++m) acc = __dadd_rn(acc, __ldcg(&prm.e_ws[base + m]));
         for (int m = 0; m < N; ++m) {
             const double e = __ldcg(&prm.e_ws[base + m]);
+            acc = __dadd_rn(acc, e);
             sq = __dadd_rn(sq, __dmul_rn(e, e));
         }
         s_S = acc;
@@ -611,6 +847,7 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex(const __grid_constant__
     const int p = (int)(op % prm.P);
     const int64_t o = op / prm.P;
     const int32_t *idx = prm.idx + (int64_t)p * N;
+    pdl_wait();                                                // src_index from the tail kernel
 
     // ---- copy plan for prompt p: destinations grouped by source (counting sort)
     for (int n = tid; n < N; n += kThreads) cnt[n] = 0;

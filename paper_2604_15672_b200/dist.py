@@ -52,6 +52,8 @@ def max_over_ranks(value: float, device, group=None) -> float:
     """Max of a host float over ranks (timing: the slowest rank sets the step time)."""
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
         return value
+    if dist.get_backend(group) == "gloo":
+        device = "cpu"
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())

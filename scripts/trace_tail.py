@@ -1,0 +1,43 @@
+#!/usr/bin/env python
+"""Timeline of fused smcsd_step calls (cfg2 by default) from the %globaltimer trace build.
+Usage (GPU): python paper_2604_15672_b200/build.py --trace && python scripts/trace_tail.py"""
+import ctypes
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["SMCSD_LIB_OVERRIDE"] = os.path.join(ROOT, "paper_2604_15672_b200", "libsmcsd_trace.so")
+import torch  # noqa: E402
+import paper_2604_15672_b200 as smc  # noqa: E402
+import synth  # noqa: E402
+
+P, N, K, V = int(os.environ.get("P", 1)), int(os.environ.get("N", 16)), 8, 128256
+dev = torch.device("cuda")
+ring = [synth.lm_logits(P, N, K, V, device=dev, seed=100 + r) for r in range(6)]
+lib = ctypes.CDLL(smc.lib_path)
+buf = (ctypes.c_ulonglong * 4096)()
+flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)
+for it in range(12):
+    lp, lq, tok = ring[it % 6]
+    flush_sum = flush.sum()  # read-only L2 flush (no dirty lines)
+    torch.cuda.synchronize()
+    lib.smcsd_trace_read(buf, 4096)
+    out = smc.smcsd_step(lp, lq, tok, V=V, eta=math.inf, step=it, fields=())
+    torch.cuda.synchronize()
+lib.smcsd_trace_read(buf, 4096)
+t = list(buf)
+starts = [x for x in t[:1024] if x]
+ends = [x for x in t[1024:2048] if x]
+t0 = min(starts)
+us = lambda x: (x - t0) / 1e3
+s = sorted(us(x) for x in starts)
+e = sorted(us(x) for x in ends)
+print(f"K1 CTAs {len(starts)}: start spread {s[-1]:.2f} us; done min {e[0]:.2f} median {e[len(e)//2]:.2f} "
+      f"p90 {e[int(len(e)*0.9)]:.2f} max {e[-1]:.2f} us")
+names = {2060: "S2 t0: loads issue", 2061: "S2 t0: parts merged", 2062: "S2 t0: ell", 2063: "S2 t0: loop done",
+         2048: "tail CTA resident", 2049: "tail after pdl_wait", 2050: "after S2", 2051: "after S3",
+         2052: "after S4-S7"}
+for k, nm in names.items():
+    print(f"{nm:22s} {us(t[k]):8.2f} us")
