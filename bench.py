@@ -280,6 +280,7 @@ def run_ours(args, rank, world, local):
         wl.kv = None
         torch.cuda.empty_cache()
         secondary["cfg4"] = measure_cfg4(dev, rank, world, hbm_peak)
+        secondary["cfg5"] = measure_cfg5(dev, rank, world, hbm_peak)
         if world == 1:
             secondary["cfg3"] = measure_cfg3(dev, hbm_peak)
 
@@ -365,6 +366,66 @@ def measure_cfg4(dev, rank, world, hbm_peak, steps=20, warmup=3):
             "unit": "prompt-steps/s", "ms_per_step": round(ms, 4), "bytes_per_rank": int(byts),
             "achieved_gbs_per_rank": round(gbs, 1), "frac_of_measured": round(gbs / hbm_peak, 4),
             "frac_of_8tbs": round(gbs / 8000.0, 4)}
+
+
+def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
+    """configs[4]: V=128256 vocab-sharded over the ranks (TP), P=1, N=64, K=8 bf16.  A step is
+    smcsd_weights_partial on this rank's columns -> all_gather of 16 B per row (S10, NCCL) ->
+    smcsd_weights_combine (rank-order merge: identical on every rank) -> smcsd_resample (same
+    Philox counter everywhere, no communication).  At one GPU the shard is the whole row."""
+    import torch
+    import paper_2604_15672_b200 as smc
+    import synth
+    from paper_2604_15672_b200.dist import exchange_partials_into, vocab_shard
+    P, N, K, V = 1, 64, 8, 128256
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, device=dev,
+                                  seed=synth.GEN_SEED_BASE + 5)   # same on every rank
+    b, e = vocab_shard(V, world, rank)
+    w = e - b
+    ldw = synth.padded_ld(w, torch.bfloat16)
+    sp = torch.zeros((P, N, K + 1, ldw), dtype=torch.bfloat16, device=dev)
+    sq = torch.zeros((P, N, K, ldw), dtype=torch.bfloat16, device=dev)
+    sp[..., :w] = lp[..., b:e]
+    sq[..., :w] = lq[..., b:e]
+    del lp, lq
+    torch.cuda.empty_cache()
+    ws_p, ws_c = smc.Workspace(dev), smc.Workspace(dev)
+    part = torch.empty((P, 2, N, K, 4), dtype=torch.float32, device=dev)
+    gathered = torch.empty((world, P, 2, N, K, 4), dtype=torch.float32, device=dev)
+    logw = synth.uniform_prior(P, N, device=dev)
+    oc = smc.Outputs(logw=torch.empty_like(logw))
+    orr = smc.Outputs(logw=logw)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    phases = [0.0, 0.0, 0.0]
+
+    def fn(i, ev=None):
+        if ev: ev[0].record()
+        smc.smcsd_weights_partial(sp, sq, tok, v_begin=b, v_len=w, partials=part, workspace=ws_p)
+        if ev: ev[1].record()
+        if world > 1:
+            exchange_partials_into(gathered, part)
+        else:
+            gathered[0].copy_(part)
+        if ev: ev[2].record()
+        smc.smcsd_weights_combine(gathered, tok, V=V, logw_prev=logw, out=oc, fields=(), workspace=ws_c)
+        smc.smcsd_resample(oc.logw, eta=math.inf, step=i, out=orr, fields=())
+        if ev: ev[3].record()
+    ms = _time_steps(fn, steps, warmup, world, dev)        # overlapped steps: the metric
+    for i in range(steps):                                 # phase breakdown (events per phase)
+        fn(i, ev)
+        torch.cuda.synchronize()
+        for j in range(3):
+            phases[j] += ev[j].elapsed_time(ev[j + 1])
+    byts = 2 * N * K * w * 2
+    part_ms = phases[0] / steps
+    gbs = byts / (part_ms / 1e3) / 1e9
+    return {"workload": f"cfg5: P=1, N={N}, K={K}, V={V} bf16 vocab-sharded {world}-way "
+                        f"({w} columns on this rank); partial -> all_gather -> combine -> resample",
+            "steps_per_s": round(1e3 / ms, 1), "ms_per_step": round(ms, 4),
+            "note": "per-step phase times are measured with a host sync per step (not overlapped)",
+            "partial_ms": round(part_ms, 4), "exchange_ms": round(phases[1] / steps, 4),
+            "combine_resample_ms": round(phases[2] / steps, 4), "bytes_per_rank": int(byts),
+            "partial_achieved_gbs": round(gbs, 1), "partial_frac_of_measured": round(gbs / hbm_peak, 4)}
 
 
 def measure_cfg3(dev, hbm_peak, steps=5, warmup=2):

@@ -45,6 +45,10 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     extra = ["-DSMCSD_TRACE"] if trace else []
     if trace and os.environ.get("SMCSD_TRACE_TWICE"):
         extra.append("-DSMCSD_TRACE_TWICE")
+    if trace and os.environ.get("SMCSD_EXTRA_DEFS"):                  # timing experiments
+        extra += ["-D" + x for x in os.environ["SMCSD_EXTRA_DEFS"].split(",")]
+        lib = lib.replace("_trace.so", "_" + os.environ["SMCSD_EXTRA_DEFS"].replace(",", "_").lower() + ".so")
+        tmp = lib + ".tmp"
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC,
            "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
     res = subprocess.run(cmd, capture_output=True, text=True)

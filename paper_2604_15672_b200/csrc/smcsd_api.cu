@@ -74,11 +74,11 @@ smcsd_rc check_logits(const void *lp, int64_t ld_p, int rpp_p, const void *lq, i
 // predecessor in the stream drains; it calls griddepcontrol.wait before touching that
 // predecessor's outputs.
 template <typename... KArgs, typename... Args>
-smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaStream_t st,
-                    Args &&...args) {
+smcsd_rc launch_pdl_b(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaStream_t st,
+                      unsigned block, Args &&...args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -90,21 +90,29 @@ smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaSt
                ? SMCSD_OK : SMCSD_ECUDA;
 }
 
-// K1 persistent grid: SMs x resident CTAs, capped by the number of work items.
+template <typename... KArgs, typename... Args>
+smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaStream_t st,
+                    Args &&...args) {
+    return launch_pdl_b(kernel, grid, smem, st, (unsigned)kThreads, std::forward<Args>(args)...);
+}
+
+// K1 persistent grid: SMs x resident CTAs (shared-memory ring), capped by the work items.
 template <int DT>
 smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     static int ctas[64] = {0};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
+    const size_t smem = rowstats_smem_bytes<DT>();
     if (ctas[dev] == 0) {
         int occ = 0, sms = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT>, kThreads, 0) != cudaSuccess ||
+        if (cudaFuncSetAttribute(k_rowstats<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT>, kK1Threads, smem) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || occ < 1)
             return SMCSD_ECUDA;
         ctas[dev] = occ * sms;
     }
     const int64_t grid = items < ctas[dev] ? items : ctas[dev];
-    return launch_pdl(k_rowstats<DT>, (unsigned)grid, 0, st, prm);
+    return launch_pdl_b(k_rowstats<DT>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
 }
 
 // K2 tail: one CTA per prompt; the per-row S2 statistics live in dynamic shared memory when
@@ -114,24 +122,33 @@ smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
     if (!attr_set[dev]) {
-        const int big = (int)(kStageBytes + kRowStatSmem * sizeof(float4));
+        const int big = (int)(kTailStageBytes + kRowStatSmem * sizeof(float4));
         if (cudaFuncSetAttribute(k_tail<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tail<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tail_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStageBytes) != cudaSuccess)
+            cudaFuncSetAttribute(k_tail<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tail_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess)
             return SMCSD_ECUDA;
         attr_set[dev] = true;
     }
     const int64_t rows = 2ll * prm.N * prm.K;
-    if (prm.N > kTailMaxN) return launch_pdl(k_tail_large, (unsigned)prm.P, kStageBytes, st, prm);
+    if (prm.N > kTailMaxN) return launch_pdl(k_tail_large, (unsigned)prm.P, kTailStageBytes, st, prm);
     if (rows <= kRowStatSmem && prm.N * (int64_t)prm.K <= 2 * kTailMaxN)
-        return launch_pdl(k_tail<true>, (unsigned)prm.P, kStageBytes + (size_t)rows * sizeof(float4), st,
+        return launch_pdl(k_tail<true>, (unsigned)prm.P, kTailStageBytes + (size_t)rows * sizeof(float4), st,
                           prm, resample_mode);
-    return launch_pdl(k_tail<false>, (unsigned)prm.P, kStageBytes, st, prm, resample_mode);
+    return launch_pdl(k_tail<false>, (unsigned)prm.P, kTailStageBytes, st, prm, resample_mode);
 }
 
 smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st) {
     return dtype == SMCSD_BF16 ? launch_rowstats_dt<1>(prm, items, st)
                                : launch_rowstats_dt<0>(prm, items, st);
+}
+
+// Magic multiplier for division by d (1 <= d < 2^31): x / d == (x * mg) >> (32 + sh) for
+// every x < 2^31, with sh = ceil(log2 d) and mg = ceil(2^(32+sh) / d) < 2^33.
+void set_magic(int d, unsigned long long &mg, int &sh) {
+    sh = 0;
+    while ((1ll << sh) < d) ++sh;
+    const unsigned __int128 num = (unsigned __int128)1 << (32 + sh);
+    mg = (unsigned long long)((num + (unsigned)d - 1) / (unsigned)d);
 }
 
 // Common Params for the logits entry points.
@@ -149,6 +166,10 @@ Params logits_params(const void *lp, int64_t ld_p, int rpp_p, const void *lq, in
     prm.c_p = (float)((double)tp * kLog2e);
     prm.c_q = (float)((double)tq * kLog2e);
     prm.alpha = 1.0;
+    set_magic(prm.nseg, prm.mg_nseg, prm.sh_nseg);
+    set_magic(K, prm.mg_K, prm.sh_K);
+    set_magic(N, prm.mg_N, prm.sh_N);
+    prm.x_from_logits = 1;
     return prm;
 }
 
@@ -186,6 +207,7 @@ smcsd_rc smcsd_weights(const void *logits_p, int64_t ld_p, int rows_per_particle
                                rows_per_particle_q, tokens, n_drafted, P, N, K, V, 0, V,
                                inv_temp_p, inv_temp_q);
     prm.alpha = (double)alpha;
+    prm.dtype = dtype;
     prm.logw_prev = logw_prev;
     prm.logw_out = logw_out; prm.logp_tok = logp_tok; prm.logq_tok = logq_tok;
     prm.lse = lse_out; prm.ess = ess_out; prm.wnorm = wnorm_out; prm.status = status;
@@ -246,6 +268,7 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
                                rows_per_particle_q, tokens, n_drafted, P, N, K, V, 0, V,
                                inv_temp_p, inv_temp_q);
     prm.alpha = (double)alpha;
+    prm.dtype = dtype;
     prm.logw_prev = logw_prev;
     prm.eta = (double)eta; prm.seed = seed; prm.step = step; prm.prompt_base = prompt_base;
     prm.uniforms = uniforms;
@@ -279,6 +302,7 @@ smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_
                                rows_per_particle_q, tokens, n_drafted, P, N, K,
                                v_begin + v_len, v_begin, v_len, inv_temp_p, inv_temp_q);
     prm.partials_out = reinterpret_cast<float4 *>(partials);
+    prm.dtype = dtype;
     bind_workspace(prm, workspace, L);
     cudaStream_t st = as_stream(stream);
     rc = launch_rowstats(prm, dtype, 2ll * P * N * K * prm.nseg, st);

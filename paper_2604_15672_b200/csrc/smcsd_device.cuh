@@ -12,9 +12,13 @@ constexpr int kTailMaxN = 1024;          // fused tail / resample keep per-promp
 
 // ---- scalars -------------------------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x) {
+#ifdef SMCSD_EXPERIMENT_NO_EX2          // timing experiment only: wrong numerics
+    return x * 0.5f;
+#else
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+#endif
 }
 
 __device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }

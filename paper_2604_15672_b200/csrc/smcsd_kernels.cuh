@@ -64,6 +64,10 @@ struct Params {
     float *lam_ws;                              // [P*N]   (N > kTailMaxN path)
     double *e_ws, *c_ws;                        // [P*N]
     float4 *rowstat_ws;                         // [P*2*N*K] (rows > kRowStatSmem)
+    unsigned long long mg_nseg, mg_K, mg_N;     // magic multipliers: x / d == (x * mg) >> (32 + sh)
+    int sh_nseg, sh_K, sh_N;
+    int dtype;                                  // 0 fp32, 1 bf16 (logits)
+    int x_from_logits;                          // 1: tail loads t_d from the logits; 0: from parts
     unsigned *work_ctr;                         // K1 dynamic work counter (re-armed by K2)
 };
 
@@ -94,11 +98,23 @@ __device__ __forceinline__ int drafted_len(const Params &prm, int64_t pn) {
     return prm.n_drafted ? prm.n_drafted[pn] : prm.K;
 }
 
-// Reduce one item held in registers: lane 0 of each warp writes red[warp] = {m_w, s_w}; the
-// thread holding the drafted token (local index dl) writes *xs = t_d.
+// t_d = inv_temp * z_d * log2(e) for global token d of row (model, pn, j), or -inf when d is not
+// among this row's columns [v_begin, v_begin + v_len).
+__device__ __forceinline__ float load_x(const Params &prm, int model, int64_t pn, int j, int64_t d) {
+    const int64_t dl = d - prm.v_begin;
+    if (dl < 0 || dl >= prm.v_len) return -INFINITY;
+    const int esz = prm.dtype == 1 ? 2 : 4;
+    const char *row = model == 0 ? prm.lp + ((pn * prm.rpp_p + j) * prm.ld_p) * esz
+                                 : prm.lq + ((pn * prm.rpp_q + j) * prm.ld_q) * esz;
+    const float z = prm.dtype == 1 ? bf16lo(__ldg((const unsigned short *)row + dl))
+                                   : __ldg((const float *)row + dl);
+    return z * (model == 0 ? prm.c_p : prm.c_q);
+}
+
+// Reduce one item held in registers: lane 0 of each warp writes red[warp] = {m_w, s_w}.
 template <int DT>
 __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], int nv, float c,
-                                            int dl, float2 *red, float *xs) {
+                                            float2 *red) {
     using T = ItemTraits<DT>;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (nv < kSeg) {                                          // ragged last segment: mask >= V
@@ -115,19 +131,6 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
                     if (e + k >= nv) w[k] = T::kNegInf;
                 }
             }
-        }
-    }
-    if (dl >= 0 && dl < nv) {                                 // drafted token of this segment
-        const int vi = dl / T::kVec, k = dl % T::kVec;
-        if ((vi % kThreads) == tid) {
-            const int i = vi / kThreads;
-            uint4 w = v[0];
-#pragma unroll
-            for (int q = 1; q < T::kLoads; ++q) if (q == i) w = v[q];
-            const uint32_t word = (DT == 1 ? k >> 1 : k) == 0 ? w.x : (DT == 1 ? k >> 1 : k) == 1 ? w.y
-                                : (DT == 1 ? k >> 1 : k) == 2 ? w.z : w.w;
-            const float z = DT == 1 ? ((k & 1) ? bf16hi(word) : bf16lo(word)) : __uint_as_float(word);
-            *xs = z * c;
         }
     }
     // max over the warp's elements (raw logits; c > 0 so max(z)*c = max(z*c))
@@ -175,58 +178,43 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
     if (lane == 0) red[warp] = make_float2(mw, s);
 }
 
-// Decoded work item (thread 0 decodes, the CTA reads it from shared memory).
+// Unsigned division by a runtime constant d via a precomputed magic number (host computes
+// mg = ceil(2^(32+sh) / d) with sh = ceil(log2 d), < 2^33); exact for x, d < 2^31.
+__device__ __forceinline__ unsigned fastdiv(unsigned x, unsigned long long mg, int sh) {
+    return (unsigned)(((unsigned long long)x * mg) >> (32 + sh));
+}
+
+// Per-item data derived from the item index (every thread, no broadcast).
 struct ItemInfo {
     const char *seg;        // first byte of the segment
-    long long item;         // global item index (>= total: no more work)
     int nv;                 // valid elements in the segment
-    int dl;                 // drafted token's index inside the segment, or -1
     float c;                // inv_temp * log2(e) of the row's model
     int valid;              // row is read (j < k_n)
 };
 
-// Two-step decode on thread 0: start() does the index arithmetic and issues the token /
-// n_drafted loads; finish() (one iteration later) consumes them, so no load latency sits in
-// front of the per-item barrier.
-struct ItemDecode {
-    const char *seg;
-    long long item;
-    int nv, j, kn, tok;
-    float c;
-    template <int DT>
-    __device__ __forceinline__ void start(const Params &prm, long long it, long long total) {
-        item = it;
-        seg = nullptr;
-        nv = 0; j = 0; kn = 0; tok = -1; c = 0.0f;
-        if (it >= total) return;
-        const unsigned u = (unsigned)it;                    // total < 2^31 (validated)
-        const unsigned sg = u % (unsigned)prm.nseg;
-        unsigned row = u / (unsigned)prm.nseg;
-        j = (int)(row % (unsigned)prm.K); row /= (unsigned)prm.K;
-        const int n = (int)(row % (unsigned)prm.N); row /= (unsigned)prm.N;
-        const int model = (int)(row & 1u);
-        const int64_t pn = (int64_t)(row >> 1) * prm.N + n;
-        constexpr int kEsz = ItemTraits<DT>::kEsz;
-        const int64_t v0 = (int64_t)sg * kSeg;
-        const char *row_ptr = model == 0 ? prm.lp + ((pn * prm.rpp_p + j) * prm.ld_p) * kEsz
-                                         : prm.lq + ((pn * prm.rpp_q + j) * prm.ld_q) * kEsz;
-        seg = row_ptr + v0 * kEsz;
-        nv = (int)min((int64_t)kSeg, prm.v_len - v0);
-        c = model == 0 ? prm.c_p : prm.c_q;
-        kn = prm.n_drafted ? prm.n_drafted[pn] : prm.K;     // loads issued here ...
-        tok = prm.tokens[pn * prm.K + j] - (int)(prm.v_begin + v0);
-    }
-    __device__ __forceinline__ ItemInfo finish(const Params &prm) const {   // ... used here
-        ItemInfo f;
-        f.item = item;
-        f.seg = seg;
-        f.nv = nv;
-        f.c = c;
-        f.valid = seg != nullptr && kn >= 0 && kn <= prm.K && j < kn;
-        f.dl = (f.valid && tok >= 0 && tok < nv) ? tok : -1;
-        return f;
-    }
-};
+template <int DT>
+__device__ __forceinline__ ItemInfo item_info(const Params &prm, long long item) {
+    ItemInfo f;
+    const unsigned u = (unsigned)item;                      // total < 2^31 (validated)
+    unsigned row = fastdiv(u, prm.mg_nseg, prm.sh_nseg);
+    const int seg = (int)(u - row * (unsigned)prm.nseg);
+    const unsigned r1 = fastdiv(row, prm.mg_K, prm.sh_K);
+    const int j = (int)(row - r1 * (unsigned)prm.K);
+    const unsigned r2 = fastdiv(r1, prm.mg_N, prm.sh_N);
+    const int n = (int)(r1 - r2 * (unsigned)prm.N);
+    const int model = (int)(r2 & 1u);
+    const int64_t pn = (int64_t)(r2 >> 1) * prm.N + n;
+    const int kn = prm.n_drafted ? prm.n_drafted[pn] : prm.K;
+    f.valid = kn >= 0 && kn <= prm.K && j < kn;
+    constexpr int kEsz = ItemTraits<DT>::kEsz;
+    const int64_t v0 = (int64_t)seg * kSeg;
+    const char *row_ptr = model == 0 ? prm.lp + ((pn * prm.rpp_p + j) * prm.ld_p) * kEsz
+                                     : prm.lq + ((pn * prm.rpp_q + j) * prm.ld_q) * kEsz;
+    f.seg = row_ptr + v0 * kEsz;
+    f.nv = (int)min((int64_t)kSeg, prm.v_len - v0);
+    f.c = model == 0 ? prm.c_p : prm.c_q;
+    return f;
+}
 
 // Issue this thread's loads of one decoded item.
 template <int DT>
@@ -246,70 +234,141 @@ __device__ __forceinline__ void load_seg(uint4 (&v)[ItemTraits<DT>::kLoads], con
     }
 }
 
-// grid = min(items, SMs x resident CTAs), block = kThreads; writes prm.part_ws[item].
-// Items are handed out dynamically (first three per CTA static, then an atomic counter read
-// two iterations ahead of use) so that CTAs finish together; every thread keeps the NEXT
-// item's loads in flight while it reduces the current one.
+// K1 kernel: warp-specialised bulk-copy (TMA) pipeline, no CTA-wide barriers.
+//   warp 8 (producer, lane 0): takes items in global order from an atomic counter (first item
+//     per CTA static), decodes them, and streams each item's bytes into a kStages-deep
+//     shared-memory ring with cp.async.bulk (completion counted on full[s] in bytes);
+//   warps 0..7 (consumers): wait full[s], reduce the item from shared memory, write their
+//     warp partial; the last consumer warp to finish an item (shared-memory counter) merges
+//     the 8 partials in fixed tree order, stores {m, s, -inf, 0}, and every warp releases the
+//     slot on empty[s].
+// The drafted-token logit is not taken here (the tail loads it).  grid = min(items, SMs x
+// resident CTAs), block = kK1Threads, dynamic smem = kStages x stage + bookkeeping.
+constexpr int kK1Threads = kThreads + 32;
+#ifndef SMCSD_K1_STAGES
+#define SMCSD_K1_STAGES 2
+#endif
+#ifndef SMCSD_K1_MINB
+#define SMCSD_K1_MINB 6
+#endif
+constexpr int kStages = SMCSD_K1_STAGES;
+
+struct StageMeta {
+    long long item;         // global item index, or -1: no more work
+    int nv;                 // valid elements in the segment
+    float c;                // inv_temp * log2(e) of the row's model
+    int valid;              // row is read (j < k_n)
+};
+
 template <int DT>
-__global__ void __launch_bounds__(kThreads, DT == 1 ? 4 : 2) k_rowstats(const __grid_constant__ Params prm) {
+constexpr size_t rowstats_smem_bytes() {
+    return (size_t)kStages * kSeg * ItemTraits<DT>::kEsz            // data ring
+         + kStages * (2 * sizeof(uint64_t) + sizeof(StageMeta) + kWarps * sizeof(float2) + 16);
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_rowstats(const __grid_constant__ Params prm) {
     using T = ItemTraits<DT>;
-    __shared__ float2 red[2][kWarps];
-    __shared__ float xs[2];
-    __shared__ ItemInfo info[3];
+    constexpr uint32_t kStageBytes = (uint32_t)kSeg * T::kEsz;
+    extern __shared__ __align__(128) char smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+    uint64_t *empty = full + kStages;
+    StageMeta *meta = reinterpret_cast<StageMeta *>(empty + kStages);
+    float2 *red = reinterpret_cast<float2 *>(meta + kStages);       // [kStages][kWarps]
+    int *done = reinterpret_cast<int *>(red + kStages * kWarps);    // [kStages]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long total = 2ll * prm.P * prm.N * prm.K * prm.nseg;
-    long long pending = 0;                                    // thread 0: fetched index
-    ItemDecode dec;                                           // thread 0: decode in flight
-    if (tid < 2) xs[tid] = -INFINITY;
+
     if (tid == 0) {
         SMCSD_TRACE_AT(blockIdx.x & 1023);                      // K1 CTA start
-        ItemDecode d0, d1;
-        d0.template start<DT>(prm, blockIdx.x, total);
-        d1.template start<DT>(prm, (long long)gridDim.x + blockIdx.x, total);
-        dec.template start<DT>(prm, 2ll * gridDim.x + blockIdx.x, total);
-        pending = 3ll * gridDim.x + atomicAdd(prm.work_ctr, 1u);
-        info[0] = d0.finish(prm);
-        info[1] = d1.finish(prm);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWarps);
+            done[s] = 0;
+        }
+        fence_mbar_init();
     }
     __syncthreads();
-    uint4 a[T::kLoads], b[T::kLoads];
-    if (info[0].valid) load_seg<DT>(a, info[0]);
 
-    for (int it = 0;; ++it) {
-        const ItemInfo &cur = info[it % 3];                   // slots it%3, (it+1)%3 are not
-        if (cur.item >= total) break;                         // written during this iteration
-        const ItemInfo &nxt = info[(it + 1) % 3];
-        if (nxt.valid) load_seg<DT>(b, nxt);                  // prefetch the next item
-        if (tid == 0) {                                       // scheduler pipeline
-            info[(it + 2) % 3] = dec.finish(prm);
-            dec.template start<DT>(prm, pending, total);
-            if (pending < total) pending = 3ll * gridDim.x + atomicAdd(prm.work_ctr, 1u);
-        }
-        const int par = it & 1;
-        if (cur.valid) reduce_item<DT>(a, cur.nv, cur.c, cur.dl, red[par], &xs[par]);
-        __syncthreads();
-        if (warp == 0) {
-            // fixed-order (tree) merge of the 8 warp partials on lanes 0..7
-            float4 out = make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
-            if (cur.valid) {
-                const float2 rw = lane < kWarps ? red[par][lane] : make_float2(-INFINITY, 0.0f);
-                float M = rw.x;
-                M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 4));
-                M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
-                M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
-                float t = lane < kWarps ? rw.y * (rw.x == M ? 1.0f : ex2_approx(rw.x - M)) : 0.0f;
-                t += __shfl_xor_sync(0xffffffffu, t, 4);
-                t += __shfl_xor_sync(0xffffffffu, t, 2);
-                t += __shfl_xor_sync(0xffffffffu, t, 1);
-                out = make_float4(M, t, xs[par], 0.0f);
+    if (warp == kWarps) {
+        // ------------------------------------------------------------------ producer
+        if (lane == 0) {
+            long long item = blockIdx.x;
+            for (long long it = 0;; ++it) {
+                const int s = (int)(it % kStages);
+                mbar_wait(&empty[s], (uint32_t)(((it / kStages) & 1) ^ 1));   // slot released
+                StageMeta m;
+                m.item = item < total ? item : -1;
+                m.valid = 0;
+                m.nv = 0;
+                m.c = 0.0f;
+                const char *src = nullptr;
+                if (item < total) {
+                    const ItemInfo f = item_info<DT>(prm, item);
+                    m.valid = f.valid;
+                    m.nv = f.nv;
+                    m.c = f.c;
+                    src = f.seg;
+                }
+                meta[s] = m;
+                if (m.valid) {
+                    const uint32_t bytes = (uint32_t)(((m.nv + T::kVec - 1) / T::kVec) * 16);
+                    mbar_arrive_expect_tx(&full[s], bytes);
+                    bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
+                } else {
+                    mbar_arrive(&full[s]);                    // metadata only (release)
+                }
+                if (item >= total) break;
+                item = (long long)gridDim.x + atomicAdd(prm.work_ctr, 1u);
             }
-            if (lane == 0) {
-                xs[par] = -INFINITY;                          // re-armed for item it + 2
-                prm.part_ws[cur.item] = out;
-            }
         }
+    } else {
+        // ------------------------------------------------------------------ consumers
+        uint4 v[T::kLoads];
+        for (long long it = 0;; ++it) {
+            const int s = (int)(it % kStages);
+            mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
+            const StageMeta m = meta[s];
+            if (m.item < 0) break;
+            float2 *r = red + s * kWarps;
+            if (m.valid) {
+                const char *sl = smem + (size_t)s * kStageBytes;
 #pragma unroll
-        for (int i = 0; i < T::kLoads; ++i) a[i] = b[i];
+                for (int i = 0; i < T::kLoads; ++i)
+                    v[i] = *reinterpret_cast<const uint4 *>(sl + (size_t)(i * kThreads + tid) * 16);
+                reduce_item<DT>(v, m.nv, m.c, r);
+            }
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) {
+                __threadfence_block();                        // red[warp] before the count
+                last = atomicAdd(&done[s], 1) == kWarps - 1;
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                __threadfence_block();
+                // fixed-order (tree) merge of the 8 warp partials on lanes 0..7
+                float4 out = make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
+                if (m.valid) {
+                    const float2 rw = lane < kWarps ? r[lane] : make_float2(-INFINITY, 0.0f);
+                    float M = rw.x;
+                    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 4));
+                    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
+                    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
+                    float t = lane < kWarps ? rw.y * (rw.x == M ? 1.0f : ex2_approx(rw.x - M)) : 0.0f;
+                    t += __shfl_xor_sync(0xffffffffu, t, 4);
+                    t += __shfl_xor_sync(0xffffffffu, t, 2);
+                    t += __shfl_xor_sync(0xffffffffu, t, 1);
+                    out = make_float4(M, t, -INFINITY, 0.0f);
+                }
+                if (lane == 0) {
+                    prm.part_ws[m.item] = out;
+                    done[s] = 0;
+                }
+                __syncwarp();
+            }
+            if (lane == 0) mbar_arrive(&empty[s]);            // this warp is done with slot s
+        }
     }
     if (tid == 0) SMCSD_TRACE_AT(1024 + (blockIdx.x & 1023));    // K1 CTA done
     pdl_trigger();
@@ -357,7 +416,7 @@ __device__ __forceinline__ float4 merge_parts(const float4 *parts, int64_t strid
 // shared memory (row pitch 17 float4: conflict-free), then thread t merges row t of the chunk
 // in part order (online rescale across part chunks when a row has more than 16 parts).
 constexpr int kStagePitch = 17;
-constexpr size_t kStageBytes = (size_t)kThreads * kStagePitch * sizeof(float4);
+constexpr size_t kTailStageBytes = (size_t)kThreads * kStagePitch * sizeof(float4);
 
 __device__ __forceinline__ void tail_rowstats(const Params &prm, int p, float4 *rowstat, float4 *stage) {
     const int tid = threadIdx.x;
@@ -400,7 +459,7 @@ __device__ __forceinline__ void tail_rowstats(const Params &prm, int p, float4 *
 // (fp64); NaN marks an invalid pair (flag already raised).  term is shared memory when
 // term_smem != nullptr, else prm.ell_ws (global, L2).
 __device__ __forceinline__ void tail_scores(const Params &prm, int p, const float4 *rowstat, double *term_smem,
-                                            uint32_t *sh_st) {
+                                            uint32_t *sh_st, float x_pre) {
     const int N = prm.N, K = prm.K, tid = threadIdx.x;
     const int NK = N * K, rows = 2 * NK;
     double *term_g = prm.ell_ws + (int64_t)p * NK;
@@ -418,8 +477,10 @@ __device__ __forceinline__ void tail_scores(const Params &prm, int p, const floa
         if (active) {
             const int kn = drafted_len(prm, pn);
             const int64_t d = prm.tokens[pn * K + j];
-            const float4 m = rowstat[model * NK + q];
+            float4 m = rowstat[model * NK + q];
             valid = kn >= 0 && kn <= K && j < kn;
+            if (prm.x_from_logits)                            // prefetched for the first rows
+                m.z = base == 0 ? x_pre : (valid && d >= 0 && d < prm.V ? load_x(prm, model, pn, j, d) : -INFINITY);
             if (!valid) {
                 ell = 0.0;
             } else if (d < 0 || d >= prm.V) {
@@ -669,6 +730,14 @@ __global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Param
         sh.st = 0;
         if (resample_mode) tail_prologue(prm, p, sh);
     }
+    float x_pre = -INFINITY;                                  // drafted-token logit of row tid:
+    if (prm.x_from_logits && tid < 2 * N * prm.K) {           // an input, so read before the wait
+        const int model = tid & 1, q = tid >> 1, n = q / prm.K, j = q - n * prm.K;
+        const int64_t pn = (int64_t)p * N + n;
+        const int kn = drafted_len(prm, pn);
+        const int64_t d = prm.tokens[pn * prm.K + j];
+        if (kn >= 0 && kn <= prm.K && j < kn && d >= 0 && d < prm.V) x_pre = load_x(prm, model, pn, j, d);
+    }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2048);             // tail CTA resident
     pdl_wait();
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2049);             // predecessor complete
@@ -679,8 +748,8 @@ __global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Param
     else       tail_rowstats(prm, p, prm.rowstat_ws + (int64_t)p * rows, stage);
     __syncthreads();
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2053);             // S2 phase A done
-    if (kSmem) tail_scores(prm, p, rowstat_smem, sh.e, &sh.st);
-    else       tail_scores(prm, p, prm.rowstat_ws + (int64_t)p * rows, nullptr, &sh.st);
+    if (kSmem) tail_scores(prm, p, rowstat_smem, sh.e, &sh.st, x_pre);
+    else       tail_scores(prm, p, prm.rowstat_ws + (int64_t)p * rows, nullptr, &sh.st, x_pre);
     __syncthreads();
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);             // S2 done
     uint32_t st = 0;
@@ -719,7 +788,14 @@ __global__ void __launch_bounds__(kThreads) k_merge_rows(const __grid_constant__
     const int64_t p = blockIdx.x;
     for (int64_t rl = threadIdx.x; rl < rows; rl += kThreads) {
         const int64_t r = p * rows + rl;
-        prm.partials_out[r] = merge_parts(prm.part_ws + r * prm.nseg, 1, prm.nseg);
+        float4 m = merge_parts(prm.part_ws + r * prm.nseg, 1, prm.nseg);
+        const int K = prm.K, N = prm.N;
+        const int model = (int)(rl / ((int64_t)N * K)), q = (int)(rl % ((int64_t)N * K));
+        const int n = q / K, j = q % K;
+        const int64_t pn = p * N + n;
+        const int kn = drafted_len(prm, pn);
+        m.z = (kn >= 0 && kn <= K && j < kn) ? load_x(prm, model, pn, j, prm.tokens[pn * K + j]) : -INFINITY;
+        prm.partials_out[r] = m;
     }
     pdl_trigger();
 }
@@ -766,7 +842,15 @@ __global__ void __launch_bounds__(kThreads) k_tail_large(const __grid_constant__
     float4 *rowstat = prm.rowstat_ws + (int64_t)p * 2 * N * prm.K;
     tail_rowstats(prm, p, rowstat, dyn_smem);
     __syncthreads();
-    tail_scores(prm, p, rowstat, nullptr, &s_st);
+    float x_pre = -INFINITY;
+    if (prm.x_from_logits && tid < 2 * N * prm.K) {
+        const int model = tid & 1, q = tid >> 1, n = q / prm.K, j = q - n * prm.K;
+        const int64_t pn = (int64_t)p * N + n;
+        const int kn = drafted_len(prm, pn);
+        const int64_t d = prm.tokens[pn * prm.K + j];
+        if (kn >= 0 && kn <= prm.K && j < kn && d >= 0 && d < prm.V) x_pre = load_x(prm, model, pn, j, d);
+    }
+    tail_scores(prm, p, rowstat, nullptr, &s_st, x_pre);
     __syncthreads();
     const float neglogN = (float)(-log((double)N));
     uint32_t st = 0;

@@ -41,11 +41,20 @@ def exchange_partials(partials: torch.Tensor, group=None) -> torch.Tensor:
     world = dist.get_world_size(group)
     out = torch.empty((world,) + tuple(partials.shape), dtype=partials.dtype,
                       device=partials.device)
-    if partials.is_cuda:
-        dist.all_gather_into_tensor(out, partials.contiguous(), group=group)
-    else:  # gloo (CPU tests of this host logic)
-        dist.all_gather(list(out.unbind(0)), partials.contiguous(), group=group)
+    exchange_partials_into(out, partials, group)
     return out
+
+
+def exchange_partials_into(out: torch.Tensor, partials: torch.Tensor, group=None) -> None:
+    """S10 into a preallocated [G][...] buffer (NCCL all_gather_into_tensor over NVLink; gloo
+    stages through host memory -- functional tests only)."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, partials.contiguous(), group=group)
+        return
+    host = partials.detach().cpu().contiguous()
+    bufs = [torch.empty_like(host) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(bufs, host, group=group)
+    out.copy_(torch.stack(bufs))
 
 
 def max_over_ranks(value: float, device, group=None) -> float:

@@ -1,0 +1,42 @@
+#!/usr/bin/env python
+"""Device time of smcsd_step / smcsd_weights_partial on cfg4 / cfg2 / cfg5 shapes (events over
+back-to-back calls).  SMCSD_LIB_OVERRIDE selects a library variant.  Usage: python scripts/time_k1.py"""
+import math, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2604_15672_b200 as smc
+import synth
+
+dev = torch.device("cuda")
+which = os.environ.get("WHICH", "cfg4,cfg2,cfg5").split(",")
+
+def t(fn, reps, warm=3):
+    for i in range(warm): fn(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(reps): fn(i)
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+res = {}
+if "cfg4" in which:
+    lp, lq, tok = synth.lm_logits(64, 32, 8, 128256, device=dev, seed=4)
+    ws = smc.Workspace(dev); out = smc.Outputs()
+    ms = t(lambda i: smc.smcsd_step(lp, lq, tok, V=128256, step=i, out=out, fields=(), workspace=ws), 10)
+    res["cfg4"] = (ms, 8405475328 / ms / 1e6)
+    del lp, lq, tok; torch.cuda.empty_cache()
+if "cfg2" in which:
+    ring = [synth.lm_logits(1, 16, 8, 128256, device=dev, seed=10 + r) for r in range(6)]
+    ws = smc.Workspace(dev); out = smc.Outputs()
+    ms = t(lambda i: smc.smcsd_step(*ring[i % 6], V=128256, step=i, out=out, fields=(), workspace=ws), 60)
+    res["cfg2"] = (ms, 65667776 / ms / 1e6)
+    del ring; torch.cuda.empty_cache()
+if "cfg5" in which:
+    lp, lq, tok = synth.lm_logits(1, 64, 8, 128256, device=dev, seed=5)
+    ws = smc.Workspace(dev)
+    part = torch.empty((1, 2, 64, 8, 4), device=dev)
+    ms = t(lambda i: smc.smcsd_weights_partial(lp, lq, tok, v_begin=0, v_len=128256, partials=part, workspace=ws), 30)
+    res["cfg5-partial-G1"] = (ms, 262668288 / ms / 1e6)
+for k, (ms, gbs) in res.items():
+    print(f"{os.path.basename(smc.lib_path):24s} {k:16s} {ms * 1e3:9.2f} us  {gbs:8.1f} GB/s  ({gbs / 6543.7:.3f} of measured)")
