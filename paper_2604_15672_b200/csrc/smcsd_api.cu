@@ -22,7 +22,7 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 struct WsLayout {
-    size_t ctr, parts, ell, lam, e, c, rowstat, total;
+    size_t ctr, pctr, pst, parts, ell, lam, e, c, rowstat, total;
 };
 
 WsLayout ws_layout(int P, int N, int K, int64_t v_len) {
@@ -31,6 +31,8 @@ WsLayout ws_layout(int P, int N, int K, int64_t v_len) {
     const size_t nseg = (size_t)cdiv(v_len < 1 ? 1 : v_len, kSeg);
     size_t off = 0;
     L.ctr = off;      off += 256;
+    L.pctr = off;     off += align256((size_t)P * sizeof(unsigned));
+    L.pst = off;      off += align256((size_t)P * sizeof(uint32_t));
     L.parts = off;    off += align256(rows * nseg * sizeof(float4));
     L.ell = off;      off += align256(rows * sizeof(double));
     L.lam = off;      off += align256((size_t)P * N * sizeof(float));
@@ -50,6 +52,8 @@ void bind_workspace(Params &prm, void *ws, const WsLayout &L) {
     prm.c_ws = reinterpret_cast<double *>(b + L.c);
     prm.rowstat_ws = reinterpret_cast<float4 *>(b + L.rowstat);
     prm.work_ctr = reinterpret_cast<unsigned *>(b + L.ctr);
+    prm.prompt_ctr = reinterpret_cast<unsigned *>(b + L.pctr);
+    prm.st_ws = reinterpret_cast<uint32_t *>(b + L.pst);
 }
 
 bool valid_temp(float t) { return std::isfinite(t) && t > 0.0f; }
@@ -117,24 +121,27 @@ smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
 
 // K2 tail: one CTA per prompt; the per-row S2 statistics live in dynamic shared memory when
 // they fit (k_tail<true>), else in the workspace (k_tail<false>).
-smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
+// One-time (per device) opt-in to the dynamic shared memory the K2 kernels stage through.
+smcsd_rc ensure_tail_attrs() {
     static bool attr_set[64] = {false};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
     if (!attr_set[dev]) {
-        const int big = (int)(kTailStageBytes + kRowStatSmem * sizeof(float4));
-        if (cudaFuncSetAttribute(k_tail<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tail<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tail_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess)
+        if (cudaFuncSetAttribute(k_tail_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess ||
+            cudaFuncSetAttribute(k_merge_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess)
             return SMCSD_ECUDA;
         attr_set[dev] = true;
     }
-    const int64_t rows = 2ll * prm.N * prm.K;
+    return SMCSD_OK;
+}
+
+smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
+    if (ensure_tail_attrs() != SMCSD_OK) return SMCSD_ECUDA;
     if (prm.N > kTailMaxN) return launch_pdl(k_tail_large, (unsigned)prm.P, kTailStageBytes, st, prm);
-    if (rows <= kRowStatSmem && prm.N * (int64_t)prm.K <= 2 * kTailMaxN)
-        return launch_pdl(k_tail<true>, (unsigned)prm.P, kTailStageBytes + (size_t)rows * sizeof(float4), st,
-                          prm, resample_mode);
-    return launch_pdl(k_tail<false>, (unsigned)prm.P, kTailStageBytes, st, prm, resample_mode);
+    const int chunks = (int)cdiv((int64_t)prm.N * prm.K, kPairsPerCta);
+    const int64_t grid = (int64_t)prm.P * chunks;
+    if (grid >= (1ll << 31)) return SMCSD_EINVAL;
+    return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks);
 }
 
 smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st) {
@@ -304,10 +311,13 @@ smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_
     prm.partials_out = reinterpret_cast<float4 *>(partials);
     prm.dtype = dtype;
     bind_workspace(prm, workspace, L);
+    prm.parts = prm.part_ws; prm.part_row_stride = prm.nseg; prm.part_seg_stride = 1;
+    prm.nparts = prm.nseg;
     cudaStream_t st = as_stream(stream);
     rc = launch_rowstats(prm, dtype, 2ll * P * N * K * prm.nseg, st);
     if (rc != SMCSD_OK) return rc;
-    return launch_pdl(k_merge_rows, (unsigned)P, 0, st, prm);
+    if (ensure_tail_attrs() != SMCSD_OK) return SMCSD_ECUDA;
+    return launch_pdl(k_merge_rows, (unsigned)P, kTailStageBytes, st, prm);
 }
 
 smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int32_t *tokens,

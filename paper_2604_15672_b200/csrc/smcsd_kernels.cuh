@@ -69,6 +69,8 @@ struct Params {
     int dtype;                                  // 0 fp32, 1 bf16 (logits)
     int x_from_logits;                          // 1: tail loads t_d from the logits; 0: from parts
     unsigned *work_ctr;                         // K1 dynamic work counter (re-armed by K2)
+    unsigned *prompt_ctr;                       // [P] K2 chunk completion counters
+    uint32_t *st_ws;                            // [P] K2 status accumulation
 };
 
 // ------------------------------------------------------------------------------------------
@@ -708,95 +710,219 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
     SMCSD_PHASE(8);
 }
 
-// K2: tail for prompt p = blockIdx.x: S2, S3, then S4 (weights) or S4-S7 (step).
-// Launched with PDL after K1 (or after nothing, for the combine path): the prior weights are
-// prefetched before griddepcontrol.wait.  N <= kTailMaxN.  kSmem: the per-row statistics
-// (2NK <= kRowStatSmem) and S3 terms (NK <= 2 kTailMaxN) live in shared memory, so every
-// tail access has a compile-time address space; otherwise they go through the workspace.
-template <bool kSmem>
-__global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Params prm, int resample_mode) {
+// K2: the tail, distributed.  grid = P x chunks_per_prompt; CTA (p, c) owns the (particle,
+// position) pairs q in [32c, 32c + 32) of prompt p, i.e. 64 rows (32 target + 32 draft):
+//   S2  16 lanes per row merge the row's parts (coalesced 16-byte loads, fixed 16-lane tree),
+//       ell = (x - m - log2 s) ln 2 with x = t_d read from the logits before the wait;
+//   S3  term_q = alpha ell^p_q - ell^q_q (fp64) -> workspace, status bits -> workspace;
+// then a per-prompt completion counter: the last CTA of the prompt sums the terms in j order
+// (S3), and warp 0 runs S4 (weights) or S4-S7 (step).  Launched with PDL behind K1 (or behind
+// the NCCL exchange for the combine path): inputs are read before griddepcontrol.wait.
+constexpr int kPairsPerCta = 32;
+
+__device__ __forceinline__ float3 lane_premerge(const Params &prm, int64_t grow, int li) {
+    // parts li, li+16, li+32, ... of one row, merged in index order (nparts > 16 only)
+    float M = -INFINITY, S = 0.0f, X = -INFINITY;
+    for (int i = li; i < prm.nparts; i += 16)
+        M = fmaxf(M, __ldcg(&prm.parts[grow * prm.part_row_stride + (int64_t)i * prm.part_seg_stride]).x);
+    for (int i = li; i < prm.nparts; i += 16) {
+        const float4 t = __ldcg(&prm.parts[grow * prm.part_row_stride + (int64_t)i * prm.part_seg_stride]);
+        S += t.y * (t.x == M ? 1.0f : ex2_approx(t.x - M));
+        X = fmaxf(X, t.z);
+    }
+    return make_float3(M, S, X);
+}
+
+__global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Params prm, int resample_mode,
+                                                   int chunks_per_prompt) {
     __shared__ TailSmem sh;
-    extern __shared__ float4 dyn_smem[];                      // [stage][rowstat (kSmem)]
-    float4 *stage = dyn_smem, *rowstat_smem = dyn_smem + kThreads * kStagePitch;
-    const int p = blockIdx.x, N = prm.N, tid = threadIdx.x;
-    const float neglogN = (float)(-log((double)N));
-    float prev_v[kTailMaxN / kThreads];                       // prefetched before the wait
-#pragma unroll
-    for (int i = 0; i < kTailMaxN / kThreads; ++i) {
-        const int n = tid + i * kThreads;
-        prev_v[i] = (n < N && prm.logw_prev) ? prm.logw_prev[(int64_t)p * N + n] : neglogN;
+    __shared__ float4 rs[2 * kPairsPerCta];
+    __shared__ double ell_s[2 * kPairsPerCta];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int p = blockIdx.x / chunks_per_prompt, c = blockIdx.x - p * chunks_per_prompt;
+    const int N = prm.N, K = prm.K, NK = N * K, rows = 2 * NK;
+    const int q0 = c * kPairsPerCta, nq = min(kPairsPerCta, NK - q0);
+    const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+
+    // ---- inputs (not produced by the predecessor): before the wait
+    int lr_model = 0, lr_q = 0, lr_kn = 0;
+    int64_t lr_pn = 0, lr_d = -1;
+    float x_pre = -INFINITY;
+    const bool row_thread = tid < 2 * kPairsPerCta && (tid & (kPairsPerCta - 1)) < nq;
+    if (row_thread) {
+        lr_model = tid / kPairsPerCta;
+        lr_q = q0 + (tid & (kPairsPerCta - 1));
+        const int n = lr_q / K, j = lr_q - n * K;
+        lr_pn = (int64_t)p * N + n;
+        lr_kn = drafted_len(prm, lr_pn);
+        lr_d = prm.tokens[lr_pn * K + j];
+        if (prm.x_from_logits && lr_kn >= 0 && lr_kn <= K && j < lr_kn && lr_d >= 0 && lr_d < prm.V)
+            x_pre = load_x(prm, lr_model, lr_pn, j, lr_d);
     }
     if (tid == 0) {
         sh.st = 0;
         if (resample_mode) tail_prologue(prm, p, sh);
     }
-    float x_pre = -INFINITY;                                  // drafted-token logit of row tid:
-    if (prm.x_from_logits && tid < 2 * N * prm.K) {           // an input, so read before the wait
-        const int model = tid & 1, q = tid >> 1, n = q / prm.K, j = q - n * prm.K;
-        const int64_t pn = (int64_t)p * N + n;
-        const int kn = drafted_len(prm, pn);
-        const int64_t d = prm.tokens[pn * prm.K + j];
-        if (kn >= 0 && kn <= prm.K && j < kn && d >= 0 && d < prm.V) x_pre = load_x(prm, model, pn, j, d);
-    }
-    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2048);             // tail CTA resident
+    if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2048);      // tail CTA resident
     pdl_wait();
-    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2049);             // predecessor complete
-    if (tid == 0 && p == 0 && prm.work_ctr) *prm.work_ctr = 0u;   // re-arm K1's counter
-    __syncthreads();
-    const int rows = 2 * N * prm.K;
-    if (kSmem) tail_rowstats(prm, p, rowstat_smem, stage);
-    else       tail_rowstats(prm, p, prm.rowstat_ws + (int64_t)p * rows, stage);
-    __syncthreads();
-    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2053);             // S2 phase A done
-    if (kSmem) tail_scores(prm, p, rowstat_smem, sh.e, &sh.st, x_pre);
-    else       tail_scores(prm, p, prm.rowstat_ws + (int64_t)p * rows, nullptr, &sh.st, x_pre);
-    __syncthreads();
-    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);             // S2 done
-    uint32_t st = 0;
-    float lam_v[kTailMaxN / kThreads];
-#pragma unroll
-    for (int i = 0; i < kTailMaxN / kThreads; ++i) {
-        const int n = tid + i * kThreads;
-        lam_v[i] = n < N ? tail_reweight(prm, p, n, kSmem ? sh.e : nullptr, prev_v[i], &st) : 0.0f;
+    if (tid == 0 && blockIdx.x == 0) {
+        SMCSD_TRACE_AT(2049);                                   // predecessor complete
+        if (prm.work_ctr) *prm.work_ctr = 0u;                   // re-arm K1's counter
     }
-    __syncthreads();                                            // term (aliasing e/C) is dead now
+
+    // ---- S2: 16 lanes per row, 16 rows per pass, 64 rows per CTA
+    {
+        const int li = tid & 15, rsub = tid >> 4;
+        float3 q[4];
 #pragma unroll
-    for (int i = 0; i < kTailMaxN / kThreads; ++i) {
-        const int n = tid + i * kThreads;
-        if (n < N) {
-            sh.lam[n] = lam_v[i];
-            const int64_t pn = (int64_t)p * N + n;
-            if (prm.logw_pre) prm.logw_pre[pn] = lam_v[i];
-            if (!resample_mode) prm.logw_out[pn] = lam_v[i];
+        for (int u = 0; u < 4; ++u) {
+            const int lr = rsub + 16 * u;                       // local row: model = lr / 32
+            const int qq = lr & (kPairsPerCta - 1);
+            const int64_t grow = (int64_t)p * rows + (int64_t)(lr / kPairsPerCta) * NK + q0 + qq;
+            q[u] = make_float3(-INFINITY, 0.0f, -INFINITY);
+            if (qq < nq) {
+                if (prm.nparts <= 16) {
+                    if (li < prm.nparts) {
+                        const float4 t = __ldcg(&prm.parts[grow * prm.part_row_stride + (int64_t)li * prm.part_seg_stride]);
+                        q[u] = make_float3(t.x, t.y, t.z);
+                    }
+                } else {
+                    q[u] = lane_premerge(prm, grow, li);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float M = q[u].x, X = q[u].z;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {
+                M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+                X = fmaxf(X, __shfl_xor_sync(0xffffffffu, X, o));
+            }
+            float S = q[u].y * (q[u].x == M ? 1.0f : ex2_approx(q[u].x - M));
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+            if (li == 0) rs[rsub + 16 * u] = make_float4(M, S, X, 0.0f);
         }
     }
-    if (st) atomicOr(&sh.st, st);
     __syncthreads();
-    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2051);             // S3 done
+    // ---- ell per row (thread = local row), then terms per pair
+    uint32_t st = 0;
+    if (row_thread) {
+        const int j = lr_q - (lr_q / K) * K;
+        const bool valid = lr_kn >= 0 && lr_kn <= K && j < lr_kn;
+        const float4 m = rs[tid];
+        const float x = prm.x_from_logits ? x_pre : m.z;
+        double ell = 0.0;
+        if (!valid) {
+            ell = 0.0;
+        } else if (lr_d < 0 || lr_d >= prm.V) {
+            st |= ST_BAD_TOKEN;
+            ell = qnan;
+        } else if (!isfinite(m.x) || !isfinite(m.y)) {
+            st |= ST_NONFINITE;
+            ell = qnan;
+        } else {
+            ell = __dmul_rn(__dsub_rn(__dsub_rn((double)x, (double)m.x), (double)log2f(m.y)), kLn2);
+        }
+        ell_s[tid] = ell;
+        float *outp = lr_model == 0 ? prm.logp_tok : prm.logq_tok;
+        if (outp) outp[lr_pn * K + j] = (float)ell;
+    }
+    __syncthreads();
+    if (tid < nq) {
+        const int qq = q0 + tid, j = qq - (qq / K) * K;
+        const int kn = drafted_len(prm, (int64_t)p * N + qq / K);
+        double term = 0.0;
+        if (kn >= 0 && kn <= K && j < kn) {
+            const double lp = ell_s[tid], lq = ell_s[kPairsPerCta + tid];
+            if (isnan(lp) || isnan(lq)) {
+                term = qnan;
+            } else if (lq == -INFINITY) {
+                st |= ST_NOT_ABSCONT;
+                term = qnan;
+            } else {
+                term = __dsub_rn(__dmul_rn(prm.alpha, lp), lq);
+            }
+        }
+        __stcg(&prm.ell_ws[(int64_t)p * NK + qq], term);
+    }
+    if (st) atomicOr(&prm.st_ws[p], st);
+    if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2053);      // chunk 0 S2 done
+    // ---- completion: the last CTA of the prompt finishes it
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&prm.prompt_ctr[p], 1u) == (unsigned)(chunks_per_prompt - 1);
+    __syncthreads();
+    if (!s_last) {
+        pdl_trigger();
+        return;
+    }
+    __threadfence();
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);
+    // ---- S3: lam' = fl32(prev + sum_{j<k_n} term_j) in j order
+    const double *terms = prm.ell_ws + (int64_t)p * NK;
+    uint32_t st3 = 0;
+    const float neglogN = (float)(-log((double)N));
+    for (int n = tid; n < N; n += kThreads) {
+        const int64_t pn = (int64_t)p * N + n;
+        int kn = drafted_len(prm, pn);
+        bool bad = false;
+        if (kn < 0 || kn > K) {
+            st3 |= ST_BAD_TOKEN;
+            bad = true;
+            kn = 0;
+        }
+        double delta = 0.0;
+        for (int j = 0; j < kn; ++j) delta = __dadd_rn(delta, __ldcg(&terms[n * K + j]));
+        if (isnan(delta)) bad = true;                       // an invalid pair (flag raised in S2)
+        const float prev = prm.logw_prev ? prm.logw_prev[pn] : neglogN;
+        if (isnan(prev) || prev == INFINITY) {
+            st3 |= ST_NONFINITE;
+            bad = true;
+        }
+        const float lam = bad ? -INFINITY : (float)__dadd_rn((double)prev, delta);
+        sh.lam[n] = lam;
+        if (prm.logw_pre) prm.logw_pre[pn] = lam;
+        if (!resample_mode) prm.logw_out[pn] = lam;
+    }
+    if (st3) atomicOr(&sh.st, st3);
+    __syncthreads();
+    if (tid == 0) {
+        sh.st |= __ldcg(&prm.st_ws[p]);                         // flags of every chunk
+        prm.st_ws[p] = 0u;
+        prm.prompt_ctr[p] = 0u;                                  // graph-replay safe
+    }
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2051);
+    __syncthreads();
     normalise_resample(prm, p, resample_mode != 0, sh);
     __syncthreads();
     if (tid == 0) prm.status[p] = sh.st;
-    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);             // S4-S7 done
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);
     pdl_trigger();
 }
 
 // K2 (TP partial path): merge each row's segment partials into one {m, s, x, 0}.  grid = P.
+// Coalesced staged merge (tail_rowstats); x = t_d when the drafted token is in this shard.
 __global__ void __launch_bounds__(kThreads) k_merge_rows(const __grid_constant__ Params prm) {
-    pdl_wait();
-    if (threadIdx.x == 0 && blockIdx.x == 0) *prm.work_ctr = 0u;   // re-arm K1's counter
-    const int64_t rows = 2ll * prm.N * prm.K;
-    const int64_t p = blockIdx.x;
-    for (int64_t rl = threadIdx.x; rl < rows; rl += kThreads) {
-        const int64_t r = p * rows + rl;
-        float4 m = merge_parts(prm.part_ws + r * prm.nseg, 1, prm.nseg);
-        const int K = prm.K, N = prm.N;
-        const int model = (int)(rl / ((int64_t)N * K)), q = (int)(rl % ((int64_t)N * K));
-        const int n = q / K, j = q % K;
-        const int64_t pn = p * N + n;
+    extern __shared__ float4 stage[];
+    const int p = blockIdx.x, tid = threadIdx.x, N = prm.N, K = prm.K, NK = N * K;
+    const int rows = 2 * NK;
+    auto row_x = [&](int r) -> float {                        // inputs only: safe before the wait
+        const int model = r / NK, q = r - model * NK, n = q / K, j = q - n * K;
+        const int64_t pn = (int64_t)p * N + n;
         const int kn = drafted_len(prm, pn);
-        m.z = (kn >= 0 && kn <= K && j < kn) ? load_x(prm, model, pn, j, prm.tokens[pn * K + j]) : -INFINITY;
-        prm.partials_out[r] = m;
-    }
+        return (kn >= 0 && kn <= K && j < kn) ? load_x(prm, model, pn, j, prm.tokens[pn * K + j])
+                                              : -INFINITY;
+    };
+    const float x_pre = tid < rows ? row_x(tid) : -INFINITY;
+    pdl_wait();
+    if (tid == 0 && p == 0) *prm.work_ctr = 0u;               // re-arm K1's counter
+    float4 *out = prm.partials_out + (int64_t)p * rows;
+    tail_rowstats(prm, p, out, stage);
+    __syncthreads();
+    for (int r = tid; r < rows; r += kThreads) out[r].z = r == tid ? x_pre : row_x(r);
     pdl_trigger();
 }
 

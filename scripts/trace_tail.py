@@ -36,8 +36,7 @@ s = sorted(us(x) for x in starts)
 e = sorted(us(x) for x in ends)
 print(f"K1 CTAs {len(starts)}: start spread {s[-1]:.2f} us; done min {e[0]:.2f} median {e[len(e)//2]:.2f} "
       f"p90 {e[int(len(e)*0.9)]:.2f} max {e[-1]:.2f} us")
-names = {2060: "S2 t0: loads issue", 2061: "S2 t0: parts merged", 2062: "S2 t0: ell", 2063: "S2 t0: loop done",
-         2048: "tail CTA resident", 2049: "tail after pdl_wait", 2050: "after S2", 2051: "after S3",
+names = {2048: "tail CTA resident", 2049: "tail after pdl_wait", 2053: "chunk 0 S2+terms done", 2050: "last CTA of prompt 0", 2051: "after S3",
          2052: "after S4-S7"}
 for k, nm in names.items():
     print(f"{nm:22s} {us(t[k]):8.2f} us")
