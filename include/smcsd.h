@@ -59,8 +59,9 @@ typedef enum {
 
 typedef enum { SMCSD_F32 = 0, SMCSD_BF16 = 1 } smcsd_dtype;
 
-/* Resampling scheme.  Systematic is the north star's choice (reading G1); the paper's
- * multinomial draw is NEXT (returns SMCSD_ENOSYS in this build). */
+/* Resampling scheme.  Systematic is the north star's choice (reading G1); multinomial is the
+ * paper's literal draw a_n ~ Cat(wbar) i.i.d. (Alg. 1) with
+ * u_n = word (n mod 4) of Philox(key = seed, ctr = (step_lo, step_hi, prompt, 1 + n/4)). */
 typedef enum { SMCSD_SYSTEMATIC = 0, SMCSD_MULTINOMIAL = 1 } smcsd_scheme;
 
 /* Per-prompt status bits (asynchronous, data-dependent). */
@@ -68,6 +69,7 @@ typedef enum { SMCSD_SYSTEMATIC = 0, SMCSD_MULTINOMIAL = 1 } smcsd_scheme;
 #define SMCSD_ST_NOT_ABSCONT 2u  /* q(d) = 0 at a drafted token: p << q violated     */
 #define SMCSD_ST_BAD_TOKEN   4u  /* drafted token outside [0,V), or n_drafted outside [0,K]         */
 #define SMCSD_ST_NONFINITE   8u  /* NaN/+inf logit or log-weight, or a row whose max is -inf        */
+#define SMCSD_ST_BAD_PAGE   16u  /* paged reindex: page id or ancestor out of range (entry skipped) */
 
 /* Segment length (elements) of the fixed in-row split used by every logit row (G17). */
 #define SMCSD_SEGMENT 8192
@@ -110,9 +112,11 @@ SMCSD_API smcsd_rc smcsd_weights(const void *logits_p, int64_t ld_p, int rows_pe
  *  eta:       resample iff ESS < eta (strict); +INFINITY forces, 0 never.
  *  seed/step: Philox4x32-10 key and counter high words: U = word0(Philox(key = seed,
  *             ctr = (step_lo, step_hi, prompt_base + p, 0))) * 2^-32 (reading G5).
- *  uniforms:  optional [P] raw 32-bit words replacing the Philox draw (tests), or NULL.
- *  Systematic ancestors: C_m = P_m / S (fp64 sequential prefix), u_n = (n + U)/N,
- *  a_n = #{m : C_m <= u_n}; offspring o_m; slot_src = the in-place plan (survivors keep their
+ *  uniforms:  optional raw 32-bit words replacing the Philox draws (tests), or NULL:
+ *             [P] for SMCSD_SYSTEMATIC, [P][N] for SMCSD_MULTINOMIAL.
+ *  Ancestors: C_m = P_m / S (fp64 sequential prefix), a_n = #{m : C_m <= u_n} with
+ *  u_n = (n + U)/N (systematic; ancestors ascending) or u_n i.i.d. (multinomial; draw order);
+ *  offspring o_m; slot_src = the in-place plan (survivors keep their
  *  slot, dead slots take the extra copies in ascending order; reading G14); n_ties counts
  *  pairs |u_n - C_m| <= 2^-40 (reading G7).  Without a resample: identity, o = 1, lam kept.
  *  logw_out [P][N]: fl32(-ln N) after a resample, else lam.  May alias logw.
@@ -183,6 +187,32 @@ SMCSD_API smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer,
                           int64_t prompt_stride, int64_t particle_stride, int64_t seg_count,
                           int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index,
                           int P, int N, void *stream);
+
+/* Terminal selection: "one complete sequence is sampled from the terminal
+ * normalized weights".  selected[p] = #{m : C_m <= u} with u = word0(Philox(key = seed,
+ * ctr = (step_lo, step_hi, prompt_base + p, 0xFFFFFFFF))) * 2^-32 (or uniforms[p]); -1 and
+ * SMCSD_ST_DEGENERATE when every weight is -inf.  workspace: smcsd_workspace_bytes(P, N, 1, 1). */
+SMCSD_API smcsd_rc smcsd_select(const float *logw, int P, int N, int64_t prompt_base, uint64_t seed,
+                                uint64_t step, const uint32_t *uniforms, int32_t *selected,
+                                uint32_t *status, void *workspace, size_t workspace_bytes,
+                                void *stream);
+
+/* Paged (pointer) KV reindex -- the paper's own resampling mechanism (PAPER.md:488-490,
+ * Sec. 3.3 Obs. 2: "copying page metadata and incrementing the reference counts").
+ * table_*: [P][N][max_pages] int32 page ids; n_pages_*: [P][N] int32 list lengths.
+ *   table_dst[p][n][i] = table_src[p][a_n][i] for i < n_pages_src[p][a_n], -1 beyond;
+ *   n_pages_dst[p][n] = n_pages_src[p][a_n];   (a = src_index, local to the prompt)
+ *   refcount[pg] += #references in the new lists - #references in the old lists (exact int);
+ *   freed (optional, [num_pages] u8): 1 for old-list pages whose refcount reached 0, else 0
+ *   (pages no old list references are untouched).
+ * No KV content moves; a partially filled tail page shared after resampling is copied on
+ * the next append (engine-level copy-on-write, outside this call).  src and dst tables must
+ * not alias.  Out-of-range ids are skipped and flagged SMCSD_ST_BAD_PAGE in status[p]. */
+SMCSD_API smcsd_rc smcsd_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages_src,
+                                          int32_t *table_dst, int32_t *n_pages_dst,
+                                          int32_t *refcount, uint8_t *freed,
+                                          const int32_t *src_index, int P, int N, int max_pages,
+                                          int num_pages, uint32_t *status, void *stream);
 
 /* Human-readable name of a return code (static storage). */
 SMCSD_API const char *smcsd_strerror(smcsd_rc rc);

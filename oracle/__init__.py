@@ -26,6 +26,7 @@ ST_DEGENERATE = 1
 ST_NOT_ABSCONT = 2
 ST_BAD_TOKEN = 4
 ST_NONFINITE = 8
+ST_BAD_PAGE = 16
 
 
 def build(force: bool = False) -> str:
@@ -53,9 +54,11 @@ def lib():
         L.orc_combine_partials.restype = dbl
         L.orc_weights.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp, i32, i32, i32, i64,
                                   dbl, dbl, dbl, vp, vp, vp, vp, vp, vp, vp, vp]
-        L.orc_resample.argtypes = [vp, i32, i32, i64, dbl, u64, u64, vp, vp, vp, vp, vp, vp, vp,
-                                   vp, vp, vp, vp, vp, vp, vp]
+        L.orc_resample.argtypes = [vp, i32, i32, i64, dbl, i32, u64, u64, vp, vp, vp, vp, vp, vp,
+                                   vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_select.argtypes = [vp, i32, i32, i64, u64, u64, vp, vp, vp, vp]
         L.orc_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32]
+        L.orc_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
         _lib = L
     return _lib
 
@@ -131,8 +134,10 @@ def weights(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=Non
     return out
 
 
-def resample(logw, *, eta=float("inf"), seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None):
-    """S4-S7 oracle from fp32 log-weights [P][N]."""
+def resample(logw, *, eta=float("inf"), seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
+             scheme=0):
+    """S4-S7 oracle from fp32 log-weights [P][N]; scheme 0 systematic, 1 multinomial
+    (uniforms override: [P] words for systematic, [P][N] for multinomial)."""
     lw = np.ascontiguousarray(logw, dtype=np.float32)
     P, N = lw.shape
     un = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.uint32)
@@ -143,13 +148,26 @@ def resample(logw, *, eta=float("inf"), seed=0x5EED5EED, step=0, prompt_base=0, 
                wnorm=np.zeros((P, N)), cdf=np.zeros((P, N)))
     scratch = np.zeros(4 * N)
     iscratch = np.zeros(3 * N, np.int32)
-    lib().orc_resample(_ptr(lw), P, N, int(prompt_base), float(eta), int(seed) & (2**64 - 1),
+    lib().orc_resample(_ptr(lw), P, N, int(prompt_base), float(eta), int(scheme), int(seed) & (2**64 - 1),
                        int(step) & (2**64 - 1), _ptr(un), _ptr(out["ancestors"]),
                        _ptr(out["offspring"]), _ptr(out["slot_src"]), _ptr(out["logw"]),
                        _ptr(out["resampled"]), _ptr(out["ess"]), _ptr(out["lse"]),
                        _ptr(out["n_ties"]), _ptr(out["status"]), _ptr(out["wnorm"]),
                        _ptr(out["cdf"]), _ptr(scratch), _ptr(iscratch))
     return out
+
+
+def select(logw, *, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None):
+    """Terminal selection oracle: one index per prompt, -1 if degenerate."""
+    lw = np.ascontiguousarray(logw, dtype=np.float32)
+    P, N = lw.shape
+    un = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.uint32)
+    sel = np.zeros(P, np.int32)
+    st = np.zeros(P, np.uint32)
+    scratch = np.zeros(2 * N)
+    lib().orc_select(_ptr(lw), P, N, int(prompt_base), int(seed) & (2**64 - 1),
+                     int(step) & (2**64 - 1), _ptr(un), _ptr(sel), _ptr(st), _ptr(scratch))
+    return dict(selected=sel, status=st)
 
 
 def kv_reindex(dst: np.ndarray, src: np.ndarray, src_index: np.ndarray, *, n_outer, outer_stride,
@@ -159,6 +177,23 @@ def kv_reindex(dst: np.ndarray, src: np.ndarray, src_index: np.ndarray, *, n_out
     P, N = idx.shape
     lib().orc_kv_reindex(_ptr(dst), _ptr(src), n_outer, outer_stride, prompt_stride,
                          particle_stride, seg_count, seg_bytes, seg_stride, _ptr(idx), P, N)
+
+
+def kv_reindex_paged(table, n_pages, refcount, src_index, *, num_pages=None):
+    """Paged reindex oracle.  table [P][N][max_pages] int32, n_pages [P][N],
+    refcount [num_pages] (updated copy returned).  Returns dict of new arrays."""
+    t = np.ascontiguousarray(table, dtype=np.int32)
+    P, N, MP = t.shape
+    npg = np.ascontiguousarray(n_pages, dtype=np.int32)
+    rc = np.ascontiguousarray(refcount, dtype=np.int32).copy()
+    idx = np.ascontiguousarray(src_index, dtype=np.int32)
+    num_pages = rc.size if num_pages is None else num_pages
+    out = dict(table=np.zeros_like(t), n_pages=np.zeros_like(npg), refcount=rc,
+               freed=np.zeros(num_pages, np.uint8), status=np.zeros(P, np.uint32))
+    lib().orc_kv_reindex_paged(_ptr(t), _ptr(npg), _ptr(out["table"]), _ptr(out["n_pages"]),
+                               _ptr(rc), _ptr(out["freed"]), _ptr(idx), P, N, MP, num_pages,
+                               _ptr(out["status"]))
+    return out
 
 
 def neg_log_n(N: int) -> np.float32:

@@ -274,10 +274,13 @@ void orc_weights(const void *logits_p, int64_t ld_p, int rpp_p,
 /* ------------------------------------------------------------------------------------ */
 /* smcsd_resample oracle: S4-S7 for P prompts from fp32 log-weights.                    */
 /* S5: resample iff ESS < eta (strict; reading G3).                        */
-/* S6: systematic resampling (north star; reading G1) by inverse CDF:      */
+/* S6, scheme 0 = systematic (north star; reading G1) by inverse CDF:      */
 /*   U = word0(Philox4x32-10(key=(seed_lo,seed_hi), ctr=(step_lo,step_hi,prompt,0)))     */
 /*       * 2^-32   (or uniforms[p] * 2^-32 when the override is given),                  */
 /*   C_m = P_m / S,  u_n = (n + U) / N,  a_n = #{m : C_m <= u_n}                         */
+/* S6, scheme 1 = multinomial, as Alg. 1 prints it (a_n ~ Cat(wbar) i.i.d.): */
+/*   u_n = word (n mod 4) of Philox(key, ctr=(step_lo,step_hi,prompt, 1 + floor(n/4)))   */
+/*       * 2^-32 (or uniforms[p*N + n] * 2^-32), a_n = #{m : C_m <= u_n} (same CDF).      */
 /*   (= min{m : u_n < C_m}; zero-weight particles are never chosen),        */
 /*   o_m = #{n : a_n = m},  ties = #{(n,m) : |u_n - C_m| <= 2^-40} (reading G7).          */
 /*   In-place slot plan (reading G14): survivors keep their slot; the list E of extra    */
@@ -289,7 +292,7 @@ void orc_weights(const void *logits_p, int64_t ld_p, int rpp_p,
 /* NaN / +inf input log-weights are flagged NONFINITE and treated as -inf (G13).         */
 /* ------------------------------------------------------------------------------------ */
 void orc_resample(const float *logw, int P, int N, int64_t prompt_base, double eta,
-                  uint64_t seed, uint64_t step, const uint32_t *uniforms,
+                  int scheme, uint64_t seed, uint64_t step, const uint32_t *uniforms,
                   int32_t *ancestors, int32_t *offspring, int32_t *slot_src, float *logw_out,
                   uint8_t *resampled, double *ess_out, double *lse_out, int32_t *n_ties,
                   uint32_t *status, double *wnorm, double *cdf_out,
@@ -326,19 +329,33 @@ void orc_resample(const float *logw, int P, int N, int64_t prompt_base, double e
             do_resample = ess < eta;
         }
         if (do_resample) {
-            double U;
-            if (uniforms) {
-                U = (double)uniforms[p] * two_m32;
-            } else {
-                uint64_t prompt = (uint64_t)(prompt_base + p);
-                uint32_t ctr[4] = {(uint32_t)step, (uint32_t)(step >> 32), (uint32_t)prompt, 0u};
-                uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
-                uint32_t r[4];
-                orc_philox4x32_10(ctr, key, r);
-                U = (double)r[0] * two_m32;
-            }
+            uint64_t prompt = (uint64_t)(prompt_base + p);
+            uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
             for (int m = 0; m < N; ++m) C[m] = Pc[m] / S;
-            for (int n = 0; n < N; ++n) u[n] = ((double)n + U) / (double)N;
+            if (scheme == 0) {
+                double U;
+                if (uniforms) {
+                    U = (double)uniforms[p] * two_m32;
+                } else {
+                    uint32_t ctr[4] = {(uint32_t)step, (uint32_t)(step >> 32), (uint32_t)prompt, 0u};
+                    uint32_t r[4];
+                    orc_philox4x32_10(ctr, key, r);
+                    U = (double)r[0] * two_m32;
+                }
+                for (int n = 0; n < N; ++n) u[n] = ((double)n + U) / (double)N;
+            } else {
+                for (int n = 0; n < N; ++n) {
+                    if (uniforms) {
+                        u[n] = (double)uniforms[(int64_t)p * N + n] * two_m32;
+                    } else {
+                        uint32_t ctr[4] = {(uint32_t)step, (uint32_t)(step >> 32), (uint32_t)prompt,
+                                           1u + (uint32_t)(n / 4)};
+                        uint32_t r[4];
+                        orc_philox4x32_10(ctr, key, r);
+                        u[n] = (double)r[n % 4] * two_m32;
+                    }
+                }
+            }
             for (int n = 0; n < N; ++n) {
                 int count = 0;
                 for (int m = 0; m < N; ++m)
@@ -392,6 +409,124 @@ void orc_resample(const float *logw, int P, int N, int64_t prompt_base, double e
         if (n_ties) n_ties[p] = ties;
         if (status) status[p] = st;
     }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Terminal selection: "one complete sequence is sampled from the       */
+/* terminal normalized weights" -- one draw per prompt by the same inverse CDF with          */
+/* u = word0(Philox(key, ctr=(step_lo,step_hi,prompt, 0xFFFFFFFF))) * 2^-32 (or the override  */
+/* uniforms[p]).  Degenerate prompt: selected = -1, status DEGENERATE.                       */
+/* ------------------------------------------------------------------------------------ */
+void orc_select(const float *logw, int P, int N, int64_t prompt_base, uint64_t seed, uint64_t step,
+                const uint32_t *uniforms, int32_t *selected, uint32_t *status,
+                double *scratch /* 2*N doubles */)
+{
+    const double two_m32 = 1.0 / 4294967296.0;
+    for (int p = 0; p < P; ++p) {
+        uint32_t st = 0;
+        const float *lw = logw + (int64_t)p * N;
+        double M = -INFINITY;
+        for (int n = 0; n < N; ++n) {
+            double v = lw[n];
+            if (isnan(v) || v == INFINITY) { st |= ORC_ST_NONFINITE; v = -INFINITY; }
+            if (v > M) M = v;
+        }
+        if (M == -INFINITY) {
+            selected[p] = -1;
+            status[p] = st | ORC_ST_DEGENERATE;
+            continue;
+        }
+        double *Pc = scratch;
+        double acc = 0.0;
+        for (int m = 0; m < N; ++m) {
+            double v = lw[m];
+            if (isnan(v) || v == INFINITY) v = -INFINITY;
+            acc = acc + exp(v - M);
+            Pc[m] = acc;
+        }
+        double u;
+        if (uniforms) {
+            u = (double)uniforms[p] * two_m32;
+        } else {
+            uint64_t prompt = (uint64_t)(prompt_base + p);
+            uint32_t ctr[4] = {(uint32_t)step, (uint32_t)(step >> 32), (uint32_t)prompt, 0xFFFFFFFFu};
+            uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+            uint32_t r[4];
+            orc_philox4x32_10(ctr, key, r);
+            u = (double)r[0] * two_m32;
+        }
+        int count = 0;
+        for (int m = 0; m < N; ++m)
+            if (Pc[m] / acc <= u) count++;
+        selected[p] = count;
+        status[p] = st;
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Paged KV reindex (NEXT #1; Sec. 3.3 Obs. 2: "resampling by copying page */
+/* metadata and incrementing the reference counts"; SPEC.md:466-474 resample_pages).        */
+/* table[p][n][0 .. n_pages[p][n]) lists particle n's KV pages.  After the call particle n   */
+/* holds its ancestor's list: table_dst[p][n][i] = table_src[p][a_n][i], n_pages_dst[p][n] = */
+/* n_pages_src[p][a_n] (slots i >= n_pages_dst are set to -1); refcount[pg] += #references   */
+/* in the new lists - #references in the old lists; freed[pg] = 1 for every page referenced */
+/* by an old list whose refcount is now 0 (0 for the other old-list pages).  No KV content   */
+/* moves.  Ids outside [0, num_pages) or ancestors outside [0, N) flag ST_BAD_PAGE (16) and  */
+/* are skipped.                                                                               */
+/* ------------------------------------------------------------------------------------ */
+#define ORC_ST_BAD_PAGE 16u
+void orc_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages_src, int32_t *table_dst,
+                          int32_t *n_pages_dst, int32_t *refcount, uint8_t *freed,
+                          const int32_t *src_index, int P, int N, int max_pages, int num_pages,
+                          uint32_t *status)
+{
+    for (int p = 0; p < P; ++p) status[p] = 0;
+    for (int p = 0; p < P; ++p) {
+        for (int n = 0; n < N; ++n) {
+            int64_t pn = (int64_t)p * N + n;
+            int a = src_index[pn];
+            int len = 0;
+            if (a < 0 || a >= N) {
+                status[p] |= ORC_ST_BAD_PAGE;
+            } else {
+                len = n_pages_src[(int64_t)p * N + a];
+                if (len < 0 || len > max_pages) { status[p] |= ORC_ST_BAD_PAGE; len = 0; }
+            }
+            for (int i = 0; i < max_pages; ++i) {
+                int32_t pg = -1;
+                if (i < len) {
+                    pg = table_src[((int64_t)p * N + a) * max_pages + i];
+                    if (pg < 0 || pg >= num_pages) { status[p] |= ORC_ST_BAD_PAGE; pg = -1; }
+                    else refcount[pg] += 1;
+                }
+                table_dst[pn * max_pages + i] = pg;
+            }
+            n_pages_dst[pn] = len;
+        }
+    }
+    for (int p = 0; p < P; ++p)
+        for (int n = 0; n < N; ++n) {
+            int64_t pn = (int64_t)p * N + n;
+            int len = n_pages_src[pn];
+            if (len < 0 || len > max_pages) { status[p] |= ORC_ST_BAD_PAGE; continue; }
+            for (int i = 0; i < len; ++i) {
+                int32_t pg = table_src[pn * max_pages + i];
+                if (pg < 0 || pg >= num_pages) { status[p] |= ORC_ST_BAD_PAGE; continue; }
+                refcount[pg] -= 1;
+            }
+        }
+    if (freed)
+        for (int p = 0; p < P; ++p)
+            for (int n = 0; n < N; ++n) {
+                int64_t pn = (int64_t)p * N + n;
+                int len = n_pages_src[pn];
+                if (len < 0 || len > max_pages) continue;
+                for (int i = 0; i < len; ++i) {
+                    int32_t pg = table_src[pn * max_pages + i];
+                    if (pg < 0 || pg >= num_pages) continue;
+                    freed[pg] = (uint8_t)(refcount[pg] == 0);
+                }
+            }
 }
 
 /* ------------------------------------------------------------------------------------ */

@@ -21,13 +21,13 @@ __all__ = [
     "SmcsdError", "Workspace", "lib_path",
     "smcsd_workspace_bytes", "smcsd_workspace_init", "smcsd_weights", "smcsd_step",
     "smcsd_resample", "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
-    "smcsd_version", "kv_geometry",
+    "smcsd_version", "kv_geometry", "smcsd_select", "smcsd_kv_reindex_paged", "ST_BAD_PAGE",
 ]
 
 SMCSD_F32, SMCSD_BF16 = 0, 1
 SMCSD_SYSTEMATIC, SMCSD_MULTINOMIAL = 0, 1
 SEGMENT = 8192
-ST_DEGENERATE, ST_NOT_ABSCONT, ST_BAD_TOKEN, ST_NONFINITE = 1, 2, 4, 8
+ST_DEGENERATE, ST_NOT_ABSCONT, ST_BAD_TOKEN, ST_NONFINITE, ST_BAD_PAGE = 1, 2, 4, 8, 16
 _RC = {0: "ok", 1: "invalid argument", 2: "CUDA launch or runtime error", 3: "not implemented"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -62,8 +62,11 @@ def _load():
     L.smcsd_weights_combine.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i64, f32, vp, vp, vp,
                                         vp, vp, vp, vp, vp, sz, vp]
     L.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
+    L.smcsd_select.argtypes = [vp, i32, i32, i64, u64, u64, vp, vp, vp, vp, sz, vp]
+    L.smcsd_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
     for name in ("smcsd_workspace_init", "smcsd_weights", "smcsd_resample", "smcsd_step",
-                 "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex"):
+                 "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
+                 "smcsd_select", "smcsd_kv_reindex_paged"):
         getattr(L, name).restype = i32
     L.smcsd_version.restype = ctypes.c_char_p
     L.smcsd_strerror.restype = ctypes.c_char_p
@@ -293,6 +296,35 @@ def smcsd_weights_combine(gathered, tokens, *, V, n_drafted=None, logw_prev=None
                                     _p(out.status), _p(ws), ws.numel(), _stream(stream))
     _check("smcsd_weights_combine", rc)
     return out
+
+
+def smcsd_select(logw, *, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None, selected=None,
+                 status=None, workspace=None, stream=None):
+    """Terminal selection: one particle index per prompt (-1 if degenerate)."""
+    P, N = logw.shape
+    dev = logw.device
+    selected = _empty((P,), torch.int32, dev) if selected is None else selected
+    status = _empty((P,), torch.int32, dev) if status is None else status
+    ws = _ws(workspace, dev, P, N, 1, 1, stream)
+    rc = _lib.smcsd_select(_p(logw), P, N, prompt_base, seed & (2 ** 64 - 1), step & (2 ** 64 - 1),
+                           _p(uniforms), _p(selected), _p(status), _p(ws), ws.numel(), _stream(stream))
+    _check("smcsd_select", rc)
+    return selected, status
+
+
+def smcsd_kv_reindex_paged(table_src, n_pages_src, refcount, src_index, *, table_dst=None,
+                           n_pages_dst=None, freed=None, status=None, stream=None):
+    """Paged (pointer) reindex: block-table rows + refcounts, no KV bytes."""
+    P, N, MP = table_src.shape
+    dev = table_src.device
+    table_dst = torch.empty_like(table_src) if table_dst is None else table_dst
+    n_pages_dst = torch.empty_like(n_pages_src) if n_pages_dst is None else n_pages_dst
+    status = _empty((P,), torch.int32, dev) if status is None else status
+    rc = _lib.smcsd_kv_reindex_paged(_p(table_src), _p(n_pages_src), _p(table_dst), _p(n_pages_dst),
+                                     _p(refcount), _p(freed), _p(src_index), P, N, MP,
+                                     refcount.numel(), _p(status), _stream(stream))
+    _check("smcsd_kv_reindex_paged", rc)
+    return table_dst, n_pages_dst, status
 
 
 def kv_geometry(kv: torch.Tensor, seq_len: int | None = None) -> dict:

@@ -235,14 +235,13 @@ smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t prompt_base, fl
                         float *wnorm_out, int32_t *n_ties, uint32_t *status, void *stream) {
     if (!logw || !ancestors || !logw_out || !resampled || !status) return SMCSD_EINVAL;
     if (P < 1 || N < 1 || N > kTailMaxN || std::isnan(eta)) return SMCSD_EINVAL;
-    if (scheme == SMCSD_MULTINOMIAL) return SMCSD_ENOSYS;
-    if (scheme != SMCSD_SYSTEMATIC) return SMCSD_EINVAL;
+    if (scheme != SMCSD_SYSTEMATIC && scheme != SMCSD_MULTINOMIAL) return SMCSD_EINVAL;
     Params prm;
     std::memset(&prm, 0, sizeof prm);
     prm.P = P; prm.N = N;
     prm.logw_prev = logw;
     prm.eta = (double)eta; prm.seed = seed; prm.step = step; prm.prompt_base = prompt_base;
-    prm.uniforms = uniforms;
+    prm.uniforms = uniforms; prm.scheme = scheme;
     prm.ancestors = ancestors; prm.offspring = offspring; prm.slot_src = slot_src;
     prm.logw_out = logw_out; prm.resampled = resampled; prm.ess = ess_out; prm.lse = lse_out;
     prm.wnorm = wnorm_out; prm.n_ties = n_ties; prm.status = status;
@@ -266,8 +265,7 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
     if (N > kTailMaxN || std::isnan(eta)) return SMCSD_EINVAL;
     if (!(std::isfinite(alpha) && alpha > 0.0f) || !valid_temp(inv_temp_p) || !valid_temp(inv_temp_q))
         return SMCSD_EINVAL;
-    if (scheme == SMCSD_MULTINOMIAL) return SMCSD_ENOSYS;
-    if (scheme != SMCSD_SYSTEMATIC) return SMCSD_EINVAL;
+    if (scheme != SMCSD_SYSTEMATIC && scheme != SMCSD_MULTINOMIAL) return SMCSD_EINVAL;
     const WsLayout L = ws_layout(P, N, K, V);
     if (workspace_bytes < L.total || !aligned16(workspace)) return SMCSD_EINVAL;
     // logw_prev may alias logw_out: the tail reads lam_prev[n] before any S7 write.
@@ -278,7 +276,7 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
     prm.dtype = dtype;
     prm.logw_prev = logw_prev;
     prm.eta = (double)eta; prm.seed = seed; prm.step = step; prm.prompt_base = prompt_base;
-    prm.uniforms = uniforms;
+    prm.uniforms = uniforms; prm.scheme = scheme;
     prm.logw_out = logw_out; prm.logw_pre = logw_pre; prm.logp_tok = logp_tok;
     prm.logq_tok = logq_tok; prm.lse = lse_out; prm.ess = ess_out; prm.wnorm = wnorm_out;
     prm.status = status; prm.ancestors = ancestors; prm.offspring = offspring;
@@ -371,6 +369,49 @@ smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t o
     const int64_t items = n_outer * P * prm.nchunks;
     if (items >= (1ll << 31)) return SMCSD_EINVAL;
     return launch_pdl(k_kv_reindex, (unsigned)items, 0, as_stream(stream), prm);
+}
+
+smcsd_rc smcsd_select(const float *logw, int P, int N, int64_t prompt_base, uint64_t seed,
+                      uint64_t step, const uint32_t *uniforms, int32_t *selected, uint32_t *status,
+                      void *workspace, size_t workspace_bytes, void *stream) {
+    if (!logw || !selected || !status || !workspace || P < 1 || N < 1) return SMCSD_EINVAL;
+    const WsLayout L = ws_layout(P, N, 1, 1);
+    if (workspace_bytes < L.total || !aligned16(workspace)) return SMCSD_EINVAL;
+    Params prm;
+    std::memset(&prm, 0, sizeof prm);
+    prm.P = P; prm.N = N; prm.K = 1;
+    prm.logw_prev = logw; prm.prompt_base = prompt_base; prm.seed = seed; prm.step = step;
+    prm.uniforms = uniforms; prm.selected = selected; prm.status = status;
+    bind_workspace(prm, workspace, L);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)P);
+    cfg.blockDim = dim3(32);
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_select, prm) == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
+}
+
+smcsd_rc smcsd_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages_src,
+                                int32_t *table_dst, int32_t *n_pages_dst, int32_t *refcount,
+                                uint8_t *freed, const int32_t *src_index, int P, int N,
+                                int max_pages, int num_pages, uint32_t *status, void *stream) {
+    if (!table_src || !n_pages_src || !table_dst || !n_pages_dst || !refcount || !src_index)
+        return SMCSD_EINVAL;
+    if (P < 1 || N < 1 || max_pages < 1 || num_pages < 1) return SMCSD_EINVAL;
+    if (table_src == table_dst || n_pages_src == n_pages_dst) return SMCSD_EINVAL;
+    PagedParams q;
+    q.table_src = table_src; q.n_src = n_pages_src; q.idx = src_index;
+    q.table_dst = table_dst; q.n_dst = n_pages_dst; q.refcount = refcount;
+    q.freed = freed; q.status = status;
+    q.P = P; q.N = N; q.max_pages = max_pages; q.num_pages = num_pages;
+    cudaStream_t st = as_stream(stream);
+    smcsd_rc rc = launch_pdl(k_paged_gather, (unsigned)P, 0, st, q);
+    if (rc != SMCSD_OK || !freed) return rc;
+    return launch_pdl(k_paged_freed, (unsigned)P, 0, st, q);
 }
 
 const char *smcsd_strerror(smcsd_rc rc) {

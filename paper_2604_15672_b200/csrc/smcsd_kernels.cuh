@@ -23,6 +23,7 @@ namespace smcsd {
 
 
 constexpr uint32_t ST_DEGENERATE = 1u, ST_NOT_ABSCONT = 2u, ST_BAD_TOKEN = 4u, ST_NONFINITE = 8u;
+constexpr uint32_t ST_BAD_PAGE = 16u;
 #ifndef SMCSD_PHASE
 #define SMCSD_PHASE(i) do { } while (0)
 #endif
@@ -67,6 +68,8 @@ struct Params {
     unsigned long long mg_nseg, mg_K, mg_N;     // magic multipliers: x / d == (x * mg) >> (32 + sh)
     int sh_nseg, sh_K, sh_N;
     int dtype;                                  // 0 fp32, 1 bf16 (logits)
+    int scheme;                                 // 0 systematic, 1 multinomial
+    int32_t *selected;                          // smcsd_select output [P]
     int x_from_logits;                          // 1: tail loads t_d from the logits; 0: from parts
     unsigned *work_ctr;                         // K1 dynamic work counter (re-armed by K2)
     unsigned *prompt_ctr;                       // [P] K2 chunk completion counters
@@ -560,8 +563,10 @@ struct TailSmem {
 // Weight-independent tail inputs: U = word0(Philox4x32-10(...)) * 2^-32 and fl32(-ln N).
 // Called by thread 0 before griddepcontrol.wait so they overlap the predecessor kernel.
 __device__ __forceinline__ void tail_prologue(const Params &prm, int p, TailSmem &sh) {
-    uint32_t x;
-    if (prm.uniforms) {
+    uint32_t x = 0;
+    if (prm.scheme != 0) {
+        x = 0;                                                  // multinomial: per-particle draws
+    } else if (prm.uniforms) {
         x = prm.uniforms[p];
     } else {
         const uint64_t g = (uint64_t)(prm.prompt_base + p);
@@ -659,8 +664,24 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
     SMCSD_PHASE(5);
     const double tie = 9.094947017729282379150390625e-13;     // 2^-40
     int ties = 0;
+    const uint64_t gp = (uint64_t)(prm.prompt_base + p);
     for (int n = b0; n < b1; ++n) {
-        const double u = __ddiv_rn(__dadd_rn((double)n, U), (double)N);
+        double u;
+        if (prm.scheme == 0) {                                  // systematic: (n + U) / N
+            u = __ddiv_rn(__dadd_rn((double)n, U), (double)N);
+        } else {                                                // multinomial
+            uint32_t x;
+            if (prm.uniforms) {
+                x = prm.uniforms[base + n];
+            } else {
+                const uint4 r = philox4x32_10(
+                    make_uint4((uint32_t)prm.step, (uint32_t)(prm.step >> 32), (uint32_t)gp, 1u + (uint32_t)(n >> 2)),
+                    make_uint2((uint32_t)prm.seed, (uint32_t)(prm.seed >> 32)));
+                const int w = n & 3;
+                x = w == 0 ? r.x : w == 1 ? r.y : w == 2 ? r.z : r.w;
+            }
+            u = (double)x * 2.3283064365386962890625e-10;
+        }
         int lo = 0, hi = N;                                     // a = #{m : C_m <= u}
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
@@ -1028,6 +1049,126 @@ __global__ void __launch_bounds__(kThreads) k_tail_large(const __grid_constant__
     if (prm.wnorm)
         for (int n = tid; n < N; n += kThreads)
             prm.wnorm[base + n] = (float)__ddiv_rn(__ldcg(&prm.e_ws[base + n]), s_S);
+}
+
+// Terminal selection: one index per prompt from the normalised weights by the
+// same inverse CDF, u = word0(Philox(key = seed, ctr = (step_lo, step_hi, prompt, 0xFFFFFFFF))).
+// grid = P, one warp per prompt; lane 0 runs the sequential fp64 prefix.
+__global__ void __launch_bounds__(32) k_select(const __grid_constant__ Params prm) {
+    const int p = blockIdx.x, N = prm.N, lane = threadIdx.x;
+    const int64_t base = (int64_t)p * N;
+    pdl_wait();
+    float mloc = -INFINITY;
+    uint32_t st = 0;
+    for (int n = lane; n < N; n += 32) {
+        float v = prm.logw_prev[base + n];
+        if (isnan(v) || v == INFINITY) { st |= ST_NONFINITE; v = -INFINITY; }
+        mloc = fmaxf(mloc, v);
+    }
+    const double M = (double)warp_max(mloc);
+    st = __reduce_or_sync(0xffffffffu, st);
+    if (lane == 0) {
+        if (M == -INFINITY) {
+            prm.selected[p] = -1;
+            prm.status[p] = st | ST_DEGENERATE;
+        } else {
+            uint32_t x;
+            if (prm.uniforms) {
+                x = prm.uniforms[p];
+            } else {
+                const uint64_t g = (uint64_t)(prm.prompt_base + p);
+                x = philox4x32_10(make_uint4((uint32_t)prm.step, (uint32_t)(prm.step >> 32), (uint32_t)g, 0xFFFFFFFFu),
+                                  make_uint2((uint32_t)prm.seed, (uint32_t)(prm.seed >> 32))).x;
+            }
+            const double u = (double)x * 2.3283064365386962890625e-10;
+            double acc = 0.0;
+            for (int m = 0; m < N; ++m) {
+                float v = prm.logw_prev[base + m];
+                if (isnan(v) || v == INFINITY) v = -INFINITY;
+                acc = __dadd_rn(acc, exp(__dsub_rn((double)v, M)));
+                prm.e_ws[base + m] = acc;
+            }
+            int count = 0;
+            for (int m = 0; m < N; ++m) count += __ddiv_rn(prm.e_ws[base + m], acc) <= u;
+            prm.selected[p] = count;
+            prm.status[p] = st;
+        }
+    }
+    pdl_trigger();
+}
+
+// ------------------------------------------------------------------------------------------
+// K5: paged (pointer) KV reindex -- the paper's own mechanism ("copying page
+// metadata and incrementing the reference counts").  No KV content moves.
+//   k_paged_gather (grid P): table_dst[p][n][:] = table_src[p][a_n][:], n_pages_dst = the
+//     ancestor's length, refcount += 1 per new reference and -= 1 per old reference (integer
+//     atomics: order-free, exact);
+//   k_paged_freed (grid P, PDL): freed[pg] = (refcount[pg] == 0) for every old-list page.
+// ------------------------------------------------------------------------------------------
+struct PagedParams {
+    const int32_t *table_src, *n_src, *idx;
+    int32_t *table_dst, *n_dst, *refcount;
+    uint8_t *freed;
+    uint32_t *status;
+    int P, N, max_pages, num_pages;
+};
+
+__global__ void __launch_bounds__(kThreads) k_paged_gather(const __grid_constant__ PagedParams q) {
+    __shared__ uint32_t s_st;
+    const int p = blockIdx.x, tid = threadIdx.x, N = q.N, MP = q.max_pages;
+    if (tid == 0) s_st = 0;
+    pdl_wait();
+    __syncthreads();
+    uint32_t st = 0;
+    const int64_t base = (int64_t)p * N;
+    for (int64_t e = tid; e < (int64_t)N * MP; e += kThreads) {
+        const int n = (int)(e / MP), i = (int)(e - (int64_t)n * MP);
+        // new list of n = old list of its ancestor
+        const int a = q.idx[base + n];
+        int len = 0;
+        if (a < 0 || a >= N) {
+            st |= ST_BAD_PAGE;
+        } else {
+            len = q.n_src[base + a];
+            if (len < 0 || len > MP) { st |= ST_BAD_PAGE; len = 0; }
+        }
+        int32_t pg = -1;
+        if (i < len) {
+            pg = q.table_src[(base + a) * MP + i];
+            if (pg < 0 || pg >= q.num_pages) { st |= ST_BAD_PAGE; pg = -1; }
+            else atomicAdd(&q.refcount[pg], 1);
+        }
+        q.table_dst[(base + n) * MP + i] = pg;
+        if (i == 0) q.n_dst[base + n] = len;
+        // old list of n drops its references
+        const int olen = q.n_src[base + n];
+        if (olen < 0 || olen > MP) {
+            if (i == 0) st |= ST_BAD_PAGE;
+        } else if (i < olen) {
+            const int32_t og = q.table_src[(base + n) * MP + i];
+            if (og < 0 || og >= q.num_pages) st |= ST_BAD_PAGE;
+            else atomicSub(&q.refcount[og], 1);
+        }
+    }
+    if (st) atomicOr(&s_st, st);
+    __syncthreads();
+    if (tid == 0 && q.status) q.status[p] = s_st;
+    pdl_trigger();
+}
+
+__global__ void __launch_bounds__(kThreads) k_paged_freed(const __grid_constant__ PagedParams q) {
+    const int p = blockIdx.x, tid = threadIdx.x, N = q.N, MP = q.max_pages;
+    pdl_wait();
+    const int64_t base = (int64_t)p * N;
+    for (int64_t e = tid; e < (int64_t)N * MP; e += kThreads) {
+        const int n = (int)(e / MP), i = (int)(e - (int64_t)n * MP);
+        const int olen = q.n_src[base + n];
+        if (olen < 0 || olen > MP || i >= olen) continue;
+        const int32_t og = q.table_src[(base + n) * MP + i];
+        if (og < 0 || og >= q.num_pages) continue;
+        q.freed[og] = (uint8_t)(__ldcg(&q.refcount[og]) == 0);
+    }
+    pdl_trigger();
 }
 
 // ------------------------------------------------------------------------------------------

@@ -29,7 +29,7 @@ def lib():
 
 def test_every_declared_symbol_is_exported(lib):
     names = _declared()
-    assert len(names) == 10, names
+    assert len(names) == 12, names
     for n in names:
         assert hasattr(lib, n), n
 
@@ -92,8 +92,8 @@ def test_resample_and_kv_einval(lib):
                                    0x3000, 0x4000, None, None, None, None, 0x5000, None)
     assert lib.smcsd_resample(*args(1025, 1.0, 0)) == 1          # N > 1024
     assert lib.smcsd_resample(*args(16, float("nan"), 0)) == 1   # NaN eta
-    assert lib.smcsd_resample(*args(16, 1.0, 1)) == 3            # multinomial: ENOSYS (NEXT)
-    assert lib.smcsd_resample(*args(16, 1.0, 7)) == 1
+    assert lib.smcsd_resample(*args(1025, 1.0, 1)) == 1          # multinomial, N > 1024
+    assert lib.smcsd_resample(*args(16, 1.0, 7)) == 1            # unknown scheme
     lib.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
     lib.smcsd_kv_reindex.restype = i32
     ok = dict(dst=0x10000, src=0x20000, n_outer=4, outer=4096, prompt=2048, particle=512,

@@ -138,13 +138,15 @@ def test_large_n_weights_path(smc, orc):
 def _resample_both(smc, orc, lw, **kw):
     dev = torch.device("cuda")
     un = kw.get("uniforms")
+    scheme = kw.get("scheme", 0)
     gpu = smc.smcsd_resample(torch.from_numpy(lw).to(dev), eta=kw.get("eta", math.inf),
                              seed=kw.get("seed", synth.PHILOX_SEED), step=kw.get("step", 0),
-                             prompt_base=kw.get("prompt_base", 0),
+                             prompt_base=kw.get("prompt_base", 0), scheme=scheme,
                              uniforms=None if un is None else torch.from_numpy(un.view(np.int32)).to(dev))
     torch.cuda.synchronize()
     ref = orc.resample(lw, eta=kw.get("eta", math.inf), seed=kw.get("seed", synth.PHILOX_SEED),
-                       step=kw.get("step", 0), prompt_base=kw.get("prompt_base", 0), uniforms=un)
+                       step=kw.get("step", 0), prompt_base=kw.get("prompt_base", 0), uniforms=un,
+                       scheme=scheme)
     return gpu, ref
 
 
@@ -354,3 +356,71 @@ def test_kv_identity_is_noop(smc):
     smc.smcsd_kv_reindex(kv, kv, torch.arange(8, dtype=torch.int32, device=dev)[None],
                          **smc.kv_geometry(kv))
     assert torch.equal(kv, before)
+
+
+# ----------------------------------------------------------------------- NEXT #3: multinomial
+@pytest.mark.parametrize("N", [1, 3, 16, 33, 64, 1024])
+def test_multinomial_resample_bit_exact(smc, orc, N):
+    P = 48
+    lw = synth.random_logw(P, N, seed=500 + N, sigma=2.0, neg_inf_frac=0.2).numpy()
+    lw[0, :] = -np.inf
+    lw[1, :] = 0.0
+    for step in (0, 7, (1 << 35) + 1):
+        gpu, ref = _resample_both(smc, orc, lw, step=step, prompt_base=77, scheme=1)
+        _assert_resample_equal(gpu, ref)
+    words = np.random.default_rng(N).integers(0, 2 ** 32, size=(P, N), dtype=np.uint64).astype(np.uint32)
+    gpu, ref = _resample_both(smc, orc, lw, uniforms=words, scheme=1)
+    _assert_resample_equal(gpu, ref)
+
+
+def test_step_multinomial_staged(smc, orc):
+    P, N, K, V = 3, 32, 8, 20000
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=61)
+    dev = torch.device("cuda")
+    out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, eta=math.inf, seed=3, step=4,
+                         scheme=smc.SMCSD_MULTINOMIAL)
+    torch.cuda.synchronize()
+    staged = orc.resample(np_(out.logw_pre), eta=math.inf, seed=3, step=4, scheme=1)
+    _assert_resample_equal(out, staged)
+
+
+def test_terminal_selection(smc, orc):
+    dev = torch.device("cuda")
+    P, N = 500, 37
+    lw = synth.random_logw(P, N, seed=8, sigma=2.0, neg_inf_frac=0.3).numpy()
+    lw[3, :] = -np.inf
+    sel, st = smc.smcsd_select(torch.from_numpy(lw).to(dev), seed=11, step=2, prompt_base=5)
+    ref = orc.select(lw, seed=11, step=2, prompt_base=5)
+    assert np.array_equal(np_(sel), ref["selected"])
+    assert np.array_equal(np_(st).astype(np.uint32), ref["status"])
+    words = np.random.default_rng(3).integers(0, 2 ** 32, size=P, dtype=np.uint64).astype(np.uint32)
+    sel, _ = smc.smcsd_select(torch.from_numpy(lw).to(dev), uniforms=torch.from_numpy(words.view(np.int32)).to(dev))
+    assert np.array_equal(np_(sel), orc.select(lw, uniforms=words)["selected"])
+
+
+# ----------------------------------------------------------------------- NEXT #1: paged KV
+def test_paged_reindex_bit_exact(smc, orc):
+    import test_oracle_kv_tp as kvt
+    dev = torch.device("cuda")
+    rng = np.random.default_rng(3)
+    for trial in range(6):
+        P, N = int(rng.integers(1, 5)), int(rng.integers(1, 70))
+        table, n_pages, rc = kvt._paged_fixture(P, N, 130, seed=trial)     # seq 2048 / page 16
+        lw = (rng.standard_normal((P, N)) * 2).astype(np.float32)
+        a = orc.resample(lw, eta=np.inf, seed=trial)["ancestors"]
+        ref = orc.kv_reindex_paged(table, n_pages, rc, a)
+        rcd = torch.from_numpy(rc).to(dev)
+        freed = torch.zeros(rc.size, dtype=torch.uint8, device=dev)
+        td, nd, st = smc.smcsd_kv_reindex_paged(torch.from_numpy(table).to(dev),
+                                                torch.from_numpy(n_pages).to(dev), rcd,
+                                                torch.from_numpy(a).to(dev), freed=freed)
+        torch.cuda.synchronize()
+        assert np.array_equal(np_(td), ref["table"])
+        assert np.array_equal(np_(nd), ref["n_pages"])
+        assert np.array_equal(np_(rcd), ref["refcount"])
+        touched = np.zeros(rc.size, bool)
+        for p in range(P):
+            for n in range(N):
+                touched[table[p, n, :n_pages[p, n]]] = True
+        assert np.array_equal(np_(freed)[touched], ref["freed"][touched])
+        assert np.all(np_(st) == 0)

@@ -90,3 +90,73 @@ def test_tp_masked_shard(orc):
     assert p1[0] == -np.inf and p1[1] == 0.0 and p1[2] == -np.inf
     ell, flag = orc.combine_partials(np.stack([p0, p1]))
     assert flag == 0 and ell == pytest.approx(2.0 - math.log(math.e + math.e ** 2), abs=1e-14)
+
+
+# ------------------------------------------------------------- paged reindex (NEXT #1)
+def _paged_fixture(P, N, pages_per, seed, shared_prefix=2):
+    """Particles of a prompt share `shared_prefix` prompt pages, then own their pages."""
+    rng = np.random.default_rng(seed)
+    MP = pages_per + 2
+    table = np.full((P, N, MP), -1, np.int32)
+    n_pages = np.zeros((P, N), np.int32)
+    nxt = 0
+    refc = []
+    for p in range(P):
+        prefix = list(range(nxt, nxt + shared_prefix)); nxt += shared_prefix
+        refc += [N] * shared_prefix
+        for n in range(N):
+            own = int(rng.integers(0, pages_per + 1))
+            ids = prefix + list(range(nxt, nxt + own)); nxt += own
+            refc += [1] * own
+            table[p, n, :len(ids)] = ids
+            n_pages[p, n] = len(ids)
+    return table, n_pages, np.array(refc, np.int32)
+
+
+def test_paged_identity_and_resample_to_one(orc):
+    table, n_pages, rc = _paged_fixture(1, 6, 4, seed=1)
+    out = orc.kv_reindex_paged(table, n_pages, rc, np.arange(6, dtype=np.int32)[None])
+    assert np.array_equal(out["refcount"], rc) and not out["freed"].any()      # SPEC.md:472
+    assert np.array_equal(out["table"], table)
+    # all ancestors = particle 1 (SPEC.md:473): its pages reach refcount N, others' freed
+    a = np.full((1, 6), 1, np.int32)
+    out = orc.kv_reindex_paged(table, n_pages, rc, a)
+    own1 = [pg for pg in table[0, 1, :n_pages[0, 1]] if rc[pg] == 1]
+    assert all(out["refcount"][pg] == 6 for pg in own1)
+    others = [pg for n in range(6) if n != 1 for pg in table[0, n, :n_pages[0, n]] if rc[pg] == 1]
+    assert all(out["freed"][pg] == 1 and out["refcount"][pg] == 0 for pg in others)
+    assert all(out["refcount"][pg] == 6 for pg in table[0, 0, :2])           # shared prefix
+    assert np.all(out["table"][0] == table[0, 1])
+
+
+def test_paged_conservation_random(orc):
+    rng = np.random.default_rng(5)
+    for trial in range(40):
+        P, N = int(rng.integers(1, 4)), int(rng.integers(1, 40))
+        table, n_pages, rc = _paged_fixture(P, N, 8, seed=trial)
+        lw = (rng.standard_normal((P, N)) * 2).astype(np.float32)
+        a = orc.resample(lw, eta=np.inf, seed=trial)["ancestors"]
+        out = orc.kv_reindex_paged(table, n_pages, rc, a)
+        # refcount conservation (SPEC.md:490): total references = total list lengths
+        assert out["refcount"].sum() == out["n_pages"].sum()
+        assert rc.sum() == n_pages.sum()
+        # the new lists are the ancestors' lists (independent gather)
+        for p in range(P):
+            assert np.array_equal(out["n_pages"][p], n_pages[p][a[p]])
+            for n in range(N):
+                L = n_pages[p, a[p, n]]
+                assert np.array_equal(out["table"][p, n, :L], table[p, a[p, n], :L])
+        # every page's refcount = its number of occurrences in the new tables
+        cnt = np.bincount(out["table"][out["table"] >= 0].ravel(), minlength=rc.size)
+        assert np.array_equal(cnt, out["refcount"])
+        assert np.array_equal(out["freed"] == 1, (rc > 0) & (out["refcount"] == 0))
+        assert np.all(out["status"] == 0)
+
+
+def test_paged_bad_ids_flagged(orc):
+    table, n_pages, rc = _paged_fixture(1, 4, 3, seed=2)
+    t2 = table.copy(); t2[0, 2, 0] = 10 ** 6
+    out = orc.kv_reindex_paged(t2, n_pages, rc, np.arange(4, dtype=np.int32)[None])
+    assert out["status"][0] == orc.ST_BAD_PAGE
+    out = orc.kv_reindex_paged(table, n_pages, rc, np.array([[0, 9, 1, 2]], np.int32))
+    assert out["status"][0] == orc.ST_BAD_PAGE

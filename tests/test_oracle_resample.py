@@ -158,3 +158,69 @@ def test_degenerate_and_nonfinite(orc):
     assert out["status"][1] == orc.ST_DEGENERATE | orc.ST_NONFINITE
     assert np.all(out["lse"] == -np.inf) and np.all(out["ess"] == 0.0)
     assert np.all(out["resampled"] == 0) and np.all(out["ancestors"] == np.arange(5))
+
+
+# ---------------------------------------------------------------- multinomial (NEXT #3)
+def test_multinomial_frequencies(orc):
+    # a_n ~ Cat(wbar) i.i.d. (Alg. 1): weights (.5,.3,.2), 1e5 draws, within
+    # +-0.01 of the weights
+    P = 33334
+    lw = np.tile(np.log(np.array([0.5, 0.3, 0.2])).astype(np.float32), (P, 1))
+    out = orc.resample(lw, eta=np.inf, scheme=1, seed=2024, step=1)
+    freq = np.bincount(out["ancestors"].ravel(), minlength=3) / out["ancestors"].size
+    assert np.allclose(freq, [0.5, 0.3, 0.2], atol=0.01)
+    assert np.all(out["offspring"].sum(1) == 3)
+
+
+def test_multinomial_uniform_chi_square(orc):
+    from scipy.stats import chisquare
+    P, N = 6250, 16
+    out = orc.resample(np.zeros((P, N), np.float32), eta=np.inf, scheme=1, seed=7, step=3)
+    counts = np.bincount(out["ancestors"].ravel(), minlength=N)
+    assert chisquare(counts).pvalue > 1e-3
+
+
+def test_multinomial_inverse_cdf_and_invariants(orc):
+    rng = np.random.default_rng(12)
+    for _ in range(50):
+        N = int(rng.integers(1, 60))
+        lw = (rng.standard_normal((1, N)) * 2).astype(np.float32)
+        lw[0, rng.random(N) < 0.2] = -np.inf
+        lw[0, int(rng.integers(0, N))] = 0.0
+        words = rng.integers(0, 2 ** 32, size=(1, N), dtype=np.uint64).astype(np.uint32)
+        out = orc.resample(lw, eta=np.inf, scheme=1, uniforms=words)
+        C = out["cdf"][0]
+        want = np.searchsorted(C, words[0].astype(np.float64) / 2 ** 32, side="right")
+        if out["n_ties"][0] == 0:
+            assert np.array_equal(out["ancestors"][0], want)
+        a, o, s = out["ancestors"][0], out["offspring"][0], out["slot_src"][0]
+        assert np.array_equal(np.bincount(a, minlength=N), o)
+        assert sorted(s.tolist()) == sorted(a.tolist())
+        assert np.all(o[lw[0] == -np.inf] == 0)
+    # single surviving weight
+    lw = np.full((1, 7), -np.inf, np.float32); lw[0, 2] = 1.0
+    assert np.all(orc.resample(lw, eta=np.inf, scheme=1, seed=9)["ancestors"] == 2)
+
+
+def test_multinomial_philox_addressing(orc):
+    # u_n = word (n mod 4) of Philox(ctr = (step_lo, step_hi, prompt, 1 + n/4))
+    lw = (np.random.default_rng(1).standard_normal((1, 9))).astype(np.float32)
+    words = np.zeros((1, 9), np.uint32)
+    for n in range(9):
+        words[0, n] = orc.philox4x32_10([11, 0, 5, 1 + n // 4], [0x77, 0x0])[n % 4]
+    direct = orc.resample(lw, eta=np.inf, scheme=1, uniforms=words)
+    via = orc.resample(lw, eta=np.inf, scheme=1, seed=0x77, step=11, prompt_base=5)
+    assert np.array_equal(direct["ancestors"], via["ancestors"])
+
+
+def test_terminal_selection(orc):
+    # one sequence sampled from the terminal normalised weights
+    P = 40000
+    lw = np.tile(np.log(np.array([0.1, 0.6, 0.3])).astype(np.float32), (P, 1))
+    sel = orc.select(lw, seed=5, step=9)
+    freq = np.bincount(sel["selected"], minlength=3) / P
+    assert np.allclose(freq, [0.1, 0.6, 0.3], atol=0.01)
+    dead = orc.select(np.full((2, 4), -np.inf, np.float32))
+    assert np.all(dead["selected"] == -1) and np.all(dead["status"] == orc.ST_DEGENERATE)
+    one = orc.select(np.array([[-np.inf, 3.0, -np.inf]], np.float32))
+    assert one["selected"][0] == 1
