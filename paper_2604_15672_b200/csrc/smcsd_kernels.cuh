@@ -382,326 +382,6 @@ __global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_row
     pdl_trigger();
 }
 
-__device__ __forceinline__ int drafted_len(const Params &prm, int64_t pn) {
-    return prm.n_drafted ? prm.n_drafted[pn] : prm.K;
-}
-
-// t_d = inv_temp * z_d * log2(e) for global token d of row (model, pn, j), or -inf when d is not
-// among this row's columns [v_begin, v_begin + v_len).
-__device__ __forceinline__ float load_x(const Params &prm, int model, int64_t pn, int j, int64_t d) {
-    const int64_t dl = d - prm.v_begin;
-    if (dl < 0 || dl >= prm.v_len) return -INFINITY;
-    const int esz = prm.dtype == 1 ? 2 : 4;
-    const char *row = model == 0 ? prm.lp + ((pn * prm.rpp_p + j) * prm.ld_p) * esz
-                                 : prm.lq + ((pn * prm.rpp_q + j) * prm.ld_q) * esz;
-    const float z = prm.dtype == 1 ? bf16lo(__ldg((const unsigned short *)row + dl))
-                                   : __ldg((const float *)row + dl);
-    return z * (model == 0 ? prm.c_p : prm.c_q);
-}
-
-// Reduce one item held in registers: lane 0 of each warp writes red[warp] = {m_w, s_w}.
-template <int DT>
-__device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], int nv, float c,
-                                            float2 *red) {
-    using T = ItemTraits<DT>;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (nv < kSeg) {                                          // ragged last segment: mask >= V
-#pragma unroll
-        for (int i = 0; i < T::kLoads; ++i) {
-            const int e = (i * kThreads + tid) * T::kVec;
-            uint32_t *w = reinterpret_cast<uint32_t *>(&v[i]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (DT == 1) {
-                    if (e + 2 * k >= nv)     w[k] = (w[k] & 0xffff0000u) | 0x0000FF80u;
-                    if (e + 2 * k + 1 >= nv) w[k] = (w[k] & 0x0000ffffu) | 0xFF800000u;
-                } else {
-                    if (e + k >= nv) w[k] = T::kNegInf;
-                }
-            }
-        }
-    }
-    // max over the warp's elements (raw logits; c > 0 so max(z)*c = max(z*c))
-    float mt;
-    if (DT == 1) {
-        uint32_t acc = v[0].x;
-#pragma unroll
-        for (int i = 0; i < T::kLoads; ++i) {
-            const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) asm("max.bf16x2 %0, %0, %1;" : "+r"(acc) : "r"(w4[k]));
-        }
-        mt = fmaxf(bf16lo(acc), bf16hi(acc));
-    } else {
-        mt = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < T::kLoads; ++i)
-            mt = fmaxf(mt, fmaxf(fmaxf(__uint_as_float(v[i].x), __uint_as_float(v[i].y)),
-                                 fmaxf(__uint_as_float(v[i].z), __uint_as_float(v[i].w))));
-    }
-    const float mw = warp_max(mt) * c;                       // warp max of t = z*c
-    const float off = mw == -INFINITY ? 0.0f : mw;           // all -inf: sum(2^-inf) = 0, NaN kept
-    // sum of 2^(t - m): exactly one ex2 per element
-    float s_acc[T::kLoads];
-#pragma unroll
-    for (int i = 0; i < T::kLoads; ++i) {
-        const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-        float a = 0.0f;
-        if (DT == 1) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                a += ex2_approx(fmaf(bf16lo(w4[k]), c, -off));
-                a += ex2_approx(fmaf(bf16hi(w4[k]), c, -off));
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) a += ex2_approx(fmaf(__uint_as_float(w4[k]), c, -off));
-        }
-        s_acc[i] = a;
-    }
-    float s = s_acc[0];
-#pragma unroll
-    for (int i = 1; i < T::kLoads; ++i) s += s_acc[i];
-    s = warp_sum(s);
-    if (lane == 0) red[warp] = make_float2(mw, s);
-}
-
-// Unsigned division by a runtime constant d via a precomputed magic number (host computes
-// mg = ceil(2^(32+sh) / d) with sh = ceil(log2 d), < 2^33); exact for x, d < 2^31.
-__device__ __forceinline__ unsigned fastdiv(unsigned x, unsigned long long mg, int sh) {
-    return (unsigned)(((unsigned long long)x * mg) >> (32 + sh));
-}
-
-// Per-item data derived from the item index (every thread, no broadcast).
-struct ItemInfo {
-    const char *seg;        // first byte of the segment
-    int nv;                 // valid elements in the segment
-    float c;                // inv_temp * log2(e) of the row's model
-    int valid;              // row is read (j < k_n)
-};
-
-template <int DT>
-__device__ __forceinline__ ItemInfo item_info(const Params &prm, long long item) {
-    ItemInfo f;
-    const unsigned u = (unsigned)item;                      // total < 2^31 (validated)
-    unsigned row = fastdiv(u, prm.mg_nseg, prm.sh_nseg);
-    const int seg = (int)(u - row * (unsigned)prm.nseg);
-    const unsigned r1 = fastdiv(row, prm.mg_K, prm.sh_K);
-    const int j = (int)(row - r1 * (unsigned)prm.K);
-    const unsigned r2 = fastdiv(r1, prm.mg_N, prm.sh_N);
-    const int n = (int)(r1 - r2 * (unsigned)prm.N);
-    const int model = (int)(r2 & 1u);
-    const int64_t pn = (int64_t)(r2 >> 1) * prm.N + n;
-    const int kn = prm.n_drafted ? prm.n_drafted[pn] : prm.K;
-    f.valid = kn >= 0 && kn <= prm.K && j < kn;
-    constexpr int kEsz = ItemTraits<DT>::kEsz;
-    const int64_t v0 = (int64_t)seg * kSeg;
-    const char *row_ptr = model == 0 ? prm.lp + ((pn * prm.rpp_p + j) * prm.ld_p) * kEsz
-                                     : prm.lq + ((pn * prm.rpp_q + j) * prm.ld_q) * kEsz;
-    f.seg = row_ptr + v0 * kEsz;
-    f.nv = (int)min((int64_t)kSeg, prm.v_len - v0);
-    f.c = model == 0 ? prm.c_p : prm.c_q;
-    return f;
-}
-
-// Issue this thread's loads of one decoded item.
-template <int DT>
-__device__ __forceinline__ void load_seg(uint4 (&v)[ItemTraits<DT>::kLoads], const ItemInfo &f) {
-    using T = ItemTraits<DT>;
-    const int tid = threadIdx.x;
-    if (f.nv == kSeg) {
-#pragma unroll
-        for (int i = 0; i < T::kLoads; ++i) v[i] = ld_stream(f.seg + (size_t)(i * kThreads + tid) * 16);
-    } else {
-#pragma unroll
-        for (int i = 0; i < T::kLoads; ++i) {
-            const int e = (i * kThreads + tid) * T::kVec;
-            v[i] = e < f.nv ? ld_stream(f.seg + (size_t)(i * kThreads + tid) * 16)
-                            : make_uint4(T::kNegInf, T::kNegInf, T::kNegInf, T::kNegInf);
-        }
-    }
-}
-
-// K1 kernel: warp-specialised bulk-copy (TMA) pipeline, no CTA-wide barriers.
-//   warp 8 (producer, lane 0): takes items in global order from an atomic counter (first item
-//     per CTA static), decodes them, and streams each item's bytes into a kStages-deep
-//     shared-memory ring with cp.async.bulk (completion counted on full[s] in bytes);
-//   warps 0..7 (consumers): wait full[s], reduce the item from shared memory, write their
-//     warp partial; the last consumer warp to finish an item (shared-memory counter) merges
-//     the 8 partials in fixed tree order, stores {m, s, -inf, 0}, and every warp releases the
-//     slot on empty[s].
-// The drafted-token logit is not taken here (the tail loads it).  grid = min(items, SMs x
-// resident CTAs), block = kK1Threads, dynamic smem = kStages x stage + bookkeeping.
-constexpr int kK1Threads = kThreads + 32;
-#ifndef SMCSD_K1_STAGES
-#define SMCSD_K1_STAGES 2
-#endif
-#ifndef SMCSD_K1_MINB
-#define SMCSD_K1_MINB 6
-#endif
-constexpr int kStages = SMCSD_K1_STAGES;
-
-struct StageMeta {
-    long long item;         // global item index, or -1: no more work
-    int nv;                 // valid elements in the segment
-    float c;                // inv_temp * log2(e) of the row's model
-    int valid;              // row is read (j < k_n)
-};
-
-template <int DT>
-constexpr size_t rowstats_smem_bytes() {
-    return (size_t)kStages * kSeg * ItemTraits<DT>::kEsz            // data ring
-         + kStages * (2 * sizeof(uint64_t) + sizeof(StageMeta) + kWarps * sizeof(float2) + 16);
-}
-
-template <int DT>
-__global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_rowstats(const __grid_constant__ Params prm) {
-    using T = ItemTraits<DT>;
-    constexpr uint32_t kStageBytes = (uint32_t)kSeg * T::kEsz;
-    extern __shared__ __align__(128) char smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
-    uint64_t *empty = full + kStages;
-    StageMeta *meta = reinterpret_cast<StageMeta *>(empty + kStages);
-    float2 *red = reinterpret_cast<float2 *>(meta + kStages);       // [kStages][kWarps]
-    int *done = reinterpret_cast<int *>(red + kStages * kWarps);    // [kStages]
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long total = 2ll * prm.P * prm.N * prm.K * prm.nseg;
-
-    if (tid == 0) {
-        SMCSD_TRACE_AT(blockIdx.x & 1023);                      // K1 CTA start
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWarps);
-            done[s] = 0;
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == kWarps) {
-        // ------------------------------------------------------------------ producer
-        if (lane == 0) {
-            // The predecessor may have produced the logits (or re-armed work_ctr): wait for it
-            // before the first global access.  Setup above overlapped its tail.
-            pdl_wait();
-            long long item = blockIdx.x;
-            for (long long it = 0;; ++it) {
-                const int s = (int)(it % kStages);
-                mbar_wait(&empty[s], (uint32_t)(((it / kStages) & 1) ^ 1));   // slot released
-                StageMeta m;
-                m.item = item < total ? item : -1;
-                m.valid = 0;
-                m.nv = 0;
-                m.c = 0.0f;
-                const char *src = nullptr;
-                if (item < total) {
-                    const ItemInfo f = item_info<DT>(prm, item);
-                    m.valid = f.valid;
-                    m.nv = f.nv;
-                    m.c = f.c;
-                    src = f.seg;
-                }
-                meta[s] = m;
-                if (m.valid) {
-                    const uint32_t bytes = (uint32_t)(((m.nv + T::kVec - 1) / T::kVec) * 16);
-                    mbar_arrive_expect_tx(&full[s], bytes);
-                    bulk_g2s(smem + (size_t)s * kStageBytes, src, bytes, &full[s]);
-                } else {
-                    mbar_arrive(&full[s]);                    // metadata only (release)
-                }
-                if (item >= total) break;
-                item = (long long)gridDim.x + atomicAdd(prm.work_ctr, 1u);
-            }
-        }
-    } else {
-        // ------------------------------------------------------------------ consumers
-        uint4 v[T::kLoads];
-        for (long long it = 0;; ++it) {
-            const int s = (int)(it % kStages);
-            mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
-            const StageMeta m = meta[s];
-            if (m.item < 0) break;
-            float2 *r = red + s * kWarps;
-            if (m.valid) {
-                const char *sl = smem + (size_t)s * kStageBytes;
-#pragma unroll
-                for (int i = 0; i < T::kLoads; ++i)
-                    v[i] = *reinterpret_cast<const uint4 *>(sl + (size_t)(i * kThreads + tid) * 16);
-                reduce_item<DT>(v, m.nv, m.c, r);
-            }
-            __syncwarp();
-            int last = 0;
-            if (lane == 0) {
-                __threadfence_block();                        // red[warp] before the count
-                last = atomicAdd(&done[s], 1) == kWarps - 1;
-            }
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (last) {
-                __threadfence_block();
-                // fixed-order (tree) merge of the 8 warp partials on lanes 0..7
-                float4 out = make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
-                if (m.valid) {
-                    const float2 rw = lane < kWarps ? r[lane] : make_float2(-INFINITY, 0.0f);
-                    float M = rw.x;
-                    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 4));
-                    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
-                    M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
-                    float t = lane < kWarps ? rw.y * (rw.x == M ? 1.0f : ex2_approx(rw.x - M)) : 0.0f;
-                    t += __shfl_xor_sync(0xffffffffu, t, 4);
-                    t += __shfl_xor_sync(0xffffffffu, t, 2);
-                    t += __shfl_xor_sync(0xffffffffu, t, 1);
-                    out = make_float4(M, t, -INFINITY, 0.0f);
-                }
-                if (lane == 0) {
-                    prm.part_ws[m.item] = out;
-                    done[s] = 0;
-                }
-                __syncwarp();
-            }
-            if (lane == 0) mbar_arrive(&empty[s]);            // this warp is done with slot s
-        }
-    }
-    if (tid == 0) SMCSD_TRACE_AT(1024 + (blockIdx.x & 1023));    // K1 CTA done
-    pdl_trigger();
-}
-
-// Merge a row's parts in fixed index order: M = max m_i, S = sum s_i 2^(m_i - M), X = max x_i.
-// Up to 16 parts are loaded at once (one L2 round trip).
-__device__ __forceinline__ float4 merge_parts(const float4 *parts, int64_t stride, int count) {
-    constexpr int kC = 16;
-    float M = -INFINITY, S = 0.0f, X = -INFINITY;
-    if (count <= kC) {
-        float3 q[kC];
-#pragma unroll
-        for (int i = 0; i < kC; ++i) {
-            if (i < count) {
-                const float4 t = __ldcg(&parts[i * stride]);
-                q[i] = make_float3(t.x, t.y, t.z);
-            } else {
-                q[i] = make_float3(-INFINITY, 0.0f, -INFINITY);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < kC; ++i) M = fmaxf(M, q[i].x);
-#pragma unroll
-        for (int i = 0; i < kC; ++i) {
-            if (i < count) {
-                S += q[i].y * (q[i].x == M ? 1.0f : ex2_approx(q[i].x - M));
-                X = fmaxf(X, q[i].z);
-            }
-        }
-        return make_float4(M, S, X, 0.0f);
-    }
-    for (int i = 0; i < count; ++i) M = fmaxf(M, __ldcg(&parts[i * stride]).x);
-    for (int i = 0; i < count; ++i) {
-        const float4 q = __ldcg(&parts[i * stride]);
-        S += q.y * (q.x == M ? 1.0f : ex2_approx(q.x - M));
-        X = fmaxf(X, q.z);
-    }
-    return make_float4(M, S, X, 0.0f);
-}
-
-
 // S2, phase A: merged {M, S, X} of every row of prompt p into rowstat[0 .. 2NK).  Chunks of
 // 256 rows x 16 parts are read with coalesced 16-byte loads (16 per thread in flight), staged in
 // shared memory (row pitch 17 float4: conflict-free), then thread t merges row t of the chunk
