@@ -214,6 +214,18 @@ SMCSD_API smcsd_rc smcsd_kv_reindex_paged(const int32_t *table_src, const int32_
                                           const int32_t *src_index, int P, int N, int max_pages,
                                           int num_pages, uint32_t *status, void *stream);
 
+/* PowerSMC weights (App. F): K = 1, no bonus token, draft = target.  Row 0
+ * of each particle (rows_per_particle >= 1) gives p = softmax(inv_temp * z) and the weight
+ * increment log w = ln sum_v p_v^alpha; lam' = fl32(lam_prev + log w), then
+ * S4.  Resample with smcsd_resample.  log_inc (optional, [P][N] fp32) receives log w.
+ * alpha = 1 gives log w = 0 exactly.  workspace: smcsd_workspace_bytes(P, N, 1, V); N <= 1024. */
+SMCSD_API smcsd_rc smcsd_powersmc_weights(const void *logits, int64_t ld, int rows_per_particle,
+                                          int dtype, const float *logw_prev, int P, int N,
+                                          int64_t V, float alpha, float inv_temp,
+                                          float *logw_out, float *log_inc, double *lse_out,
+                                          double *ess_out, float *wnorm_out, uint32_t *status,
+                                          void *workspace, size_t workspace_bytes, void *stream);
+
 /* Human-readable name of a return code (static storage). */
 SMCSD_API const char *smcsd_strerror(smcsd_rc rc);
 

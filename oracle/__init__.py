@@ -57,6 +57,8 @@ def lib():
         L.orc_resample.argtypes = [vp, i32, i32, i64, dbl, i32, u64, u64, vp, vp, vp, vp, vp, vp,
                                    vp, vp, vp, vp, vp, vp, vp, vp]
         L.orc_select.argtypes = [vp, i32, i32, i64, u64, u64, vp, vp, vp, vp]
+        L.orc_powersmc_weights.argtypes = [vp, i64, i32, i32, vp, i32, i32, i64, dbl, dbl, vp, vp,
+                                           vp, vp, vp, vp, vp]
         L.orc_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32]
         L.orc_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
         _lib = L
@@ -154,6 +156,21 @@ def resample(logw, *, eta=float("inf"), seed=0x5EED5EED, step=0, prompt_base=0, 
                        _ptr(out["resampled"]), _ptr(out["ess"]), _ptr(out["lse"]),
                        _ptr(out["n_ties"]), _ptr(out["status"]), _ptr(out["wnorm"]),
                        _ptr(out["cdf"]), _ptr(scratch), _ptr(iscratch))
+    return out
+
+
+def powersmc_weights(logits, *, V=None, logw_prev=None, alpha=1.0, tau=1.0):
+    """PowerSMC oracle (App. F): log w = ln sum_x p(x)^alpha of row j = 0."""
+    lg = np.ascontiguousarray(logits)
+    P, N, rpp, ld = lg.shape
+    V = ld if V is None else V
+    lw = None if logw_prev is None else np.ascontiguousarray(logw_prev, dtype=np.float32)
+    out = dict(logw=np.zeros((P, N), np.float32), inc=np.zeros((P, N)), lse=np.zeros(P),
+               ess=np.zeros(P), wnorm=np.zeros((P, N)), status=np.zeros(P, np.uint32))
+    scratch = np.zeros(2 * N)
+    lib().orc_powersmc_weights(_ptr(lg), ld, rpp, _dtype_code(lg), _ptr(lw), P, N, V, float(alpha),
+                               float(tau), _ptr(out["logw"]), _ptr(out["inc"]), _ptr(out["lse"]),
+                               _ptr(out["ess"]), _ptr(out["wnorm"]), _ptr(out["status"]), _ptr(scratch))
     return out
 
 

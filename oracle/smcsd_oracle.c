@@ -412,6 +412,61 @@ void orc_resample(const float *logw, int P, int N, int64_t prompt_base, double e
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* PowerSMC weights (NEXT #4; App. F): K = 1, no bonus token, target and */
+/* draft the same model; a particle's importance weight is w = sum_x p(x | prefix)^alpha    */
+/* (PAPER.md:1426), here with p = softmax(tau * z) of the particle's row j = 0:              */
+/*   log p_v = y_v - m - ln sum_u exp(y_u - m),  log w = ln sum_v exp(alpha * log p_v),      */
+/*   lam' = fl32(lam_prev + log w),  then S4 (normalise, ESS) exactly as in orc_weights.      */
+/* inc (optional [P][N] fp64) receives log w.                                                */
+/* ------------------------------------------------------------------------------------ */
+void orc_powersmc_weights(const void *logits, int64_t ld, int rpp, int dtype, const float *logw_prev,
+                          int P, int N, int64_t V, double alpha, double tau, float *logw_out,
+                          double *inc, double *lse_out, double *ess_out, double *wnorm,
+                          uint32_t *status, double *scratch /* 2*N doubles */)
+{
+    size_t esz = dtype == 1 ? 2 : 4;
+    for (int p = 0; p < P; ++p) {
+        uint32_t st = 0;
+        for (int n = 0; n < N; ++n) {
+            int64_t pn = (int64_t)p * N + n;
+            const char *row = (const char *)logits + (pn * rpp) * ld * (int64_t)esz;
+            double m, s, x;
+            int bad = row_stats_range(row, dtype, V, tau, -1, &m, &s, &x);
+            double lw = NAN;
+            if (bad || m == -INFINITY) {
+                st |= ORC_ST_NONFINITE;
+                bad = 1;
+            } else {
+                double lse = m + log(s);
+                double w = 0.0;
+                for (int64_t v = 0; v < V; ++v) {
+                    double logp = tau * decode_logit(row, dtype, v) - lse;
+                    w = w + exp(alpha * logp);
+                }
+                lw = log(w);
+            }
+            if (inc) inc[pn] = lw;
+            float prev = logw_prev ? logw_prev[pn] : (float)(-log((double)N));
+            if (isnan(prev) || prev == INFINITY) { st |= ORC_ST_NONFINITE; bad = 1; }
+            logw_out[pn] = bad ? -INFINITY : (float)((double)prev + lw);
+        }
+        double S, lse, ess;
+        double *e = scratch, *Pc = scratch + N;
+        if (s4_normalise(logw_out + (int64_t)p * N, N, e, Pc, &S, &lse, &ess)) {
+            st |= ORC_ST_DEGENERATE;
+            if (lse_out) lse_out[p] = -INFINITY;
+            if (ess_out) ess_out[p] = 0.0;
+            if (wnorm) for (int n = 0; n < N; ++n) wnorm[(int64_t)p * N + n] = 0.0;
+        } else {
+            if (lse_out) lse_out[p] = lse;
+            if (ess_out) ess_out[p] = ess;
+            if (wnorm) for (int n = 0; n < N; ++n) wnorm[(int64_t)p * N + n] = e[n] / S;
+        }
+        if (status) status[p] = st;
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* Terminal selection: "one complete sequence is sampled from the       */
 /* terminal normalized weights" -- one draw per prompt by the same inverse CDF with          */
 /* u = word0(Philox(key, ctr=(step_lo,step_hi,prompt, 0xFFFFFFFF))) * 2^-32 (or the override  */

@@ -22,6 +22,7 @@ __all__ = [
     "smcsd_workspace_bytes", "smcsd_workspace_init", "smcsd_weights", "smcsd_step",
     "smcsd_resample", "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
     "smcsd_version", "kv_geometry", "smcsd_select", "smcsd_kv_reindex_paged", "ST_BAD_PAGE",
+    "smcsd_powersmc_weights",
 ]
 
 SMCSD_F32, SMCSD_BF16 = 0, 1
@@ -64,9 +65,11 @@ def _load():
     L.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
     L.smcsd_select.argtypes = [vp, i32, i32, i64, u64, u64, vp, vp, vp, vp, sz, vp]
     L.smcsd_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
+    L.smcsd_powersmc_weights.argtypes = [vp, i64, i32, i32, vp, i32, i32, i64, f32, f32, vp, vp,
+                                         vp, vp, vp, vp, vp, sz, vp]
     for name in ("smcsd_workspace_init", "smcsd_weights", "smcsd_resample", "smcsd_step",
                  "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
-                 "smcsd_select", "smcsd_kv_reindex_paged"):
+                 "smcsd_select", "smcsd_kv_reindex_paged", "smcsd_powersmc_weights"):
         getattr(L, name).restype = i32
     L.smcsd_version.restype = ctypes.c_char_p
     L.smcsd_strerror.restype = ctypes.c_char_p
@@ -310,6 +313,27 @@ def smcsd_select(logw, *, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
                            _p(uniforms), _p(selected), _p(status), _p(ws), ws.numel(), _stream(stream))
     _check("smcsd_select", rc)
     return selected, status
+
+
+def smcsd_powersmc_weights(logits, *, V=None, logw_prev=None, alpha=1.0, inv_temp=1.0,
+                           out: Outputs | None = None, workspace=None, stream=None) -> Outputs:
+    """PowerSMC S1-S4 (App. F): log w = ln sum_v p_v^alpha of each particle's row 0.
+    Outputs: logw, logp_tok (= per-particle log w, [P][N]), lse, ess, wnorm, status."""
+    ld, rpp = _logits_geom(logits, "logits")
+    P, N = logits.shape[0], logits.shape[1]
+    V = ld if V is None else V
+    dev = logits.device
+    out = out or Outputs()
+    if out.logp_tok is None:
+        out.logp_tok = _empty((P, N), torch.float32, dev)
+    out = _alloc(out, dev, P, N, 1, ("logw", "status", "lse", "ess", "wnorm"))
+    ws = _ws(workspace, dev, P, N, 1, V, stream)
+    rc = _lib.smcsd_powersmc_weights(_p(logits), ld, rpp, _dtype_code(logits), _p(logw_prev), P, N, V,
+                                     alpha, inv_temp, _p(out.logw), _p(out.logp_tok), _p(out.lse),
+                                     _p(out.ess), _p(out.wnorm), _p(out.status), _p(ws), ws.numel(),
+                                     _stream(stream))
+    _check("smcsd_powersmc_weights", rc)
+    return out
 
 
 def smcsd_kv_reindex_paged(table_src, n_pages_src, refcount, src_index, *, table_dst=None,

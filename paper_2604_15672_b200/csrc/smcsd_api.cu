@@ -101,7 +101,7 @@ smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaSt
 }
 
 // K1 persistent grid: SMs x resident CTAs (shared-memory ring), capped by the work items.
-template <int DT>
+template <int DT, bool POWER>
 smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     static int ctas[64] = {0};
     int dev = 0;
@@ -109,14 +109,14 @@ smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     const size_t smem = rowstats_smem_bytes<DT>();
     if (ctas[dev] == 0) {
         int occ = 0, sms = 0;
-        if (cudaFuncSetAttribute(k_rowstats<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT>, kK1Threads, smem) != cudaSuccess ||
+        if (cudaFuncSetAttribute(k_rowstats<DT, POWER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT, POWER>, kK1Threads, smem) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || occ < 1)
             return SMCSD_ECUDA;
         ctas[dev] = occ * sms;
     }
     const int64_t grid = items < ctas[dev] ? items : ctas[dev];
-    return launch_pdl_b(k_rowstats<DT>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
+    return launch_pdl_b(k_rowstats<DT, POWER>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
 }
 
 // K2 tail: one CTA per prompt; the per-row S2 statistics live in dynamic shared memory when
@@ -144,9 +144,13 @@ smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks);
 }
 
-smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st) {
-    return dtype == SMCSD_BF16 ? launch_rowstats_dt<1>(prm, items, st)
-                               : launch_rowstats_dt<0>(prm, items, st);
+smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st,
+                         bool power = false) {
+    if (power)
+        return dtype == SMCSD_BF16 ? launch_rowstats_dt<1, true>(prm, items, st)
+                                   : launch_rowstats_dt<0, true>(prm, items, st);
+    return dtype == SMCSD_BF16 ? launch_rowstats_dt<1, false>(prm, items, st)
+                               : launch_rowstats_dt<0, false>(prm, items, st);
 }
 
 // Magic multiplier for division by d (1 <= d < 2^31): x / d == (x * mg) >> (32 + sh) for
@@ -177,6 +181,8 @@ Params logits_params(const void *lp, int64_t ld_p, int rpp_p, const void *lq, in
     set_magic(K, prm.mg_K, prm.sh_K);
     set_magic(N, prm.mg_N, prm.sh_N);
     prm.x_from_logits = 1;
+    prm.n_models = 2;
+    prm.alpha_f = 1.0f;
     return prm;
 }
 
@@ -412,6 +418,33 @@ smcsd_rc smcsd_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages
     smcsd_rc rc = launch_pdl(k_paged_gather, (unsigned)P, 0, st, q);
     if (rc != SMCSD_OK || !freed) return rc;
     return launch_pdl(k_paged_freed, (unsigned)P, 0, st, q);
+}
+
+smcsd_rc smcsd_powersmc_weights(const void *logits, int64_t ld, int rows_per_particle, int dtype,
+                                const float *logw_prev, int P, int N, int64_t V, float alpha,
+                                float inv_temp, float *logw_out, float *log_inc, double *lse_out,
+                                double *ess_out, float *wnorm_out, uint32_t *status,
+                                void *workspace, size_t workspace_bytes, void *stream) {
+    smcsd_rc rc = check_logits(logits, ld, rows_per_particle, logits, ld, rows_per_particle, dtype,
+                               reinterpret_cast<const int32_t *>(logits), P, N, 1, V);
+    if (rc != SMCSD_OK) return rc;
+    if (!logw_out || !status || !workspace || N > kTailMaxN) return SMCSD_EINVAL;
+    if (!(std::isfinite(alpha) && alpha > 0.0f) || !valid_temp(inv_temp)) return SMCSD_EINVAL;
+    const WsLayout L = ws_layout(P, N, 1, V);
+    if (workspace_bytes < L.total || !aligned16(workspace)) return SMCSD_EINVAL;
+    Params prm = logits_params(logits, ld, rows_per_particle, logits, ld, rows_per_particle,
+                               nullptr, nullptr, P, N, 1, V, 0, V, inv_temp, inv_temp);
+    prm.n_models = 1;
+    prm.alpha_f = alpha;
+    prm.dtype = dtype;
+    prm.logw_prev = logw_prev;
+    prm.logw_out = logw_out; prm.logp_tok = log_inc;
+    prm.lse = lse_out; prm.ess = ess_out; prm.wnorm = wnorm_out; prm.status = status;
+    bind_workspace(prm, workspace, L);
+    cudaStream_t st = as_stream(stream);
+    rc = launch_rowstats(prm, dtype, (int64_t)P * N * prm.nseg, st, true);
+    if (rc != SMCSD_OK) return rc;
+    return launch_pdl(k_power_tail, (unsigned)P, 0, st, prm);
 }
 
 const char *smcsd_strerror(smcsd_rc rc) {

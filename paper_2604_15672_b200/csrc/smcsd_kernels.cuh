@@ -69,6 +69,8 @@ struct Params {
     int sh_nseg, sh_K, sh_N;
     int dtype;                                  // 0 fp32, 1 bf16 (logits)
     int scheme;                                 // 0 systematic, 1 multinomial
+    int n_models;                               // 2: target + draft rows; 1: PowerSMC (target only)
+    float alpha_f;                              // PowerSMC exponent (K1 second sum)
     int32_t *selected;                          // smcsd_select output [P]
     int x_from_logits;                          // 1: tail loads t_d from the logits; 0: from parts
     unsigned *work_ctr;                         // K1 dynamic work counter (re-armed by K2)
@@ -116,10 +118,11 @@ __device__ __forceinline__ float load_x(const Params &prm, int model, int64_t pn
     return z * (model == 0 ? prm.c_p : prm.c_q);
 }
 
-// Reduce one item held in registers: lane 0 of each warp writes red[warp] = {m_w, s_w}.
-template <int DT>
+// Reduce one item held in registers: lane 0 of each warp writes red[warp] = {m_w, s_w, s2_w}
+// with s2 = sum 2^(alpha (t - m)) for PowerSMC (POWER), 0 otherwise.
+template <int DT, bool POWER = false>
 __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], int nv, float c,
-                                            float2 *red) {
+                                            float4 *red, float alpha = 1.0f) {
     using T = ItemTraits<DT>;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (nv < kSeg) {                                          // ragged last segment: mask >= V
@@ -158,29 +161,43 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
     }
     const float mw = warp_max(mt) * c;                       // warp max of t = z*c
     const float off = mw == -INFINITY ? 0.0f : mw;           // all -inf: sum(2^-inf) = 0, NaN kept
-    // sum of 2^(t - m): exactly one ex2 per element
-    float s_acc[T::kLoads];
+    // sum of 2^(t - m): exactly one ex2 per element (two for PowerSMC)
+    float s_acc[T::kLoads], s2_acc[T::kLoads];
 #pragma unroll
     for (int i = 0; i < T::kLoads; ++i) {
         const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-        float a = 0.0f;
+        float a = 0.0f, a2 = 0.0f;
         if (DT == 1) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                a += ex2_approx(fmaf(bf16lo(w4[k]), c, -off));
-                a += ex2_approx(fmaf(bf16hi(w4[k]), c, -off));
+                const float t0 = fmaf(bf16lo(w4[k]), c, -off), t1 = fmaf(bf16hi(w4[k]), c, -off);
+                a += ex2_approx(t0);
+                a += ex2_approx(t1);
+                if (POWER) {
+                    a2 += ex2_approx(t0 * alpha);
+                    a2 += ex2_approx(t1 * alpha);
+                }
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) a += ex2_approx(fmaf(__uint_as_float(w4[k]), c, -off));
+            for (int k = 0; k < 4; ++k) {
+                const float t0 = fmaf(__uint_as_float(w4[k]), c, -off);
+                a += ex2_approx(t0);
+                if (POWER) a2 += ex2_approx(t0 * alpha);
+            }
         }
         s_acc[i] = a;
+        s2_acc[i] = a2;
     }
-    float s = s_acc[0];
+    float s = s_acc[0], s2 = s2_acc[0];
 #pragma unroll
-    for (int i = 1; i < T::kLoads; ++i) s += s_acc[i];
+    for (int i = 1; i < T::kLoads; ++i) {
+        s += s_acc[i];
+        s2 += s2_acc[i];
+    }
     s = warp_sum(s);
-    if (lane == 0) red[warp] = make_float2(mw, s);
+    if (POWER) s2 = warp_sum(s2);
+    if (lane == 0) red[warp] = make_float4(mw, s, s2, 0.0f);
 }
 
 // Unsigned division by a runtime constant d via a precomputed magic number (host computes
@@ -207,8 +224,8 @@ __device__ __forceinline__ ItemInfo item_info(const Params &prm, long long item)
     const int j = (int)(row - r1 * (unsigned)prm.K);
     const unsigned r2 = fastdiv(r1, prm.mg_N, prm.sh_N);
     const int n = (int)(r1 - r2 * (unsigned)prm.N);
-    const int model = (int)(r2 & 1u);
-    const int64_t pn = (int64_t)(r2 >> 1) * prm.N + n;
+    const int model = prm.n_models == 2 ? (int)(r2 & 1u) : 0;
+    const int64_t pn = (int64_t)(prm.n_models == 2 ? (r2 >> 1) : r2) * prm.N + n;
     const int kn = prm.n_drafted ? prm.n_drafted[pn] : prm.K;
     f.valid = kn >= 0 && kn <= prm.K && j < kn;
     constexpr int kEsz = ItemTraits<DT>::kEsz;
@@ -268,10 +285,10 @@ struct StageMeta {
 template <int DT>
 constexpr size_t rowstats_smem_bytes() {
     return (size_t)kStages * kSeg * ItemTraits<DT>::kEsz            // data ring
-         + kStages * (2 * sizeof(uint64_t) + sizeof(StageMeta) + kWarps * sizeof(float2) + 16);
+         + kStages * (2 * sizeof(uint64_t) + sizeof(StageMeta) + kWarps * sizeof(float4) + 16);
 }
 
-template <int DT>
+template <int DT, bool POWER>
 __global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_rowstats(const __grid_constant__ Params prm) {
     using T = ItemTraits<DT>;
     constexpr uint32_t kStageBytes = (uint32_t)kSeg * T::kEsz;
@@ -279,10 +296,10 @@ __global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_row
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
     uint64_t *empty = full + kStages;
     StageMeta *meta = reinterpret_cast<StageMeta *>(empty + kStages);
-    float2 *red = reinterpret_cast<float2 *>(meta + kStages);       // [kStages][kWarps]
+    float4 *red = reinterpret_cast<float4 *>(meta + kStages);       // [kStages][kWarps]
     int *done = reinterpret_cast<int *>(red + kStages * kWarps);    // [kStages]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long total = 2ll * prm.P * prm.N * prm.K * prm.nseg;
+    const long long total = (long long)prm.n_models * prm.P * prm.N * prm.K * prm.nseg;
 
     if (tid == 0) {
         SMCSD_TRACE_AT(blockIdx.x & 1023);                      // K1 CTA start
@@ -338,13 +355,13 @@ __global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_row
             mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
             const StageMeta m = meta[s];
             if (m.item < 0) break;
-            float2 *r = red + s * kWarps;
+            float4 *r = red + s * kWarps;
             if (m.valid) {
                 const char *sl = smem + (size_t)s * kStageBytes;
 #pragma unroll
                 for (int i = 0; i < T::kLoads; ++i)
                     v[i] = *reinterpret_cast<const uint4 *>(sl + (size_t)(i * kThreads + tid) * 16);
-                reduce_item<DT>(v, m.nv, m.c, r);
+                reduce_item<DT, POWER>(v, m.nv, m.c, r, prm.alpha_f);
             }
             __syncwarp();
             int last = 0;
@@ -358,16 +375,24 @@ __global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_row
                 // fixed-order (tree) merge of the 8 warp partials on lanes 0..7
                 float4 out = make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
                 if (m.valid) {
-                    const float2 rw = lane < kWarps ? r[lane] : make_float2(-INFINITY, 0.0f);
+                    const float4 rw = lane < kWarps ? r[lane] : make_float4(-INFINITY, 0.0f, 0.0f, 0.0f);
                     float M = rw.x;
                     M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 4));
                     M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 2));
                     M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
-                    float t = lane < kWarps ? rw.y * (rw.x == M ? 1.0f : ex2_approx(rw.x - M)) : 0.0f;
+                    const float d = rw.x == M ? 0.0f : rw.x - M;
+                    float t = lane < kWarps ? rw.y * (rw.x == M ? 1.0f : ex2_approx(d)) : 0.0f;
                     t += __shfl_xor_sync(0xffffffffu, t, 4);
                     t += __shfl_xor_sync(0xffffffffu, t, 2);
                     t += __shfl_xor_sync(0xffffffffu, t, 1);
-                    out = make_float4(M, t, -INFINITY, 0.0f);
+                    float t2 = 0.0f;
+                    if (POWER) {
+                        t2 = lane < kWarps ? rw.z * (rw.x == M ? 1.0f : ex2_approx(d * prm.alpha_f)) : 0.0f;
+                        t2 += __shfl_xor_sync(0xffffffffu, t2, 4);
+                        t2 += __shfl_xor_sync(0xffffffffu, t2, 2);
+                        t2 += __shfl_xor_sync(0xffffffffu, t2, 1);
+                    }
+                    out = make_float4(M, t, -INFINITY, t2);
                 }
                 if (lane == 0) {
                     prm.part_ws[m.item] = out;
@@ -1015,6 +1040,57 @@ __global__ void __launch_bounds__(kThreads) k_tail_large(const __grid_constant__
     if (prm.wnorm)
         for (int n = tid; n < N; n += kThreads)
             prm.wnorm[base + n] = (float)__ddiv_rn(__ldcg(&prm.e_ws[base + n]), s_S);
+}
+
+// PowerSMC tail (NEXT #4; App. F), grid = P: per particle, merge the row's
+// segment partials {m, s, -, s2} in index order, log w = ln 2 (log2 S2 - alpha log2 S1) =
+// ln sum_v p_v^alpha, lam' = fl32(lam_prev + log w), then S4 (weights mode).
+__global__ void __launch_bounds__(kThreads) k_power_tail(const __grid_constant__ Params prm) {
+    __shared__ TailSmem sh;
+    const int p = blockIdx.x, N = prm.N, tid = threadIdx.x;
+    const float neglogN = (float)(-log((double)N));
+    if (tid == 0) sh.st = 0;
+    pdl_wait();
+    if (tid == 0 && p == 0) *prm.work_ctr = 0u;               // re-arm K1's counter
+    __syncthreads();
+    uint32_t st = 0;
+    const double a = (double)prm.alpha_f;
+    for (int n = tid; n < N; n += kThreads) {
+        const int64_t pn = (int64_t)p * N + n;
+        const float4 *parts = prm.part_ws + pn * prm.nseg;     // rows [P][N] (K = 1, one model)
+        float M = -INFINITY;
+        for (int i = 0; i < prm.nseg; ++i) M = fmaxf(M, __ldcg(&parts[i]).x);
+        float S1 = 0.0f, S2 = 0.0f;
+        for (int i = 0; i < prm.nseg; ++i) {
+            const float4 q = __ldcg(&parts[i]);
+            const float d = q.x == M ? 0.0f : q.x - M;
+            S1 += q.y * (q.x == M ? 1.0f : ex2_approx(d));
+            S2 += q.w * (q.x == M ? 1.0f : ex2_approx(d * prm.alpha_f));
+        }
+        const float prev = prm.logw_prev ? prm.logw_prev[pn] : neglogN;
+        bool bad = false;
+        double inc = __longlong_as_double(0x7ff8000000000000ll);
+        if (!isfinite(M) || !isfinite(S1) || !isfinite(S2)) {
+            st |= ST_NONFINITE;
+            bad = true;
+        } else {
+            inc = __dmul_rn(__dsub_rn(log2((double)S2), __dmul_rn(a, log2((double)S1))), kLn2);
+        }
+        if (isnan(prev) || prev == INFINITY) {
+            st |= ST_NONFINITE;
+            bad = true;
+        }
+        const float lam = bad ? -INFINITY : (float)__dadd_rn((double)prev, inc);
+        sh.lam[n] = lam;
+        prm.logw_out[pn] = lam;
+        if (prm.logp_tok) prm.logp_tok[pn] = (float)inc;        // per-particle log w
+    }
+    if (st) atomicOr(&sh.st, st);
+    __syncthreads();
+    normalise_resample(prm, p, false, sh);
+    __syncthreads();
+    if (tid == 0) prm.status[p] = sh.st;
+    pdl_trigger();
 }
 
 // Terminal selection: one index per prompt from the normalised weights by the

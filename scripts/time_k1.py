@@ -8,7 +8,7 @@ import paper_2604_15672_b200 as smc
 import synth
 
 dev = torch.device("cuda")
-which = os.environ.get("WHICH", "cfg4,cfg2,cfg5").split(",")
+which = os.environ.get("WHICH", "cfg4,cfg2,cfg5,power").split(",")
 
 def t(fn, reps, warm=3):
     for i in range(warm): fn(i)
@@ -38,5 +38,11 @@ if "cfg5" in which:
     part = torch.empty((1, 2, 64, 8, 4), device=dev)
     ms = t(lambda i: smc.smcsd_weights_partial(lp, lq, tok, v_begin=0, v_len=128256, partials=part, workspace=ws), 30)
     res["cfg5-partial-G1"] = (ms, 262668288 / ms / 1e6)
+if "power" in which:
+    lg, _, _ = synth.lm_logits(64, 32, 1, 128256, device=dev, seed=6, bonus=False)
+    ws = smc.Workspace(dev); out = smc.Outputs()
+    ms = t(lambda i: smc.smcsd_powersmc_weights(lg, V=128256, alpha=4.0, out=out, workspace=ws), 30)
+    res["power-P64N32"] = (ms, 64 * 32 * 128256 * 2 / ms / 1e6)
+    del lg; torch.cuda.empty_cache()
 for k, (ms, gbs) in res.items():
     print(f"{os.path.basename(smc.lib_path):24s} {k:16s} {ms * 1e3:9.2f} us  {gbs:8.1f} GB/s  ({gbs / 6543.7:.3f} of measured)")

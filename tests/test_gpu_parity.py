@@ -424,3 +424,51 @@ def test_paged_reindex_bit_exact(smc, orc):
                 touched[table[p, n, :n_pages[p, n]]] = True
         assert np.array_equal(np_(freed)[touched], ref["freed"][touched])
         assert np.all(np_(st) == 0)
+
+
+# ------------------------------------------------------------- PowerSMC weights (NEXT #4)
+def _power_both(smc, orc, lg, V, alpha, tau=1.0, prev=None):
+    dev = torch.device("cuda")
+    gpu = smc.smcsd_powersmc_weights(lg.to(dev), V=V, alpha=alpha, inv_temp=tau,
+                                     logw_prev=None if prev is None else prev.to(dev))
+    torch.cuda.synchronize()
+    ref = orc.powersmc_weights(to_host(lg), V=V, alpha=alpha, tau=tau, logw_prev=np_(prev))
+    return gpu, ref
+
+
+@pytest.mark.parametrize("alpha", [0.5, 2.0, 4.0])
+@pytest.mark.parametrize("P,N,V,dtype", [(1, 16, 128256, torch.bfloat16), (2, 33, 20001, torch.float32),
+                                         (3, 5, 8193, torch.bfloat16), (1, 1, 3, torch.float32)])
+def test_powersmc_weights_parity(smc, orc, P, N, V, dtype, alpha):
+    lg, _, _ = synth.lm_logits(P, N, 1, V, dtype=dtype, seed=4000 + V + N, bonus=False)
+    prev = synth.random_logw(P, N, seed=8, sigma=0.5)
+    gpu, ref = _power_both(smc, orc, lg, V, alpha, tau=1.0 / 0.8, prev=prev)
+    assert np.array_equal(np_(gpu.status).astype(np.uint32), ref["status"])
+    assert max_abs(np_(gpu.logp_tok), ref["inc"]) <= TOL_LOGW
+    assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW
+    assert np.allclose(np_(gpu.lse), ref["lse"], rtol=0, atol=TOL_LOGW)
+    assert np.allclose(np_(gpu.ess), ref["ess"], rtol=1e-3)
+    assert np.allclose(np_(gpu.wnorm), ref["wnorm"], rtol=1e-3, atol=1e-6)
+
+
+def test_powersmc_alpha_one_is_exact_zero(smc):
+    # alpha = 1: S2 and S1 are the same fp32 sum, so log w = ln2 (log2 S - log2 S) = 0 exactly
+    lg, _, _ = synth.lm_logits(2, 16, 1, 128256, dtype=torch.bfloat16, seed=3, bonus=False)
+    dev = torch.device("cuda")
+    prev = torch.full((2, 16), -math.log(16), device=dev)
+    out = smc.smcsd_powersmc_weights(lg.to(dev), V=128256, alpha=1.0, logw_prev=prev)
+    assert torch.all(out.logp_tok == 0.0)
+    assert torch.equal(out.logw, prev)
+    assert torch.all(out.ess == 16.0)
+
+
+def test_powersmc_status_and_masked_rows(smc, orc):
+    lg, _, _ = synth.lm_logits(3, 4, 1, 9000, dtype=torch.float32, seed=21, bonus=False)
+    lg[0, 2, 0, 8700] = float("nan")                   # NONFINITE, particle dead
+    lg[1, :, 0, :] = -float("inf")                     # every row masked -> all dead, DEGENERATE
+    lg[2, 1, 0, :8000] = -float("inf")                 # partially masked row: fine
+    gpu, ref = _power_both(smc, orc, lg, 9000, 2.0)
+    assert np_(gpu.status).astype(np.uint32).tolist() == ref["status"].tolist()
+    assert ref["status"].tolist() == [8, 9, 0]
+    assert np.array_equal(np.isneginf(np_(gpu.logw)), np.isneginf(ref["logw"]))
+    assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW

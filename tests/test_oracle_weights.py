@@ -216,3 +216,32 @@ def test_status_flags(orc):
     allbad = np.full((1, 4), -np.inf, np.float32)
     o = orc.weights(lp, lq, tok, V=64, logw_prev=allbad)
     assert o["status"][0] == orc.ST_DEGENERATE and o["lse"][0] == -np.inf and o["ess"][0] == 0.0
+
+
+# ------------------------------------------------------------- PowerSMC (NEXT #4, App. F)
+def test_powersmc_closed_forms(orc):
+    # alpha = 1: per-token weight = log sum p = 0
+    rng = np.random.default_rng(3)
+    lg = (rng.standard_normal((2, 5, 1, 1000)) * 3).astype(np.float32)
+    out = orc.powersmc_weights(lg, alpha=1.0, logw_prev=np.zeros((2, 5), np.float32))
+    assert np.allclose(out["inc"], 0.0, atol=1e-12)
+    # alpha = 2, single-position p = (0.6, 0.4): sum p^2 = 0.52
+    row = np.log(np.array([[[[0.6, 0.4, np.nan, np.nan]]]])).astype(np.float32)
+    out = orc.powersmc_weights(row, V=2, alpha=2.0, logw_prev=np.zeros((1, 1), np.float32))
+    assert out["inc"][0, 0] == pytest.approx(math.log(0.6 ** 2 + 0.4 ** 2), abs=1e-7)
+    # uniform row: sum (1/V)^alpha = V^(1 - alpha)
+    for V, a in ((1000, 0.5), (128, 3.0)):
+        u = np.zeros((1, 1, 1, V), np.float32)
+        out = orc.powersmc_weights(u, alpha=a, logw_prev=np.zeros((1, 1), np.float32))
+        assert out["inc"][0, 0] == pytest.approx((1 - a) * math.log(V), abs=1e-10)
+
+
+def test_powersmc_matches_scipy(orc):
+    from scipy.special import logsumexp, log_softmax
+    rng = np.random.default_rng(8)
+    lg = (rng.standard_normal((1, 3, 2, 3000)) * 2.5).astype(np.float32)
+    for a, tau in ((0.5, 1.0), (4.0, 0.7)):
+        out = orc.powersmc_weights(lg, alpha=a, tau=tau, logw_prev=np.zeros((1, 3), np.float32))
+        for n in range(3):
+            lp = log_softmax(tau * lg[0, n, 0].astype(np.float64))
+            assert out["inc"][0, n] == pytest.approx(logsumexp(a * lp), abs=1e-10)
