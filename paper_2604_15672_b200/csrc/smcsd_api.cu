@@ -101,7 +101,7 @@ smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaSt
 }
 
 // K1 persistent grid: SMs x resident CTAs (shared-memory ring), capped by the work items.
-template <int DT, bool POWER>
+template <int DT, int PW>
 smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     static int ctas[64] = {0};
     int dev = 0;
@@ -109,14 +109,14 @@ smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     const size_t smem = rowstats_smem_bytes<DT>();
     if (ctas[dev] == 0) {
         int occ = 0, sms = 0;
-        if (cudaFuncSetAttribute(k_rowstats<DT, POWER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT, POWER>, kK1Threads, smem) != cudaSuccess ||
+        if (cudaFuncSetAttribute(k_rowstats<DT, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT, PW>, kK1Threads, smem) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || occ < 1)
             return SMCSD_ECUDA;
         ctas[dev] = occ * sms;
     }
     const int64_t grid = items < ctas[dev] ? items : ctas[dev];
-    return launch_pdl_b(k_rowstats<DT, POWER>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
+    return launch_pdl_b(k_rowstats<DT, PW>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
 }
 
 // K2 tail: one CTA per prompt; the per-row S2 statistics live in dynamic shared memory when
@@ -144,13 +144,23 @@ smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks);
 }
 
+template <int PW>
+smcsd_rc launch_rowstats_pw(const Params &prm, int dtype, int64_t items, cudaStream_t st) {
+    return dtype == SMCSD_BF16 ? launch_rowstats_dt<1, PW>(prm, items, st)
+                               : launch_rowstats_dt<0, PW>(prm, items, st);
+}
+
+// power: 0 = plain row statistics; otherwise PowerSMC's second sum, with integer alpha in
+// 1..4 taken by repeated multiplication of the first sum's ex2 (see pow_term).
 smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st,
                          bool power = false) {
-    if (power)
-        return dtype == SMCSD_BF16 ? launch_rowstats_dt<1, true>(prm, items, st)
-                                   : launch_rowstats_dt<0, true>(prm, items, st);
-    return dtype == SMCSD_BF16 ? launch_rowstats_dt<1, false>(prm, items, st)
-                               : launch_rowstats_dt<0, false>(prm, items, st);
+    if (!power) return launch_rowstats_pw<0>(prm, dtype, items, st);
+    const float a = prm.alpha_f;
+    if (a == 1.0f) return launch_rowstats_pw<1>(prm, dtype, items, st);
+    if (a == 2.0f) return launch_rowstats_pw<2>(prm, dtype, items, st);
+    if (a == 3.0f) return launch_rowstats_pw<3>(prm, dtype, items, st);
+    if (a == 4.0f) return launch_rowstats_pw<4>(prm, dtype, items, st);
+    return launch_rowstats_pw<-1>(prm, dtype, items, st);
 }
 
 // Magic multiplier for division by d (1 <= d < 2^31): x / d == (x * mg) >> (32 + sh) for

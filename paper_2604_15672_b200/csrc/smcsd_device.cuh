@@ -11,6 +11,34 @@ constexpr int kSeg = 8192;               // SMCSD_SEGMENT: fixed in-row segment 
 constexpr int kTailMaxN = 1024;          // fused tail / resample keep per-prompt state in smem
 
 // ---- scalars -------------------------------------------------------------------------
+// Packed fp32x2 arithmetic (sm_100a FFMA2 / FADD2 / FMUL2): two lanes of IEEE fp32 per issue
+// slot, each lane rounded exactly as its scalar counterpart (fma fused, add/mul rn).
+__device__ __forceinline__ unsigned long long pk2(float2 a) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long r) {
+    float2 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+    return upk2(r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+    return upk2(r);
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
 #ifdef SMCSD_EXPERIMENT_NO_EX2          // timing experiment only: wrong numerics
     return x * 0.5f;

@@ -119,8 +119,23 @@ __device__ __forceinline__ float load_x(const Params &prm, int model, int64_t pn
 }
 
 // Reduce one item held in registers: lane 0 of each warp writes red[warp] = {m_w, s_w, s2_w}
-// with s2 = sum 2^(alpha (t - m)) for PowerSMC (POWER), 0 otherwise.
-template <int DT, bool POWER = false>
+// with s2 = sum 2^(alpha (t - m)) for PowerSMC (PW != 0), 0 otherwise.  PW = -1: general alpha,
+// a second ex2 per element; PW = k in 1..4: alpha == k, 2^(k t') = (2^t')^k by k-1 multiplies of
+// the ex2 already taken for s (no second MUFU op; keeps the power sum at the HBM roofline).
+template <int PW>
+__device__ __forceinline__ float2 pow_acc(float2 acc, float2 e, float2 t, float alpha) {
+    if (PW == -1) {
+        const float2 ta = fmul2(t, make_float2(alpha, alpha));
+        return fadd2(acc, make_float2(ex2_approx(ta.x), ex2_approx(ta.y)));
+    }
+    if (PW == 1) return fadd2(acc, e);
+    if (PW == 2) return ffma2(e, e, acc);
+    if (PW == 3) return ffma2(fmul2(e, e), e, acc);
+    const float2 e2 = fmul2(e, e);
+    return ffma2(e2, e2, acc);
+}
+
+template <int DT, int PW = 0>
 __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], int nv, float c,
                                             float4 *red, float alpha = 1.0f) {
     using T = ItemTraits<DT>;
@@ -161,42 +176,34 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
     }
     const float mw = warp_max(mt) * c;                       // warp max of t = z*c
     const float off = mw == -INFINITY ? 0.0f : mw;           // all -inf: sum(2^-inf) = 0, NaN kept
-    // sum of 2^(t - m): exactly one ex2 per element (two for PowerSMC)
-    float s_acc[T::kLoads], s2_acc[T::kLoads];
+    // sum of 2^(t - m): exactly one ex2 per element; t and the sums in packed fp32x2 (element
+    // pairs), halving the FMA-pipe issue slots of this issue-bound loop
+    const float2 cc = make_float2(c, c), mo = make_float2(-off, -off);
+    float2 acc[T::kLoads], acc2[T::kLoads];
 #pragma unroll
     for (int i = 0; i < T::kLoads; ++i) {
         const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-        float a = 0.0f, a2 = 0.0f;
-        if (DT == 1) {
+        float2 a = make_float2(0.0f, 0.0f), a2 = make_float2(0.0f, 0.0f);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float t0 = fmaf(bf16lo(w4[k]), c, -off), t1 = fmaf(bf16hi(w4[k]), c, -off);
-                a += ex2_approx(t0);
-                a += ex2_approx(t1);
-                if (POWER) {
-                    a2 += ex2_approx(t0 * alpha);
-                    a2 += ex2_approx(t1 * alpha);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float t0 = fmaf(__uint_as_float(w4[k]), c, -off);
-                a += ex2_approx(t0);
-                if (POWER) a2 += ex2_approx(t0 * alpha);
-            }
+        for (int k = 0; k < (DT == 1 ? 4 : 2); ++k) {
+            const float2 z = DT == 1 ? make_float2(bf16lo(w4[k]), bf16hi(w4[k]))
+                                     : make_float2(__uint_as_float(w4[2 * k]), __uint_as_float(w4[2 * k + 1]));
+            const float2 t = ffma2(z, cc, mo);
+            const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+            a = fadd2(a, e);
+            if (PW) a2 = pow_acc<PW>(a2, e, t, alpha);
         }
-        s_acc[i] = a;
-        s2_acc[i] = a2;
+        acc[i] = a;
+        acc2[i] = a2;
     }
-    float s = s_acc[0], s2 = s2_acc[0];
+    float s = acc[0].x + acc[0].y, s2 = acc2[0].x + acc2[0].y;
 #pragma unroll
     for (int i = 1; i < T::kLoads; ++i) {
-        s += s_acc[i];
-        s2 += s2_acc[i];
+        s += acc[i].x + acc[i].y;
+        s2 += acc2[i].x + acc2[i].y;
     }
     s = warp_sum(s);
-    if (POWER) s2 = warp_sum(s2);
+    if (PW) s2 = warp_sum(s2);
     if (lane == 0) red[warp] = make_float4(mw, s, s2, 0.0f);
 }
 
@@ -288,8 +295,13 @@ constexpr size_t rowstats_smem_bytes() {
          + kStages * (2 * sizeof(uint64_t) + sizeof(StageMeta) + kWarps * sizeof(float4) + 16);
 }
 
-template <int DT, bool POWER>
-__global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_rowstats(const __grid_constant__ Params prm) {
+// bf16 path: SMCSD_K1_MINB CTAs/SM (32 registers); the general-alpha and cube power sums need
+// a few more live registers, one CTA/SM fewer.
+template <int DT, int PW>
+constexpr int k1_min_blocks() { return DT != 1 ? 1 : (PW == -1 || PW == 3) ? SMCSD_K1_MINB - 1 : SMCSD_K1_MINB; }
+
+template <int DT, int PW>
+__global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstats(const __grid_constant__ Params prm) {
     using T = ItemTraits<DT>;
     constexpr uint32_t kStageBytes = (uint32_t)kSeg * T::kEsz;
     extern __shared__ __align__(128) char smem[];
@@ -361,7 +373,7 @@ __global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_row
 #pragma unroll
                 for (int i = 0; i < T::kLoads; ++i)
                     v[i] = *reinterpret_cast<const uint4 *>(sl + (size_t)(i * kThreads + tid) * 16);
-                reduce_item<DT, POWER>(v, m.nv, m.c, r, prm.alpha_f);
+                reduce_item<DT, PW>(v, m.nv, m.c, r, prm.alpha_f);
             }
             __syncwarp();
             int last = 0;
@@ -386,7 +398,7 @@ __global__ void __launch_bounds__(kK1Threads, DT == 1 ? SMCSD_K1_MINB : 1) k_row
                     t += __shfl_xor_sync(0xffffffffu, t, 2);
                     t += __shfl_xor_sync(0xffffffffu, t, 1);
                     float t2 = 0.0f;
-                    if (POWER) {
+                    if (PW) {
                         t2 = lane < kWarps ? rw.z * (rw.x == M ? 1.0f : ex2_approx(d * prm.alpha_f)) : 0.0f;
                         t2 += __shfl_xor_sync(0xffffffffu, t2, 4);
                         t2 += __shfl_xor_sync(0xffffffffu, t2, 2);

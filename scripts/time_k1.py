@@ -39,10 +39,12 @@ if "cfg5" in which:
     ms = t(lambda i: smc.smcsd_weights_partial(lp, lq, tok, v_begin=0, v_len=128256, partials=part, workspace=ws), 30)
     res["cfg5-partial-G1"] = (ms, 262668288 / ms / 1e6)
 if "power" in which:
-    lg, _, _ = synth.lm_logits(64, 32, 1, 128256, device=dev, seed=6, bonus=False)
+    PP = int(os.environ.get("POWER_P", "64"))
+    lg, _, _ = synth.lm_logits(PP, 32, 1, 128256, device=dev, seed=6, bonus=False)
     ws = smc.Workspace(dev); out = smc.Outputs()
-    ms = t(lambda i: smc.smcsd_powersmc_weights(lg, V=128256, alpha=4.0, out=out, workspace=ws), 30)
-    res["power-P64N32"] = (ms, 64 * 32 * 128256 * 2 / ms / 1e6)
+    for al in (4.0, 2.5):
+        ms = t(lambda i: smc.smcsd_powersmc_weights(lg, V=128256, alpha=al, out=out, workspace=ws), 30)
+        res[f"power-P{PP}-a{al}"] = (ms, PP * 32 * 128256 * 2 / ms / 1e6)
     del lg; torch.cuda.empty_cache()
 for k, (ms, gbs) in res.items():
     print(f"{os.path.basename(smc.lib_path):24s} {k:16s} {ms * 1e3:9.2f} us  {gbs:8.1f} GB/s  ({gbs / 6543.7:.3f} of measured)")

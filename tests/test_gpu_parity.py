@@ -436,7 +436,7 @@ def _power_both(smc, orc, lg, V, alpha, tau=1.0, prev=None):
     return gpu, ref
 
 
-@pytest.mark.parametrize("alpha", [0.5, 2.0, 4.0])
+@pytest.mark.parametrize("alpha", [0.5, 2.0, 2.5, 3.0, 4.0])
 @pytest.mark.parametrize("P,N,V,dtype", [(1, 16, 128256, torch.bfloat16), (2, 33, 20001, torch.float32),
                                          (3, 5, 8193, torch.bfloat16), (1, 1, 3, torch.float32)])
 def test_powersmc_weights_parity(smc, orc, P, N, V, dtype, alpha):
