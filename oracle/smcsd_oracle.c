@@ -519,6 +519,104 @@ void orc_select(const float *logw, int P, int N, int64_t prompt_base, uint64_t s
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* Bonus token (NEXT #2; Alg. 1 line "sample bonus token x+ ~ p(. | x, y)";   */
+/* PAPER.md:330 appends it; weight-neutral).  Reading G22: an    */
+/* exact draw from softmax(tau z) of the target row j = k_n (k_n = n_drafted or K) by a      */
+/* two-level sampler with counter-based uniforms:                                             */
+/*   1. segment masses w_i = sum_{v in seg i} exp(tau z_v - M), M = max_v tau z_v, segments  */
+/*      of 8192 columns [8192 i, min(V, 8192 (i+1))); W = sum_i w_i (left to right);          */
+/*   2. U = word0(Philox(key = seed, ctr = (step_lo, step_hi, prompt, 2^31 + 2^20 n))) 2^-32; */
+/*      a = #{i : C_i / W <= U}, C_i = w_0 + ... + w_i  (inverse CDF, as in S6);              */
+/*   3. Gumbel-max inside segment a: for column v = 8192 a + 4 q + k, word k of               */
+/*      Philox(ctr = (step_lo, step_hi, prompt, 2^31 + 2^20 n + 1 + q)) gives                  */
+/*      u_v = (word + 1/2) 2^-32, E_v = -ln u_v (= -log1p(-(1 - u_v)) for u_v >= 1/2),        */
+/*      g_v = -ln E_v; x+ = argmax_v (tau z_v + g_v), smallest v on equal keys.               */
+/* P(x+ = v) = (w_a / W) (exp(tau z_v - M) / w_a) = softmax(tau z)_v, exactly.                */
+/* margins (optional, test tolerance for rounding-order near-ties, reading G7):               */
+/*   seg_margin[pn] = min_i |C_i / W - U|,  key_margin[pn] = key(x+) - second-best key.       */
+/* Invalid k_n: -1 and BAD_TOKEN; NaN / +inf logit or an all -inf row: -1 and NONFINITE.      */
+/* ------------------------------------------------------------------------------------ */
+#define ORC_BONUS_SEG 8192
+void orc_bonus(const void *logits_p, int64_t ld, int rpp, int dtype, const int32_t *n_drafted,
+               int P, int N, int K, int64_t V, double tau, uint64_t seed, uint64_t step,
+               int64_t prompt_base, int32_t *bonus, double *seg_margin, double *key_margin,
+               uint32_t *status)
+{
+    const double two_m32 = 1.0 / 4294967296.0;
+    size_t esz = dtype == 1 ? 2 : 4;
+    int64_t nseg = (V + ORC_BONUS_SEG - 1) / ORC_BONUS_SEG;
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int p = 0; p < P; ++p) {
+        uint32_t st = 0;
+        uint32_t prompt = (uint32_t)(uint64_t)(prompt_base + p);
+        for (int n = 0; n < N; ++n) {
+            int64_t pn = (int64_t)p * N + n;
+            bonus[pn] = -1;
+            if (seg_margin) seg_margin[pn] = INFINITY;
+            if (key_margin) key_margin[pn] = INFINITY;
+            int kn = n_drafted ? n_drafted[pn] : K;
+            if (kn < 0 || kn > K) { st |= ORC_ST_BAD_TOKEN; continue; }
+            const char *row = (const char *)logits_p + (pn * rpp + kn) * ld * (int64_t)esz;
+            /* step 1: M, segment masses */
+            double M = -INFINITY;
+            int bad = 0;
+            for (int64_t v = 0; v < V; ++v) {
+                double y = tau * decode_logit(row, dtype, v);
+                if (isnan(y) || y == INFINITY) bad = 1;
+                else if (y > M) M = y;
+            }
+            if (bad || M == -INFINITY) { st |= ORC_ST_NONFINITE; continue; }
+            double W = 0.0, C[4096];
+            if (nseg > 4096) { st |= ORC_ST_NONFINITE; continue; }
+            for (int64_t i = 0; i < nseg; ++i) {
+                double w = 0.0;
+                int64_t e = (i + 1) * ORC_BONUS_SEG < V ? (i + 1) * ORC_BONUS_SEG : V;
+                for (int64_t v = i * ORC_BONUS_SEG; v < e; ++v)
+                    w = w + exp(tau * decode_logit(row, dtype, v) - M);
+                W = W + w;
+                C[i] = W;
+            }
+            /* step 2: segment by inverse CDF */
+            uint32_t ctr[4] = {(uint32_t)step, (uint32_t)(step >> 32), prompt,
+                               0x80000000u + ((uint32_t)n << 20)};
+            uint32_t r[4];
+            orc_philox4x32_10(ctr, key, r);
+            double U = (double)r[0] * two_m32;
+            int64_t a = 0;
+            double mg = INFINITY;
+            for (int64_t i = 0; i < nseg; ++i) {
+                double c = C[i] / W;
+                if (c <= U) a++;
+                if (fabs(c - U) < mg) mg = fabs(c - U);
+            }
+            if (a >= nseg) a = nseg - 1;     /* U < 1 = C_last / W: unreachable up to rounding */
+            /* step 3: Gumbel-max inside segment a */
+            int64_t v0 = a * ORC_BONUS_SEG;
+            int64_t nv = V - v0 < ORC_BONUS_SEG ? V - v0 : ORC_BONUS_SEG;
+            double best = -INFINITY, second = -INFINITY;
+            int64_t arg = -1;
+            for (int64_t i = 0; i < nv; ++i) {
+                if (i % 4 == 0) {
+                    ctr[3] = 0x80000000u + ((uint32_t)n << 20) + 1u + (uint32_t)(i / 4);
+                    orc_philox4x32_10(ctr, key, r);
+                }
+                uint32_t w = r[i % 4];
+                double E;
+                if (w < 0x80000000u) E = -log(((double)w + 0.5) * two_m32);
+                else E = -log1p(-(((double)(0xFFFFFFFFu - w) + 0.5) * two_m32));
+                double k = tau * decode_logit(row, dtype, v0 + i) - log(E);
+                if (k > best) { second = best; best = k; arg = v0 + i; }
+                else if (k > second) second = k;
+            }
+            bonus[pn] = (int32_t)arg;
+            if (seg_margin) seg_margin[pn] = mg;
+            if (key_margin) key_margin[pn] = best - second;
+        }
+        if (status) status[p] = st;
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* Paged KV reindex (NEXT #1; Sec. 3.3 Obs. 2: "resampling by copying page */
 /* metadata and incrementing the reference counts"; SPEC.md:466-474 resample_pages).        */
 /* table[p][n][0 .. n_pages[p][n]) lists particle n's KV pages.  After the call particle n   */

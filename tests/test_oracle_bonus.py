@@ -1,0 +1,130 @@
+"""Pins for the bonus-token oracle (NEXT #2; reading G22 in DESIGN.md).
+
+The sampler must be an exact draw from softmax(tau z) of target row k_n.  Pinned by what the
+mathematics fixes, not by retyping the sampler: chi-square frequency tests against the softmax
+(across segments, ragged tail included), point masses, the tau -> inf argmax limit, invariance
+to a constant shift, uniform rows (segment frequency proportional to segment size), row choice
+by n_drafted, and the invalid-input policy."""
+import math
+
+import numpy as np
+import pytest
+from scipy import stats
+
+SEG = 8192
+
+
+def _rows(P, N, R, V, fill=-np.inf):
+    return np.full((P, N, R, V), fill, np.float32)
+
+
+def _draws(orc, lg, K, V, steps, **kw):
+    out = []
+    for s in range(steps):
+        r = orc.bonus(lg, K=K, V=V, step=s, **kw)
+        assert np.all(r["status"] == 0)
+        out.append(r["bonus"].ravel())
+    return np.concatenate(out)
+
+
+def test_frequencies_match_softmax_across_segments(orc):
+    V = 3 * SEG + 100                                     # ragged last segment
+    hot = np.array([5, 4000, 8191, 8192, 12000, 16383, 20000, 3 * SEG + 99])
+    z = np.array([1.0, 0.3, -0.5, 0.8, 0.0, 1.2, -1.0, 0.6], np.float32)
+    N, steps = 256, 12
+    lg = _rows(1, N, 1, V)
+    lg[..., hot] = z
+    b = _draws(orc, lg, 0, V, steps)
+    assert set(np.unique(b)) <= set(hot.tolist())
+    cnt = np.array([(b == h).sum() for h in hot])
+    p = np.exp(z.astype(np.float64)); p /= p.sum()
+    chi2 = ((cnt - p * b.size) ** 2 / (p * b.size)).sum()
+    assert stats.chi2.sf(chi2, len(hot) - 1) > 1e-3, (cnt, p * b.size)
+
+
+def test_temperature_scales_the_logits(orc):
+    V = 40
+    z = np.linspace(-1, 1, V).astype(np.float32)
+    lg = np.broadcast_to(z, (1, 512, 1, V)).copy()
+    tau = 2.5
+    b = _draws(orc, lg, 0, V, 8, tau=tau)
+    p = np.exp(tau * z.astype(np.float64)); p /= p.sum()
+    cnt = np.bincount(b, minlength=V)
+    # pool the low-probability tail so every cell expects >= 5 draws
+    order = np.argsort(p)
+    e = p[order] * b.size
+    k = np.searchsorted(np.cumsum(e), 5.0) + 1
+    obs = np.concatenate([[cnt[order[:k]].sum()], cnt[order[k:]]])
+    exp_ = np.concatenate([[e[:k].sum()], e[k:]])
+    chi2 = ((obs - exp_) ** 2 / exp_).sum()
+    assert stats.chi2.sf(chi2, len(obs) - 1) > 1e-3
+
+
+def test_point_mass_and_argmax_limit(orc):
+    V = 2 * SEG + 7
+    lg = _rows(2, 3, 1, V)
+    lg[0, :, 0, 2 * SEG + 6] = 0.0                         # only finite column, ragged segment
+    lg[1, :, 0, :] = np.linspace(-3, 3, V, dtype=np.float32)
+    r = orc.bonus(lg, K=0, V=V)
+    assert np.all(r["bonus"][0] == 2 * SEG + 6)
+    # tau -> inf: softmax -> argmax.  Logit spacing 3.66e-4; at tau = 1e5 the key gap (36.6)
+    # exceeds the whole Gumbel range g in [-ln(-ln 2^-33), -ln(-ln(1 - 2^-33))] = [-3.1, 22.9]
+    r = orc.bonus(lg, K=0, V=V, tau=1e5, step=3)
+    assert np.all(r["bonus"][1] == V - 1)
+    assert np.all(r["status"] == 0)
+
+
+def test_shift_invariance(orc):
+    rng = np.random.default_rng(3)
+    V = SEG + 500
+    lg = rng.integers(-8, 8, size=(2, 16, 1, V)).astype(np.float32)
+    a = orc.bonus(lg, K=0, V=V, step=11)
+    b = orc.bonus(lg + 4.0, K=0, V=V, step=11)             # exact in fp32 and fp64
+    ok = (a["seg_margin"] > 1e-9) & (a["key_margin"] > 1e-9)
+    assert ok.mean() > 0.95
+    assert np.array_equal(a["bonus"][ok], b["bonus"][ok])
+
+
+def test_uniform_row_segment_frequencies(orc):
+    V = 2 * SEG + 1000
+    lg = np.zeros((1, 512, 1, V), np.float32)
+    b = _draws(orc, lg, 0, V, 6)
+    seg = b // SEG
+    sizes = np.array([SEG, SEG, 1000], np.float64)
+    cnt = np.bincount(seg, minlength=3)
+    e = sizes / sizes.sum() * b.size
+    assert stats.chi2.sf(((cnt - e) ** 2 / e).sum(), 2) > 1e-3
+    # inside a segment the draw is uniform: mean position ~ (size - 1) / 2
+    pos = b[seg == 0] % SEG
+    assert abs(pos.mean() - (SEG - 1) / 2) < 4 * SEG / math.sqrt(12 * pos.size)
+
+
+def test_row_is_k_n_and_invalid_inputs(orc):
+    V, K = 64, 4
+    lg = _rows(2, 5, K + 1, V)
+    for j in range(K + 1):
+        lg[:, :, j, 7 * j] = 0.0                           # row j: point mass at column 7 j
+    nd = np.array([[0, 1, 2, 3, 4], [4, 4, 4, 4, 4]], np.int32)
+    r = orc.bonus(lg, K=K, V=V, n_drafted=nd)
+    assert r["bonus"].tolist() == [[0, 7, 14, 21, 28], [28] * 5]
+    assert r["status"].tolist() == [0, 0]
+    r = orc.bonus(lg, K=K, V=V)                            # n_drafted = NULL -> row K
+    assert np.all(r["bonus"] == 28)
+    nd[0, 2] = 5
+    lg[1, 3, K, 50] = np.nan
+    r = orc.bonus(lg, K=K, V=V, n_drafted=nd)
+    assert r["bonus"][0, 2] == -1 and r["bonus"][1, 3] == -1
+    assert r["status"].tolist() == [orc.ST_BAD_TOKEN, orc.ST_NONFINITE]
+    lg[1, 3, K, :] = -np.inf                               # all -inf row
+    assert orc.bonus(lg, K=K, V=V)["status"][1] == orc.ST_NONFINITE
+
+
+def test_streams_differ_by_particle_step_and_seed(orc):
+    V = 1000
+    lg = np.zeros((1, 64, 1, V), np.float32)
+    a = orc.bonus(lg, K=0, V=V, step=1)["bonus"].ravel()
+    b = orc.bonus(lg, K=0, V=V, step=2)["bonus"].ravel()
+    c = orc.bonus(lg, K=0, V=V, step=1, seed=7)["bonus"].ravel()
+    d = orc.bonus(lg, K=0, V=V, step=1, prompt_base=1)["bonus"].ravel()
+    assert len(np.unique(a)) > 55                         # 64 draws from 1000: few collisions
+    assert (a != b).mean() > 0.9 and (a != c).mean() > 0.9 and (a != d).mean() > 0.9
