@@ -130,7 +130,15 @@ SMCSD_API smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t promp
 /* Fused S1-S7 in one enqueue (one launch: row statistics + last-CTA-per-prompt tail), the
  * performance path.  Arguments as smcsd_weights + smcsd_resample; N <= 1024.
  *  logw_pre [P][N] (optional): lam' before the S7 reset -- the exact fp32 values the
- *  resampling consumed (staged parity).  logw_out receives the S7 output. */
+ *  resampling consumed (staged parity).  logw_out receives the S7 output.
+ *  bonus_tok [P][N] (optional, NEXT #2; "sample bonus token x+ ~ p"): when
+ *  non-NULL the target's row j = k_n (rows_per_particle_p >= K + 1) is streamed in the same
+ *  K1 pass and bonus_tok[p][n] receives one exact draw from softmax(inv_temp_p * z) of that
+ *  row (reading G22: segment by inverse CDF, then Gumbel-max, Philox counters
+ *  (step, prompt_base + p, 2^31 + 2^20 n + i)).  Indexed by the particle BEFORE resampling
+ *  (append it, then reindex the history with the ancestors).  -1 with
+ *  NONFINITE (NaN / +inf / all -inf row) or BAD_TOKEN (k_n outside [0, K]).  V <= 2^21.
+ *  The bonus row does not enter the weights (it cancels). */
 SMCSD_API smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
                     const void *logits_q, int64_t ld_q, int rows_per_particle_q,
                     int dtype, const int32_t *tokens, const int32_t *n_drafted,
@@ -141,7 +149,7 @@ SMCSD_API smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_p
                     float *logw_out, float *logw_pre, float *logp_tok, float *logq_tok,
                     double *lse_out, double *ess_out, float *wnorm_out, uint32_t *status,
                     int32_t *ancestors, int32_t *offspring, int32_t *slot_src,
-                    uint8_t *resampled, int32_t *n_ties,
+                    uint8_t *resampled, int32_t *n_ties, int32_t *bonus_tok,
                     void *workspace, size_t workspace_bytes, void *stream);
 
 /* S1 on this rank's vocabulary shard (tensor-parallel, north star).  Row pointers address

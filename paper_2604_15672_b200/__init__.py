@@ -57,7 +57,7 @@ def _load():
                                  vp, vp, vp, vp, vp, vp]
     L.smcsd_step.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp, i32, i32, i32, i64,
                              f32, f32, f32, f32, i32, u64, u64, i64, vp,
-                             vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+                             vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.smcsd_weights_partial.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, i32, i32, i32,
                                         i64, i64, f32, f32, vp, vp, sz, vp]
     L.smcsd_weights_combine.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i64, f32, vp, vp, vp,
@@ -175,6 +175,7 @@ class Outputs:
     resampled: torch.Tensor = None
     n_ties: torch.Tensor = None
     partials: torch.Tensor = None
+    bonus: torch.Tensor = None
 
 
 def _alloc(out: Outputs, dev, P, N, K, fields):
@@ -184,7 +185,7 @@ def _alloc(out: Outputs, dev, P, N, K, fields):
                   wnorm=((P, N), torch.float32), status=((P,), torch.int32),
                   ancestors=((P, N), torch.int32), offspring=((P, N), torch.int32),
                   slot_src=((P, N), torch.int32), resampled=((P,), torch.uint8),
-                  n_ties=((P,), torch.int32))
+                  n_ties=((P,), torch.int32), bonus=((P, N), torch.int32))
     for f in fields:
         if getattr(out, f) is None:
             shp, dt = shapes[f]
@@ -222,8 +223,9 @@ def smcsd_step(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=
                alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, eta=math.inf,
                scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
                out: Outputs | None = None, fields=_ALL_S, workspace=None,
-               stream=None) -> Outputs:
-    """Fused S1-S7 (one launch)."""
+               stream=None, bonus=False) -> Outputs:
+    """Fused S1-S7 (one launch).  bonus=True also draws the bonus token x+ of every particle
+    from target row k_n (NEXT #2; logits_p needs K+1 rows) into out.bonus [P][N]."""
     ld_p, rpp_p = _logits_geom(logits_p, "logits_p")
     ld_q, rpp_q = _logits_geom(logits_q, "logits_q")
     if logits_p.dtype != logits_q.dtype:
@@ -232,7 +234,8 @@ def smcsd_step(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=
     V = ld_p if V is None else V
     dev = logits_p.device
     out = _alloc(out or Outputs(), dev, P, N, K,
-                 ("logw", "status", "ancestors", "resampled") + tuple(fields))
+                 ("logw", "status", "ancestors", "resampled") + tuple(fields)
+                 + (("bonus",) if bonus else ()))
     ws = _ws(workspace, dev, P, N, K, V, stream)
     rc = _lib.smcsd_step(_p(logits_p), ld_p, rpp_p, _p(logits_q), ld_q, rpp_q,
                          _dtype_code(logits_p), _p(tokens), _p(n_drafted), _p(logw_prev),
@@ -241,7 +244,8 @@ def smcsd_step(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=
                          _p(out.logw), _p(out.logw_pre), _p(out.logp_tok), _p(out.logq_tok),
                          _p(out.lse), _p(out.ess), _p(out.wnorm), _p(out.status),
                          _p(out.ancestors), _p(out.offspring), _p(out.slot_src),
-                         _p(out.resampled), _p(out.n_ties), _p(ws), ws.numel(), _stream(stream))
+                         _p(out.resampled), _p(out.n_ties), _p(out.bonus) if bonus else None,
+                         _p(ws), ws.numel(), _stream(stream))
     _check("smcsd_step", rc)
     return out
 

@@ -33,7 +33,7 @@ WsLayout ws_layout(int P, int N, int K, int64_t v_len) {
     L.ctr = off;      off += 256;
     L.pctr = off;     off += align256((size_t)P * sizeof(unsigned));
     L.pst = off;      off += align256((size_t)P * sizeof(uint32_t));
-    L.parts = off;    off += align256(rows * nseg * sizeof(float4));
+    L.parts = off;    off += align256((rows + (size_t)P * N) * nseg * sizeof(float4));  // + bonus rows
     L.ell = off;      off += align256(rows * sizeof(double));
     L.lam = off;      off += align256((size_t)P * N * sizeof(float));
     L.e = off;        off += align256((size_t)P * N * sizeof(double));
@@ -139,9 +139,10 @@ smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     if (ensure_tail_attrs() != SMCSD_OK) return SMCSD_ECUDA;
     if (prm.N > kTailMaxN) return launch_pdl(k_tail_large, (unsigned)prm.P, kTailStageBytes, st, prm);
     const int chunks = (int)cdiv((int64_t)prm.N * prm.K, kPairsPerCta);
-    const int64_t grid = (int64_t)prm.P * chunks;
+    const int bonus_ctas = prm.bonus_tok ? prm.N : 0;
+    const int64_t grid = (int64_t)prm.P * chunks + (int64_t)prm.P * bonus_ctas;
     if (grid >= (1ll << 31)) return SMCSD_EINVAL;
-    return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks);
+    return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks, bonus_ctas);
 }
 
 template <int PW>
@@ -193,6 +194,8 @@ Params logits_params(const void *lp, int64_t ld_p, int rpp_p, const void *lq, in
     prm.x_from_logits = 1;
     prm.n_models = 2;
     prm.alpha_f = 1.0f;
+    prm.main_items = 2ll * P * N * K * prm.nseg;
+    prm.bonus_items = 0;
     return prm;
 }
 
@@ -273,11 +276,14 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
                     float *logw_pre, float *logp_tok, float *logq_tok, double *lse_out,
                     double *ess_out, float *wnorm_out, uint32_t *status, int32_t *ancestors,
                     int32_t *offspring, int32_t *slot_src, uint8_t *resampled, int32_t *n_ties,
-                    void *workspace, size_t workspace_bytes, void *stream) {
+                    int32_t *bonus_tok, void *workspace, size_t workspace_bytes, void *stream) {
     smcsd_rc rc = check_logits(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
                                rows_per_particle_q, dtype, tokens, P, N, K, V);
     if (rc != SMCSD_OK) return rc;
     if (!logw_out || !status || !ancestors || !resampled || !workspace) return SMCSD_EINVAL;
+    if (bonus_tok && (rows_per_particle_p < K + 1 || cdiv(V, kSeg) > kBonusMaxSeg ||
+                      (2ll * K + 1) * P * N * cdiv(V, kSeg) >= (1ll << 31)))
+        return SMCSD_EINVAL;
     if (N > kTailMaxN || std::isnan(eta)) return SMCSD_EINVAL;
     if (!(std::isfinite(alpha) && alpha > 0.0f) || !valid_temp(inv_temp_p) || !valid_temp(inv_temp_q))
         return SMCSD_EINVAL;
@@ -297,11 +303,13 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
     prm.logq_tok = logq_tok; prm.lse = lse_out; prm.ess = ess_out; prm.wnorm = wnorm_out;
     prm.status = status; prm.ancestors = ancestors; prm.offspring = offspring;
     prm.slot_src = slot_src; prm.resampled = resampled; prm.n_ties = n_ties;
+    prm.bonus_tok = bonus_tok;
+    if (bonus_tok) prm.bonus_items = (long long)P * N * prm.nseg;
     bind_workspace(prm, workspace, L);
     prm.parts = prm.part_ws; prm.part_row_stride = prm.nseg; prm.part_seg_stride = 1;
     prm.nparts = prm.nseg;
     cudaStream_t st = as_stream(stream);
-    rc = launch_rowstats(prm, dtype, 2ll * P * N * K * prm.nseg, st);
+    rc = launch_rowstats(prm, dtype, prm.main_items + prm.bonus_items, st);
     if (rc != SMCSD_OK) return rc;
     return launch_tail(prm, 1, st);
 }
@@ -445,6 +453,7 @@ smcsd_rc smcsd_powersmc_weights(const void *logits, int64_t ld, int rows_per_par
     Params prm = logits_params(logits, ld, rows_per_particle, logits, ld, rows_per_particle,
                                nullptr, nullptr, P, N, 1, V, 0, V, inv_temp, inv_temp);
     prm.n_models = 1;
+    prm.main_items = (long long)P * N * prm.nseg;
     prm.alpha_f = alpha;
     prm.dtype = dtype;
     prm.logw_prev = logw_prev;

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <type_traits>
 #include "smcsd_device.cuh"
 
 namespace smcsd {
@@ -53,6 +54,9 @@ struct Params {
     double *lse, *ess;
     uint32_t *status;
     int32_t *ancestors, *offspring, *slot_src, *n_ties;
+    int32_t *bonus_tok;                         // [P][N] bonus token (NEXT #2) or null
+    long long main_items;                       // K1 items of the weight rows
+    long long bonus_items;                      // K1 items of the bonus rows (P*N*nseg or 0)
     uint8_t *resampled;
     float4 *partials_out;                       // MODE_PARTIAL: [P*2*N*K] {m, s, x, 0}
     // ---- S2 sources: row r's parts at parts[r*part_row_stride + i*part_seg_stride], i < nparts
@@ -224,6 +228,19 @@ struct ItemInfo {
 template <int DT>
 __device__ __forceinline__ ItemInfo item_info(const Params &prm, long long item) {
     ItemInfo f;
+    constexpr int kEsz0 = ItemTraits<DT>::kEsz;
+    if (item >= prm.main_items) {                           // bonus row k_n of target particle pn
+        const unsigned b = (unsigned)(item - prm.main_items);
+        const unsigned pn = fastdiv(b, prm.mg_nseg, prm.sh_nseg);
+        const int seg = (int)(b - pn * (unsigned)prm.nseg);
+        const int kn = prm.n_drafted ? prm.n_drafted[pn] : prm.K;
+        f.valid = kn >= 0 && kn <= prm.K;
+        const int64_t v0 = (int64_t)seg * kSeg;
+        f.seg = prm.lp + (((int64_t)pn * prm.rpp_p + (f.valid ? kn : 0)) * prm.ld_p + v0) * kEsz0;
+        f.nv = (int)min((int64_t)kSeg, prm.v_len - v0);
+        f.c = prm.c_p;
+        return f;
+    }
     const unsigned u = (unsigned)item;                      // total < 2^31 (validated)
     unsigned row = fastdiv(u, prm.mg_nseg, prm.sh_nseg);
     const int seg = (int)(u - row * (unsigned)prm.nseg);
@@ -311,7 +328,7 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
     float4 *red = reinterpret_cast<float4 *>(meta + kStages);       // [kStages][kWarps]
     int *done = reinterpret_cast<int *>(red + kStages * kWarps);    // [kStages]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const long long total = (long long)prm.n_models * prm.P * prm.N * prm.K * prm.nseg;
+    const long long total = prm.main_items + prm.bonus_items;
 
     if (tid == 0) {
         SMCSD_TRACE_AT(blockIdx.x & 1023);                      // K1 CTA start
@@ -326,6 +343,12 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
 
     if (warp == kWarps) {
         // ------------------------------------------------------------------ producer
+        if (prm.bonus_tok) {
+            // status[] is OR-ed by the bonus CTAs of the tail: zero it here, after the
+            // predecessor (the previous call's tail) has completed.
+            pdl_wait();
+            for (int q = (int)blockIdx.x * 32 + lane; q < prm.P; q += (int)gridDim.x * 32) prm.status[q] = 0u;
+        }
         if (lane == 0) {
             // The predecessor may have produced the logits (or re-armed work_ctr): wait for it
             // before the first global access.  Setup above overlapped its tail.
@@ -757,17 +780,224 @@ __device__ __forceinline__ float3 lane_premerge(const Params &prm, int64_t grow,
     return make_float3(M, S, X);
 }
 
-__global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Params prm, int resample_mode,
-                                                   int chunks_per_prompt) {
-    __shared__ TailSmem sh;
-    __shared__ float4 rs[2 * kPairsPerCta];
-    __shared__ double ell_s[2 * kPairsPerCta];
+
+// ---- bonus token (NEXT #2; "sample x+ ~ p(. | x, y)"; reading G22) -------------
+// One CTA per particle n of prompt p, inside k_tail's grid.  Exact draw from softmax(tau z) of
+// target row k_n: (1) segment a by inverse CDF over the K1 segment masses w_i = s_i 2^(m_i - M)
+// with U = word0(Philox(ctr = (step, prompt, 2^31 + 2^20 n))); (2) Gumbel-max over segment a:
+// key_v = tau z_v log2(e) - log2(E_v), E_v = -ln u_v from Philox word k of
+// ctr word3 = 2^31 + 2^20 n + 1 + q (column 4q + k of the segment).  The Gumbel terms do not
+// depend on a, so they are drawn before griddepcontrol.wait, overlapping K1's drain.
+constexpr int kBonusBlocks = kSeg / 4 / kThreads;           // Philox blocks per thread (8)
+constexpr int kBonusMaxSeg = 256;                           // V <= 2^21 for the bonus row
+
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// -log2(E), E = -ln u, u = (w + 1/2) 2^-32, branch-free.  Small E (u near 1) decides the
+// argmax, so E keeps ~1e-6 relative accuracy everywhere: u < 1/2: -ln u; u >= 1/2 with
+// r = 1 - u = (~w + 1/2) 2^-32 (exact to 2^-24 relative): r < 1/16: the log1p series
+// r + r^2/2 + ... + r^7/7 (truncation < r^8/8 < 2^-26 r); else -ln(1 - r).
+__device__ __forceinline__ float gumbel2(uint32_t w) {
+    const float u = fmaf((float)w, 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+    const float r = fmaf((float)(~w), 2.3283064365386963e-10f, 1.1641532182693481e-10f);
+    const float Ea = -lg2_approx(u) * 0.6931471805599453f;
+    const float Eb = -lg2_approx(1.0f - r) * 0.6931471805599453f;
+    float Ec = fmaf(r, 1.0f / 7.0f, 1.0f / 6.0f);
+    Ec = fmaf(r, Ec, 0.2f);
+    Ec = fmaf(r, Ec, 0.25f);
+    Ec = fmaf(r, Ec, 1.0f / 3.0f);
+    Ec = fmaf(r, Ec, 0.5f);
+    Ec = fmaf(r, Ec, 1.0f);
+    Ec *= r;
+    const float E = w < 0x80000000u ? Ea : (r < 0.0625f ? Ec : Eb);
+    return -lg2_approx(E);
+}
+
+struct BonusSmem {
+    float4 g2[kSeg / 4];        // Gumbel terms -log2(E) of the segment's columns (pre-wait)
+    double C[kBonusMaxSeg];
+    float m[kBonusMaxSeg], s[kBonusMaxSeg];
+    float bk[kWarps];
+    int bi[kWarps];
+    int a;
+    uint32_t st;
+};
+
+template <int DT>
+__device__ __noinline__ uint32_t bonus_role(const Params &prm, int p, int n, BonusSmem &bs) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t pn = (int64_t)p * prm.N + n;
+    const uint2 key = make_uint2((uint32_t)prm.seed, (uint32_t)(prm.seed >> 32));
+    const uint32_t prompt = (uint32_t)(uint64_t)(prm.prompt_base + p);
+    const uint32_t w3 = 0x80000000u + ((uint32_t)n << 20);
+    const uint32_t s0 = (uint32_t)prm.step, s1 = (uint32_t)(prm.step >> 32);
+    const int kn = prm.n_drafted ? prm.n_drafted[pn] : prm.K;
+    double U = 0.0;
+    if (tid == 0) U = (double)philox4x32_10(make_uint4(s0, s1, prompt, w3), key).x * 2.3283064365386962890625e-10;
+    // The Gumbel terms do not depend on the segment: draw them before griddepcontrol.wait so
+    // they overlap K1's drain (this CTA becomes resident as K1 CTAs retire).
+#pragma unroll 2
+    for (int r = 0; r < kBonusBlocks; ++r) {
+        const int q = tid + kThreads * r;
+        const uint4 w = philox4x32_10(make_uint4(s0, s1, prompt, w3 + 1u + (uint32_t)q), key);
+        bs.g2[q] = make_float4(gumbel2(w.x), gumbel2(w.y), gumbel2(w.z), gumbel2(w.w));
+    }
+    pdl_wait();
+    const int nseg = prm.nseg;
+    if (warp == 0) {
+        // (1) segment masses from K1's partials (one L2 round trip), fp64 prefix on lane 0,
+        // (2) a = #{i : C_i <= U W} counted across lanes
+        const float4 *parts = prm.part_ws + prm.main_items + pn * nseg;
+        float mloc = -INFINITY;
+        for (int i = lane; i < nseg; i += 32) {
+            const float4 q = __ldcg(&parts[i]);
+            bs.m[i] = q.x;
+            bs.s[i] = q.y;
+            mloc = fmaxf(mloc, q.x);
+        }
+        const float M = warp_max(mloc);
+        __syncwarp();
+        uint32_t st = 0;
+        double W = 0.0;
+        if (lane == 0) {
+            if (kn < 0 || kn > prm.K) {
+                st = ST_BAD_TOKEN;
+            } else if (!isfinite(M)) {
+                st = ST_NONFINITE;
+            } else {
+                for (int i = 0; i < nseg; ++i) {
+                    const float w = bs.s[i] * (bs.m[i] == M ? 1.0f : ex2_approx(bs.m[i] - M));
+                    W = __dadd_rn(W, (double)w);
+                    bs.C[i] = W;
+                }
+                if (isnan(W)) st = ST_NONFINITE;
+            }
+        }
+        st = __shfl_sync(0xffffffffu, st, 0);
+        const double T = __shfl_sync(0xffffffffu, U * W, 0);
+        __syncwarp();
+        int cnt = 0;
+        if (!st)
+            for (int i = lane; i < nseg; i += 32) cnt += bs.C[i] <= T;
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) {
+            bs.a = st ? -1 : min(cnt, nseg - 1);
+            bs.st = st;
+        }
+    }
+    __syncthreads();
+    const int a = bs.a;
+    const uint32_t st = bs.st;
+    if (a < 0) {
+        if (tid == 0) prm.bonus_tok[pn] = -1;
+        return st;
+    }
+    const int64_t v0 = (int64_t)a * kSeg;
+    const int nv = (int)min((int64_t)kSeg, prm.V - v0);
+    const float c = prm.c_p;
+    const char *row = prm.lp + ((int64_t)pn * prm.rpp_p + kn) * prm.ld_p * (DT == 1 ? 2 : 4);
+    // (3) Gumbel-max over segment a: key = z c + g2 (log2 units), smallest column on ties
+    using Raw = typename std::conditional<DT == 1, uint2, uint4>::type;
+    Raw raw[kBonusBlocks];
+#pragma unroll
+    for (int r = 0; r < kBonusBlocks; ++r) {
+        const int i0 = 4 * (tid + kThreads * r);
+        if (i0 < nv) raw[r] = __ldcs(reinterpret_cast<const Raw *>(row + (v0 + i0) * (DT == 1 ? 2 : 4)));
+    }
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < kBonusBlocks; ++r) {
+        const int q = tid + kThreads * r, i0 = 4 * q;
+        if (i0 < nv) {
+            const float4 g = bs.g2[q];
+            const float gk[4] = {g.x, g.y, g.z, g.w};
+            float z[4];
+            if (DT == 1) {
+                const uint2 b = *reinterpret_cast<const uint2 *>(&raw[r]);
+                z[0] = bf16lo(b.x); z[1] = bf16hi(b.x); z[2] = bf16lo(b.y); z[3] = bf16hi(b.y);
+            } else {
+                const uint4 b = *reinterpret_cast<const uint4 *>(&raw[r]);
+                z[0] = __uint_as_float(b.x); z[1] = __uint_as_float(b.y);
+                z[2] = __uint_as_float(b.z); z[3] = __uint_as_float(b.w);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float kv = fmaf(z[k], c, gk[k]);
+                if (i0 + k < nv && kv > best) {
+                    best = kv;
+                    bi = i0 + k;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    if (lane == 0) {
+        bs.bk[warp] = best;
+        bs.bi[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        best = bs.bk[0];
+        bi = bs.bi[0];
+        for (int w = 1; w < kWarps; ++w)
+            if (bs.bk[w] > best || (bs.bk[w] == best && bs.bi[w] < bi)) {
+                best = bs.bk[w];
+                bi = bs.bi[w];
+            }
+        prm.bonus_tok[pn] = bi == 0x7fffffff ? -1 : (int32_t)(v0 + bi);
+    }
+    return st;
+}
+
+__global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Params prm, int resample_mode,
+                                                   int chunks_per_prompt, int bonus_ctas) {
+    // chunk CTAs and bonus CTAs use disjoint shared state: one buffer, two views
+    struct ChunkSmem {
+        TailSmem sh;
+        float4 rs[2 * kPairsPerCta];
+        double ell_s[2 * kPairsPerCta];
+    };
+    constexpr size_t kSmemBytes = sizeof(ChunkSmem) > sizeof(BonusSmem) ? sizeof(ChunkSmem) : sizeof(BonusSmem);
+    __shared__ __align__(16) unsigned char smem_raw[kSmemBytes];
+    ChunkSmem &cs = *reinterpret_cast<ChunkSmem *>(smem_raw);
+    BonusSmem &bsm = *reinterpret_cast<BonusSmem *>(smem_raw);
+    TailSmem &sh = cs.sh;
+    float4 *rs = cs.rs;
+    double *ell_s = cs.ell_s;
     __shared__ int s_last;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int p = blockIdx.x / chunks_per_prompt, c = blockIdx.x - p * chunks_per_prompt;
+    const int tid = threadIdx.x;
     const int N = prm.N, K = prm.K, NK = N * K, rows = 2 * NK;
+    const int chunk_ctas = prm.P * chunks_per_prompt;
+    if ((int)blockIdx.x >= chunk_ctas) {
+        // bonus-token CTA (NEXT #2), after every chunk CTA in launch order.  Off the S3-S7
+        // critical path: it does not take part in the completion count, and its flags are
+        // OR-ed into status[p] (zeroed by K1's producer warp after its griddepcontrol.wait;
+        // the last chunk CTA ORs its own bits when bonus CTAs exist).
+        const int b = (int)blockIdx.x - chunk_ctas, p = b / N;
+        const uint32_t bst = prm.dtype == 1 ? bonus_role<1>(prm, p, b - p * N, bsm)
+                                            : bonus_role<0>(prm, p, b - p * N, bsm);
+        if (tid == 0 && bst) atomicOr(&prm.status[p], bst);
+        pdl_trigger();
+        return;
+    }
+    const int per_prompt = chunks_per_prompt;
+    const int p = blockIdx.x / per_prompt, c = blockIdx.x - p * per_prompt;
     const int q0 = c * kPairsPerCta, nq = min(kPairsPerCta, NK - q0);
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    {
 
     // ---- inputs (not produced by the predecessor): before the wait
     int lr_model = 0, lr_q = 0, lr_kn = 0;
@@ -874,10 +1104,11 @@ __global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Param
     }
     if (st) atomicOr(&prm.st_ws[p], st);
     if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2053);      // chunk 0 S2 done
+    }
     // ---- completion: the last CTA of the prompt finishes it
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&prm.prompt_ctr[p], 1u) == (unsigned)(chunks_per_prompt - 1);
+    if (tid == 0) s_last = atomicAdd(&prm.prompt_ctr[p], 1u) == (unsigned)(per_prompt - 1);
     __syncthreads();
     if (!s_last) {
         pdl_trigger();
@@ -922,7 +1153,10 @@ __global__ void __launch_bounds__(kThreads) k_tail(const __grid_constant__ Param
     __syncthreads();
     normalise_resample(prm, p, resample_mode != 0, sh);
     __syncthreads();
-    if (tid == 0) prm.status[p] = sh.st;
+    if (tid == 0) {
+        if (bonus_ctas) atomicOr(&prm.status[p], sh.st);
+        else prm.status[p] = sh.st;
+    }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);
     pdl_trigger();
 }

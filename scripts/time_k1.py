@@ -25,12 +25,16 @@ if "cfg4" in which:
     ws = smc.Workspace(dev); out = smc.Outputs()
     ms = t(lambda i: smc.smcsd_step(lp, lq, tok, V=128256, step=i, out=out, fields=(), workspace=ws), 10)
     res["cfg4"] = (ms, 8405475328 / ms / 1e6)
+    ms = t(lambda i: smc.smcsd_step(lp, lq, tok, V=128256, step=i, out=out, fields=(), workspace=ws, bonus=True), 10)
+    res["cfg4+bonus"] = (ms, (8405475328 + 2048 * 128256 * 2) / ms / 1e6)
     del lp, lq, tok; torch.cuda.empty_cache()
 if "cfg2" in which:
     ring = [synth.lm_logits(1, 16, 8, 128256, device=dev, seed=10 + r) for r in range(6)]
     ws = smc.Workspace(dev); out = smc.Outputs()
     ms = t(lambda i: smc.smcsd_step(*ring[i % 6], V=128256, step=i, out=out, fields=(), workspace=ws), 60)
     res["cfg2"] = (ms, 65667776 / ms / 1e6)
+    ms = t(lambda i: smc.smcsd_step(*ring[i % 6], V=128256, step=i, out=out, fields=(), workspace=ws, bonus=True), 60)
+    res["cfg2+bonus"] = (ms, (65667776 + 16 * 128256 * 2) / ms / 1e6)
     del ring; torch.cuda.empty_cache()
 if "cfg5" in which:
     lp, lq, tok = synth.lm_logits(1, 64, 8, 128256, device=dev, seed=5)

@@ -472,3 +472,72 @@ def test_powersmc_status_and_masked_rows(smc, orc):
     assert ref["status"].tolist() == [8, 9, 0]
     assert np.array_equal(np.isneginf(np_(gpu.logw)), np.isneginf(ref["logw"]))
     assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW
+
+
+# ------------------------------------------------------------- bonus token (NEXT #2)
+SEG_MARGIN_TOL = 1e-5      # |C_i/W - U| below this: segment choice is a rounding-order near-tie
+KEY_MARGIN_TOL = 1e-4      # top-2 Gumbel keys (natural units) closer than this: near-tie
+
+
+def _bonus_check(gpu_b, ref):
+    ok = (ref["seg_margin"] > SEG_MARGIN_TOL) & (ref["key_margin"] > KEY_MARGIN_TOL)
+    assert ok.mean() > 0.9
+    assert np.array_equal(gpu_b[ok], ref["bonus"][ok])
+    return ok
+
+
+@pytest.mark.parametrize("P,N,K,V,dtype", [(1, 16, 8, 128256, torch.bfloat16),   # cfg2
+                                           (2, 33, 3, 20001, torch.float32),     # ragged
+                                           (3, 5, 2, 8192, torch.bfloat16),      # one segment
+                                           (2, 4, 1, 7, torch.float32)])         # V < vector
+def test_bonus_token_parity(smc, orc, P, N, K, V, dtype):
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=dtype, seed=6000 + V + N)
+    dev = torch.device("cuda")
+    kw = dict(V=V, eta=math.inf, seed=77, step=5, prompt_base=3, inv_temp_p=1.0 / 0.7)
+    out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), bonus=True, **kw)
+    plain = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), **kw)
+    torch.cuda.synchronize()
+    ref = orc.bonus(to_host(lp), K=K, V=V, tau=1.0 / 0.7, seed=77, step=5, prompt_base=3)
+    _bonus_check(np_(out.bonus), ref)
+    assert np.all(np_(out.status) == 0) and np.all(ref["status"] == 0)
+    # the bonus row never enters the weights or the resampling
+    assert torch.equal(out.logw_pre, plain.logw_pre) and torch.equal(out.ancestors, plain.ancestors)
+
+
+def test_bonus_token_n_drafted_and_flags(smc, orc):
+    P, N, K, V = 2, 6, 4, 9000
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.float32, seed=61)
+    nd = torch.tensor([[0, 1, 2, 3, 4, 4], [4, 4, 4, 4, 4, 4]], dtype=torch.int32)
+    lp[1, 2, K, 4000] = float("nan")                       # bonus row NaN -> -1, NONFINITE
+    lp[1, 4, K, :] = -float("inf")                         # all -inf bonus row -> -1, NONFINITE
+    dev = torch.device("cuda")
+    out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, n_drafted=nd.to(dev),
+                         eta=math.inf, step=2, bonus=True)
+    torch.cuda.synchronize()
+    ref = orc.bonus(to_host(lp), K=K, V=V, n_drafted=nd.numpy(), step=2)
+    _bonus_check(np_(out.bonus), ref)
+    assert np_(out.bonus)[1, 2] == -1 and np_(out.bonus)[1, 4] == -1
+    assert int(np_(out.status)[1]) & 8
+
+
+def test_bonus_token_frequencies(smc):
+    # 8 hot columns over 3 segments (ragged tail): GPU draws follow the softmax (chi-square)
+    from scipy import stats
+    V, N = 3 * 8192 + 100, 1024
+    hot = torch.tensor([5, 4000, 8191, 8192, 12000, 16383, 20000, 3 * 8192 + 99])
+    z = torch.tensor([1.0, 0.3, -0.5, 0.8, 0.0, 1.2, -1.0, 0.6])
+    lp = torch.full((1, N, 2, V + 4), -float("inf"))
+    lp[:, :, :, hot] = z
+    lq = lp[:, :, :1].contiguous()
+    tok = torch.full((1, N, 1), 5, dtype=torch.int32)
+    dev = torch.device("cuda")
+    lpd, lqd, tokd = lp.to(dev), lq.to(dev), tok.to(dev)
+    draws = []
+    for s in range(16):
+        draws.append(np_(smc.smcsd_step(lpd, lqd, tokd, V=V, step=s, bonus=True).bonus).ravel())
+    b = np.concatenate(draws)
+    cnt = np.array([(b == h).sum() for h in hot.tolist()])
+    assert cnt.sum() == b.size
+    p = np.exp(z.double().numpy()); p /= p.sum()
+    chi2 = ((cnt - p * b.size) ** 2 / (p * b.size)).sum()
+    assert stats.chi2.sf(chi2, len(hot) - 1) > 1e-3
