@@ -283,6 +283,8 @@ def run_ours(args, rank, world, local):
         secondary["cfg5"] = measure_cfg5(dev, rank, world, hbm_peak)
         if world == 1:
             secondary["cfg3"] = measure_cfg3(dev, hbm_peak)
+            secondary["cfg2_verify"] = measure_cfg2_verify(dev, hbm_peak)
+            secondary["powersmc"] = measure_power(dev, hbm_peak)
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
@@ -358,6 +360,12 @@ def measure_cfg4(dev, rank, world, hbm_peak, steps=20, warmup=3):
     ms = _time_steps(fn, steps, warmup, world, dev)
     byts = P * (2 * N * K * V * 2 + N * K * 4 + 3 * N * 4)
     gbs = byts / (ms / 1e3) / 1e9
+    # NEXT #2: the same step plus the bonus token (target row K streamed in K1, bonus CTAs)
+    fnb = lambda i: smc.smcsd_step(lp, lq, tok, V=V, logw_prev=logw, eta=math.inf, step=i,
+                                   prompt_base=b, out=out, fields=(), workspace=ws, bonus=True)
+    msb = _time_steps(fnb, steps, warmup, world, dev)
+    bytb = byts + P * N * V * 2
+    gbb = bytb / (msb / 1e3) / 1e9
     del lp, lq, tok
     torch.cuda.empty_cache()
     return {"workload": f"cfg4: {P_all} prompts x N={N} x K={K}, V={V} bf16, {P} prompts/rank, "
@@ -365,7 +373,59 @@ def measure_cfg4(dev, rank, world, hbm_peak, steps=20, warmup=3):
             "steps_per_s": round(P_all / (ms / 1e3) if world > 1 else P / (ms / 1e3), 1),
             "unit": "prompt-steps/s", "ms_per_step": round(ms, 4), "bytes_per_rank": int(byts),
             "achieved_gbs_per_rank": round(gbs, 1), "frac_of_measured": round(gbs / hbm_peak, 4),
-            "frac_of_8tbs": round(gbs / 8000.0, 4)}
+            "frac_of_8tbs": round(gbs / 8000.0, 4),
+            "with_bonus": {"ms_per_step": round(msb, 4), "bytes_per_rank": int(bytb),
+                           "achieved_gbs_per_rank": round(gbb, 1),
+                           "frac_of_measured": round(gbb / hbm_peak, 4)}}
+
+
+def measure_cfg2_verify(dev, hbm_peak, steps=120, warmup=6):
+    """cfg2 verification only (smcsd_step S1-S7, no KV), with and without the bonus token
+    (NEXT #2): latency per step over a ring of 6 logit sets (394 MB > L2)."""
+    import torch
+    import paper_2604_15672_b200 as smc
+    import synth
+    P, N, K, V = 1, 16, 8, 128256
+    ring = [synth.lm_logits(P, N, K, V, device=dev, seed=synth.GEN_SEED_BASE + 200 + r) for r in range(6)]
+    ws = smc.Workspace(dev)
+    out = smc.Outputs()
+    res = {"workload": "cfg2 verify: smcsd_step S1-S7, P=1 N=16 K=8 V=128256 bf16, ring of 6"}
+    for bonus in (False, True):
+        fn = lambda i: smc.smcsd_step(*ring[i % 6], V=V, eta=math.inf, step=i, out=out, fields=(),
+                                      workspace=ws, bonus=bonus)
+        ms = _time_steps(fn, steps, warmup, 1, dev)
+        byts = 2 * N * K * V * 2 + (N * V * 2 if bonus else 0)
+        res["with_bonus" if bonus else "plain"] = {
+            "us_per_step": round(ms * 1e3, 2), "bytes": byts,
+            "frac_of_measured": round(byts / (ms / 1e3) / 1e9 / hbm_peak, 4)}
+    del ring
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_power(dev, hbm_peak, steps=20, warmup=3):
+    """NEXT #4 PowerSMC (App. F): K = 1, one model, log w = ln sum_v p_v^alpha per particle,
+    then S4; 64 prompts x N = 32, V = 128256 bf16 (525 MB).  alpha = 4 (integer: the power
+    sum reuses the ex2 of the softmax sum) and alpha = 2.5 (a second ex2 per element)."""
+    import torch
+    import paper_2604_15672_b200 as smc
+    import synth
+    P, N, V = 64, 32, 128256
+    lg, _, _ = synth.lm_logits(P, N, 1, V, dtype=torch.bfloat16, device=dev, bonus=False,
+                               seed=synth.GEN_SEED_BASE + 44)
+    ws = smc.Workspace(dev)
+    out = smc.Outputs()
+    res = {"workload": f"PowerSMC weights: {P} prompts x N={N}, V={V} bf16 (K=1, no bonus)"}
+    byts = P * N * V * 2
+    for a in (4.0, 2.5):
+        fn = lambda i: smc.smcsd_powersmc_weights(lg, V=V, alpha=a, out=out, workspace=ws)
+        ms = _time_steps(fn, steps, warmup, 1, dev)
+        gbs = byts / (ms / 1e3) / 1e9
+        res[f"alpha_{a}"] = {"ms_per_step": round(ms, 4), "achieved_gbs": round(gbs, 1),
+                             "frac_of_measured": round(gbs / hbm_peak, 4)}
+    del lg
+    torch.cuda.empty_cache()
+    return res
 
 
 def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
