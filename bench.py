@@ -479,13 +479,32 @@ def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
     byts = 2 * N * K * w * 2
     part_ms = phases[0] / steps
     gbs = byts / (part_ms / 1e3) / 1e9
-    return {"workload": f"cfg5: P=1, N={N}, K={K}, V={V} bf16 vocab-sharded {world}-way "
-                        f"({w} columns on this rank); partial -> all_gather -> combine -> resample",
-            "steps_per_s": round(1e3 / ms, 1), "ms_per_step": round(ms, 4),
-            "note": "per-step phase times are measured with a host sync per step (not overlapped)",
-            "partial_ms": round(part_ms, 4), "exchange_ms": round(phases[1] / steps, 4),
-            "combine_resample_ms": round(phases[2] / steps, 4), "bytes_per_rank": int(byts),
-            "partial_achieved_gbs": round(gbs, 1), "partial_frac_of_measured": round(gbs / hbm_peak, 4)}
+    res = {"workload": f"cfg5: P=1, N={N}, K={K}, V={V} bf16 vocab-sharded {world}-way "
+                       f"({w} columns on this rank); partial -> all_gather -> combine -> resample",
+           "steps_per_s": round(1e3 / ms, 1), "ms_per_step": round(ms, 4),
+           "note": "per-step phase times are measured with a host sync per step (not overlapped)",
+           "partial_ms": round(part_ms, 4), "exchange_ms": round(phases[1] / steps, 4),
+           "combine_resample_ms": round(phases[2] / steps, 4), "bytes_per_rank": int(byts),
+           "partial_achieved_gbs": round(gbs, 1), "partial_frac_of_measured": round(gbs / hbm_peak, 4)}
+    # S10 fused into K1 (smcsd_tp_step): partials pushed to every rank's exchange buffer over
+    # peer memory, epoch flags, tail merges in rank order -- 2 launches, no collective call
+    try:
+        from paper_2604_15672_b200.dist import TPExchange
+        ex = TPExchange(P, N, K, V) if world > 1 else TPExchange.local_group(P, N, K, V, 1, device=dev)[0]
+        of = smc.Outputs(logw=logw)
+        wsf = smc.Workspace(dev)
+        fnf = lambda i: ex.step(sp, sq, tok, logw_prev=logw, eta=math.inf, step=i, out=of,
+                                fields=(), workspace=wsf)
+        msf = _time_steps(fnf, steps, warmup, world, dev)
+        torch.cuda.synchronize()
+        res["fused_exchange"] = {"ms_per_step": round(msf, 4), "steps_per_s": round(1e3 / msf, 1),
+                                 "status_ok": bool((of.status == 0).all().item()),
+                                 "path": "smcsd_tp_step: K1 pushes partials to peers (P2P "
+                                         "stores + release flags), tail waits (acquire) + S2-S7"}
+        ex.close()
+    except Exception as exc:  # pragma: no cover - reported, never fatal for the bench
+        res["fused_exchange"] = {"error": repr(exc)[:300]}
+    return res
 
 
 def measure_cfg3(dev, hbm_peak, steps=5, warmup=2):

@@ -70,6 +70,7 @@ typedef enum { SMCSD_SYSTEMATIC = 0, SMCSD_MULTINOMIAL = 1 } smcsd_scheme;
 #define SMCSD_ST_BAD_TOKEN   4u  /* drafted token outside [0,V), or n_drafted outside [0,K]         */
 #define SMCSD_ST_NONFINITE   8u  /* NaN/+inf logit or log-weight, or a row whose max is -inf        */
 #define SMCSD_ST_BAD_PAGE   16u  /* paged reindex: page id or ancestor out of range (entry skipped) */
+#define SMCSD_ST_EXCHANGE   32u  /* smcsd_tp_step: a peer's partials did not arrive within 20 s     */
 
 /* Segment length (elements) of the fixed in-row split used by every logit row (G17). */
 #define SMCSD_SEGMENT 8192
@@ -233,6 +234,52 @@ SMCSD_API smcsd_rc smcsd_powersmc_weights(const void *logits, int64_t ld, int ro
                                           float *logw_out, float *log_inc, double *lse_out,
                                           double *ess_out, float *wnorm_out, uint32_t *status,
                                           void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---- S10 fused into K1: tensor-parallel step over peer memory (NVLink P2P) -------------------
+ * The north star's vocab-sharded config: every rank holds columns [v_begin, v_begin + v_len)
+ * of every logit row.  Instead of partial -> NCCL all_gather -> combine, K1 itself pushes each
+ * (row, segment) partial {m, s, x_d} (16 B) straight into every rank's exchange buffer with
+ * plain stores through peer mappings, then its last CTA publishes `epoch` in every rank's flag
+ * word (st.release.sys).  The tail waits on its own flags (ld.acquire.sys, bounded: 20 s ->
+ * SMCSD_ST_EXCHANGE) and merges the G * xnseg parts of each row in rank order -- the global
+ * column order -- so every rank computes identical weights, ancestors and resets (same Philox
+ * counters), with no collective call.  Two launches per step, like smcsd_step.
+ *
+ * Exchange buffer (one per rank, caller-allocated, 16-byte aligned, smcsd_tp_exchange_bytes):
+ * 256 B of flags then two parity halves (epoch & 1) of [2*P*N*K][G*xnseg] float4.  Initialise
+ * once with smcsd_tp_exchange_init, share it with smcsd_ipc_export / smcsd_ipc_open (plumbing;
+ * the handles travel over torch.distributed).  xnseg >= ceil(v_len / SMCSD_SEGMENT) on every
+ * rank (the same value everywhere); slots a rank never writes stay neutral.
+ * epoch: >= 1, +1 per call, identical on every rank.  A rank may run at most one step ahead
+ * of another (the parity halves make that safe). */
+SMCSD_API size_t smcsd_tp_exchange_bytes(int P, int N, int K, int G, int xnseg);
+SMCSD_API smcsd_rc smcsd_tp_exchange_init(void *xbuf, size_t xbuf_bytes, void *stream);
+/* CUDA IPC plumbing.  smcsd_ipc_export writes smcsd_ipc_handle_bytes() opaque host bytes naming
+ * the device address dev_ptr: the IPC handle of its whole allocation plus dev_ptr's offset in
+ * it (so tensors from a caching allocator work).  smcsd_ipc_open maps a peer's bytes (peer
+ * access enabled lazily) and returns the same address in this process; smcsd_ipc_close(ptr,
+ * the same bytes) unmaps it. */
+SMCSD_API size_t smcsd_ipc_handle_bytes(void);
+SMCSD_API smcsd_rc smcsd_ipc_export(const void *dev_ptr, void *handle_out);
+SMCSD_API smcsd_rc smcsd_ipc_open(const void *handle, void **dev_ptr_out);
+SMCSD_API smcsd_rc smcsd_ipc_close(void *dev_ptr, const void *handle);
+/* S1 + S10 + S2-S7 on this rank's shard.  Arguments as smcsd_step, plus
+ *  v_begin/v_len: this rank's columns (logits rows hold only them; tokens are global ids);
+ *  rank, G, xnseg, epoch: see above;  xpeer: DEVICE array [G] of every rank's exchange buffer
+ *  as mapped in this process (xpeer[rank] == xlocal);  xlocal: this rank's buffer.
+ *  Workspace: smcsd_workspace_bytes(P, N, K, v_len).  N <= 1024, G <= 32. */
+SMCSD_API smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
+                       const void *logits_q, int64_t ld_q, int rows_per_particle_q, int dtype,
+                       const int32_t *tokens, const int32_t *n_drafted, const float *logw_prev,
+                       int P, int N, int K, int64_t V, int64_t v_begin, int64_t v_len,
+                       float alpha, float inv_temp_p, float inv_temp_q, float eta, int scheme,
+                       uint64_t seed, uint64_t step, int64_t prompt_base, const uint32_t *uniforms,
+                       int rank, int G, int xnseg, uint32_t epoch, void *const *xpeer,
+                       void *xlocal, float *logw_out, float *logw_pre, float *logp_tok,
+                       float *logq_tok, double *lse_out, double *ess_out, float *wnorm_out,
+                       uint32_t *status, int32_t *ancestors, int32_t *offspring,
+                       int32_t *slot_src, uint8_t *resampled, int32_t *n_ties,
+                       void *workspace, size_t workspace_bytes, void *stream);
 
 /* Human-readable name of a return code (static storage). */
 SMCSD_API const char *smcsd_strerror(smcsd_rc rc);

@@ -22,13 +22,16 @@ __all__ = [
     "smcsd_workspace_bytes", "smcsd_workspace_init", "smcsd_weights", "smcsd_step",
     "smcsd_resample", "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
     "smcsd_version", "kv_geometry", "smcsd_select", "smcsd_kv_reindex_paged", "ST_BAD_PAGE",
-    "smcsd_powersmc_weights",
+    "smcsd_powersmc_weights", "smcsd_tp_exchange_bytes", "smcsd_tp_exchange_init",
+    "smcsd_ipc_handle_bytes", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close", "smcsd_tp_step",
+    "ST_EXCHANGE",
 ]
 
 SMCSD_F32, SMCSD_BF16 = 0, 1
 SMCSD_SYSTEMATIC, SMCSD_MULTINOMIAL = 0, 1
 SEGMENT = 8192
 ST_DEGENERATE, ST_NOT_ABSCONT, ST_BAD_TOKEN, ST_NONFINITE, ST_BAD_PAGE = 1, 2, 4, 8, 16
+ST_EXCHANGE = 32
 _RC = {0: "ok", 1: "invalid argument", 2: "CUDA launch or runtime error", 3: "not implemented"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -67,9 +70,24 @@ def _load():
     L.smcsd_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
     L.smcsd_powersmc_weights.argtypes = [vp, i64, i32, i32, vp, i32, i32, i64, f32, f32, vp, vp,
                                          vp, vp, vp, vp, vp, sz, vp]
+    u32 = ctypes.c_uint32
+    L.smcsd_tp_exchange_bytes.argtypes = [i32, i32, i32, i32, i32]
+    L.smcsd_tp_exchange_bytes.restype = sz
+    L.smcsd_tp_exchange_init.argtypes = [vp, sz, vp]
+    L.smcsd_ipc_handle_bytes.argtypes = []
+    L.smcsd_ipc_handle_bytes.restype = sz
+    L.smcsd_ipc_export.argtypes = [vp, vp]
+    L.smcsd_ipc_open.argtypes = [vp, ctypes.POINTER(ctypes.c_void_p)]
+    L.smcsd_ipc_close.argtypes = [vp, vp]
+    L.smcsd_tp_step.argtypes = [vp, i64, i32, vp, i64, i32, i32, vp, vp, vp, i32, i32, i32, i64,
+                                i64, i64, f32, f32, f32, f32, i32, u64, u64, i64, vp,
+                                i32, i32, i32, u32, vp, vp,
+                                vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     for name in ("smcsd_workspace_init", "smcsd_weights", "smcsd_resample", "smcsd_step",
                  "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
-                 "smcsd_select", "smcsd_kv_reindex_paged", "smcsd_powersmc_weights"):
+                 "smcsd_select", "smcsd_kv_reindex_paged", "smcsd_powersmc_weights",
+                 "smcsd_tp_exchange_init", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close",
+                 "smcsd_tp_step"):
         getattr(L, name).restype = i32
     L.smcsd_version.restype = ctypes.c_char_p
     L.smcsd_strerror.restype = ctypes.c_char_p
@@ -337,6 +355,68 @@ def smcsd_powersmc_weights(logits, *, V=None, logw_prev=None, alpha=1.0, inv_tem
                                      _p(out.ess), _p(out.wnorm), _p(out.status), _p(ws), ws.numel(),
                                      _stream(stream))
     _check("smcsd_powersmc_weights", rc)
+    return out
+
+
+def smcsd_tp_exchange_bytes(P: int, N: int, K: int, G: int, xnseg: int) -> int:
+    return int(_lib.smcsd_tp_exchange_bytes(P, N, K, G, xnseg))
+
+
+def smcsd_tp_exchange_init(xbuf: torch.Tensor, stream=None):
+    _check("smcsd_tp_exchange_init", _lib.smcsd_tp_exchange_init(_p(xbuf), xbuf.numel(), _stream(stream)))
+
+
+def smcsd_ipc_handle_bytes() -> int:
+    return int(_lib.smcsd_ipc_handle_bytes())
+
+
+def smcsd_ipc_export(t: torch.Tensor) -> bytes:
+    """Opaque bytes naming t's device address for another process (IPC handle + offset)."""
+    buf = ctypes.create_string_buffer(smcsd_ipc_handle_bytes())
+    _check("smcsd_ipc_export", _lib.smcsd_ipc_export(_p(t), buf))
+    return buf.raw
+
+
+def smcsd_ipc_open(handle: bytes) -> int:
+    ptr = ctypes.c_void_p()
+    _check("smcsd_ipc_open", _lib.smcsd_ipc_open(handle, ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def smcsd_ipc_close(ptr: int, handle: bytes):
+    _check("smcsd_ipc_close", _lib.smcsd_ipc_close(ptr, handle))
+
+
+def smcsd_tp_step(logits_p, logits_q, tokens, *, V, v_begin, rank, G, xnseg, epoch, xpeer, xlocal,
+                  v_len=None, n_drafted=None, logw_prev=None, alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0,
+                  eta=math.inf, scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0,
+                  uniforms=None, out: Outputs | None = None, fields=_ALL_S, workspace=None,
+                  stream=None) -> Outputs:
+    """S1 + fused peer-memory exchange (S10) + S2-S7 on this rank's vocabulary shard.
+    logits_* rows hold columns [v_begin, v_begin + v_len); xpeer: int64 device tensor [G] of
+    every rank's exchange buffer address in this process; xlocal: this rank's buffer."""
+    ld_p, rpp_p = _logits_geom(logits_p, "logits_p")
+    ld_q, rpp_q = _logits_geom(logits_q, "logits_q")
+    if logits_p.dtype != logits_q.dtype:
+        raise TypeError("logits_p and logits_q must share a dtype")
+    if xpeer.dtype != torch.int64 or xpeer.numel() != G or not xpeer.is_cuda:
+        raise ValueError("xpeer must be an int64 CUDA tensor of G buffer addresses")
+    P, N, K = tokens.shape
+    v_len = min(ld_p, V - v_begin) if v_len is None else v_len
+    dev = logits_p.device
+    out = _alloc(out or Outputs(), dev, P, N, K,
+                 ("logw", "status", "ancestors", "resampled") + tuple(fields))
+    ws = _ws(workspace, dev, P, N, K, v_len, stream)
+    rc = _lib.smcsd_tp_step(_p(logits_p), ld_p, rpp_p, _p(logits_q), ld_q, rpp_q,
+                            _dtype_code(logits_p), _p(tokens), _p(n_drafted), _p(logw_prev),
+                            P, N, K, V, v_begin, v_len, alpha, inv_temp_p, inv_temp_q, eta, scheme,
+                            seed & (2 ** 64 - 1), step & (2 ** 64 - 1), prompt_base, _p(uniforms),
+                            rank, G, xnseg, epoch & 0xFFFFFFFF, _p(xpeer), _p(xlocal),
+                            _p(out.logw), _p(out.logw_pre), _p(out.logp_tok), _p(out.logq_tok),
+                            _p(out.lse), _p(out.ess), _p(out.wnorm), _p(out.status),
+                            _p(out.ancestors), _p(out.offspring), _p(out.slot_src),
+                            _p(out.resampled), _p(out.n_ties), _p(ws), ws.numel(), _stream(stream))
+    _check("smcsd_tp_step", rc)
     return out
 
 

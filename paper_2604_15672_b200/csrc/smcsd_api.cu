@@ -1,6 +1,7 @@
 // smcsd_api.cu -- extern "C" entry points of libsmcsd.so (declared in include/smcsd.h):
 // synchronous argument validation, workspace carve-up, launch configuration.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -54,6 +55,7 @@ void bind_workspace(Params &prm, void *ws, const WsLayout &L) {
     prm.work_ctr = reinterpret_cast<unsigned *>(b + L.ctr);
     prm.prompt_ctr = reinterpret_cast<unsigned *>(b + L.pctr);
     prm.st_ws = reinterpret_cast<uint32_t *>(b + L.pst);
+    prm.xctr = reinterpret_cast<unsigned *>(b + L.ctr + 64);
 }
 
 bool valid_temp(float t) { return std::isfinite(t) && t > 0.0f; }
@@ -464,6 +466,124 @@ smcsd_rc smcsd_powersmc_weights(const void *logits, int64_t ld, int rows_per_par
     rc = launch_rowstats(prm, dtype, (int64_t)P * N * prm.nseg, st, true);
     if (rc != SMCSD_OK) return rc;
     return launch_pdl(k_power_tail, (unsigned)P, 0, st, prm);
+}
+
+size_t smcsd_tp_exchange_bytes(int P, int N, int K, int G, int xnseg) {
+    if (P < 1 || N < 1 || K < 1 || G < 1 || G > kXFlagBytes / 4 || xnseg < 1) return 0;
+    return kXFlagBytes + 2 * x_half_elems(2 * P * N * K, G, xnseg) * sizeof(float4);
+}
+
+smcsd_rc smcsd_tp_exchange_init(void *xbuf, size_t xbuf_bytes, void *stream) {
+    if (!xbuf || !aligned16(xbuf) || xbuf_bytes < (size_t)kXFlagBytes) return SMCSD_EINVAL;
+    const size_t n = (xbuf_bytes - kXFlagBytes) / sizeof(float4);
+    k_xinit<<<(unsigned)std::max<size_t>(1, std::min<size_t>(1184, cdiv((int64_t)n, 256))), 256, 0,
+              as_stream(stream)>>>(static_cast<char *>(xbuf), n);
+    return cudaGetLastError() == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
+}
+
+// An IPC handle names a whole cudaMalloc allocation and opens at its base; a tensor from a
+// caching allocator may sit at an offset inside it.  The exported bytes are the handle plus
+// that offset (found with the driver's cuMemGetAddressRange, fetched through the runtime).
+struct IpcBlob {
+    cudaIpcMemHandle_t h;
+    uint64_t offset;
+};
+
+size_t smcsd_ipc_handle_bytes(void) { return sizeof(IpcBlob); }
+
+smcsd_rc smcsd_ipc_export(const void *dev_ptr, void *handle_out) {
+    if (!dev_ptr || !handle_out) return SMCSD_EINVAL;
+    using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return SMCSD_ECUDA;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (reinterpret_cast<GetRange>(fn)(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0)
+        return SMCSD_ECUDA;
+    IpcBlob b;
+    std::memset(&b, 0, sizeof b);
+    if (cudaIpcGetMemHandle(&b.h, reinterpret_cast<void *>(base)) != cudaSuccess) return SMCSD_ECUDA;
+    b.offset = reinterpret_cast<unsigned long long>(dev_ptr) - base;
+    std::memcpy(handle_out, &b, sizeof b);
+    return SMCSD_OK;
+}
+
+smcsd_rc smcsd_ipc_open(const void *handle, void **dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return SMCSD_EINVAL;
+    IpcBlob b;
+    std::memcpy(&b, handle, sizeof b);
+    void *base = nullptr;
+    if (cudaIpcOpenMemHandle(&base, b.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+        return SMCSD_ECUDA;
+    *dev_ptr_out = static_cast<char *>(base) + b.offset;
+    return SMCSD_OK;
+}
+
+smcsd_rc smcsd_ipc_close(void *dev_ptr, const void *handle) {
+    if (!dev_ptr || !handle) return SMCSD_EINVAL;
+    IpcBlob b;
+    std::memcpy(&b, handle, sizeof b);
+    return cudaIpcCloseMemHandle(static_cast<char *>(dev_ptr) - b.offset) == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
+}
+
+smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
+                       const void *logits_q, int64_t ld_q, int rows_per_particle_q, int dtype,
+                       const int32_t *tokens, const int32_t *n_drafted, const float *logw_prev,
+                       int P, int N, int K, int64_t V, int64_t v_begin, int64_t v_len,
+                       float alpha, float inv_temp_p, float inv_temp_q, float eta, int scheme,
+                       uint64_t seed, uint64_t step, int64_t prompt_base, const uint32_t *uniforms,
+                       int rank, int G, int xnseg, uint32_t epoch, void *const *xpeer,
+                       void *xlocal, float *logw_out, float *logw_pre, float *logp_tok,
+                       float *logq_tok, double *lse_out, double *ess_out, float *wnorm_out,
+                       uint32_t *status, int32_t *ancestors, int32_t *offspring,
+                       int32_t *slot_src, uint8_t *resampled, int32_t *n_ties,
+                       void *workspace, size_t workspace_bytes, void *stream) {
+    smcsd_rc rc = check_logits(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
+                               rows_per_particle_q, dtype, tokens, P, N, K, v_len);
+    if (rc != SMCSD_OK) return rc;
+    if (!logw_out || !status || !ancestors || !resampled || !workspace || !xpeer || !xlocal)
+        return SMCSD_EINVAL;
+    if (N > kTailMaxN || std::isnan(eta) || v_begin < 0 || v_begin + v_len > V) return SMCSD_EINVAL;
+    if (G < 1 || G > 32 || rank < 0 || rank >= G || epoch == 0 || !aligned16(xlocal)) return SMCSD_EINVAL;
+    if (xnseg < cdiv(v_len, kSeg) || (int64_t)G * xnseg > 4096) return SMCSD_EINVAL;
+    if (!(std::isfinite(alpha) && alpha > 0.0f) || !valid_temp(inv_temp_p) || !valid_temp(inv_temp_q))
+        return SMCSD_EINVAL;
+    if (scheme != SMCSD_SYSTEMATIC && scheme != SMCSD_MULTINOMIAL) return SMCSD_EINVAL;
+    const WsLayout L = ws_layout(P, N, K, v_len);
+    if (workspace_bytes < L.total || !aligned16(workspace)) return SMCSD_EINVAL;
+    Params prm = logits_params(logits_p, ld_p, rows_per_particle_p, logits_q, ld_q,
+                               rows_per_particle_q, tokens, n_drafted, P, N, K, V, v_begin, v_len,
+                               inv_temp_p, inv_temp_q);
+    prm.alpha = (double)alpha;
+    prm.dtype = dtype;
+    prm.logw_prev = logw_prev;
+    prm.eta = (double)eta; prm.seed = seed; prm.step = step; prm.prompt_base = prompt_base;
+    prm.uniforms = uniforms; prm.scheme = scheme;
+    prm.logw_out = logw_out; prm.logw_pre = logw_pre; prm.logp_tok = logp_tok;
+    prm.logq_tok = logq_tok; prm.lse = lse_out; prm.ess = ess_out; prm.wnorm = wnorm_out;
+    prm.status = status; prm.ancestors = ancestors; prm.offspring = offspring;
+    prm.slot_src = slot_src; prm.resampled = resampled; prm.n_ties = n_ties;
+    bind_workspace(prm, workspace, L);
+    prm.xpeer = reinterpret_cast<char *const *>(xpeer);
+    prm.xrank = rank; prm.xG = G; prm.xnseg = xnseg; prm.xepoch = epoch;
+    cudaStream_t st = as_stream(stream);
+    rc = launch_rowstats(prm, dtype, prm.main_items, st);         // S1 + push (S10)
+    if (rc != SMCSD_OK) return rc;
+    // S2-S7 over the G * xnseg parts of every row, after every rank's flag reaches epoch
+    Params t = prm;
+    t.xpeer = nullptr;
+    t.xlocal = static_cast<char *>(xlocal);
+    t.x_from_logits = 0;
+    const int rows = 2 * P * N * K;
+    t.parts = reinterpret_cast<const float4 *>(static_cast<char *>(xlocal) + kXFlagBytes) +
+              (epoch & 1u) * x_half_elems(rows, G, xnseg);
+    t.part_row_stride = (int64_t)G * xnseg;
+    t.part_seg_stride = 1;
+    t.nparts = G * xnseg;
+    return launch_tail(t, 1, st);
 }
 
 const char *smcsd_strerror(smcsd_rc rc) {

@@ -25,6 +25,8 @@ namespace smcsd {
 
 constexpr uint32_t ST_DEGENERATE = 1u, ST_NOT_ABSCONT = 2u, ST_BAD_TOKEN = 4u, ST_NONFINITE = 8u;
 constexpr uint32_t ST_BAD_PAGE = 16u;
+constexpr uint32_t ST_EXCHANGE = 32u;                         // S10 peer flag wait timed out
+constexpr uint64_t kXTimeoutNs = 20000000000ull;              // 20 s
 #ifndef SMCSD_PHASE
 #define SMCSD_PHASE(i) do { } while (0)
 #endif
@@ -80,7 +82,38 @@ struct Params {
     unsigned *work_ctr;                         // K1 dynamic work counter (re-armed by K2)
     unsigned *prompt_ctr;                       // [P] K2 chunk completion counters
     uint32_t *st_ws;                            // [P] K2 status accumulation
+    // ---- S10 fused peer-memory exchange (TP): K1 pushes each segment partial to every rank
+    char *const *xpeer;                         // [G] device array: every rank's exchange buffer
+    char *xlocal;                               // this rank's exchange buffer (tail reads it)
+    int xrank, xG, xnseg;                       // rank, ranks, segment slots per rank
+    uint32_t xepoch;                            // this step's epoch (>= 1)
+    unsigned *xctr;                             // K1 CTA completion counter (workspace)
 };
+
+// Exchange buffer layout (one per rank, peer-mapped): uint32 flags[64] (flags[g] = last epoch
+// rank g finished pushing here), then two parity halves of [rows][G * xnseg] float4 partials
+// {m, s, x, 0}; row r's slot g * xnseg + s holds segment s of rank g's shard, so the rank-order
+// merge of a row's G * xnseg parts is the global column order.
+constexpr int kXFlagBytes = 256;
+__host__ __device__ inline size_t x_half_elems(int rows, int G, int xnseg) {
+    return (size_t)rows * G * xnseg;
+}
+__device__ __forceinline__ float4 *x_parts(char *base, int rows, int G, int xnseg, uint32_t epoch) {
+    return reinterpret_cast<float4 *>(base + kXFlagBytes) + (epoch & 1u) * x_half_elems(rows, G, xnseg);
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ------------------------------------------------------------------------------------------
 // Programmatic dependent launch (PDL): the tail / gather kernels are launched with
@@ -429,7 +462,28 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                     }
                     out = make_float4(M, t, -INFINITY, t2);
                 }
-                if (lane == 0) {
+                if (prm.xpeer) {
+                    // S10 fused exchange: x = t_d when the drafted token is in this segment
+                    // (taken from the staged segment), then one 16-byte store per rank
+                    const unsigned row = fastdiv((unsigned)m.item, prm.mg_nseg, prm.sh_nseg);
+                    const int sg = (int)((unsigned)m.item - row * (unsigned)prm.nseg);
+                    if (m.valid) {
+                        const int64_t d = prm.tokens[(int64_t)row % ((int64_t)prm.N * prm.K) +
+                                                     (int64_t)(row / (2u * prm.N * prm.K)) * prm.N * prm.K];
+                        const int64_t loc = d - prm.v_begin - (int64_t)sg * kSeg;
+                        if (loc >= 0 && loc < m.nv) {
+                            const char *sl = smem + (size_t)s * kStageBytes;
+                            const float z = DT == 1 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(sl)[loc] << 16)
+                                                    : reinterpret_cast<const float *>(sl)[loc];
+                            out.z = z * m.c;
+                        }
+                    }
+                    if (lane < prm.xG) {
+                        float4 *dst = x_parts(prm.xpeer[lane], 2 * prm.P * prm.N * prm.K, prm.xG, prm.xnseg, prm.xepoch);
+                        dst[(size_t)row * prm.xG * prm.xnseg + prm.xrank * prm.xnseg + sg] = out;
+                    }
+                    if (lane == 0) done[s] = 0;
+                } else if (lane == 0) {
                     prm.part_ws[m.item] = out;
                     done[s] = 0;
                 }
@@ -439,6 +493,18 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
         }
     }
     if (tid == 0) SMCSD_TRACE_AT(1024 + (blockIdx.x & 1023));    // K1 CTA done
+    if (prm.xpeer) {
+        // every pushed partial is visible system-wide before this CTA counts as done; the last
+        // CTA then publishes the epoch in every rank's flags (release, system scope)
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0 && atomicAdd(prm.xctr, 1u) == gridDim.x - 1) {
+            __threadfence_system();
+            for (int g = 0; g < prm.xG; ++g)
+                st_release_sys(reinterpret_cast<uint32_t *>(prm.xpeer[g]) + prm.xrank, prm.xepoch);
+            *prm.xctr = 0u;
+        }
+    }
     pdl_trigger();
 }
 
@@ -1024,6 +1090,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         SMCSD_TRACE_AT(2049);                                   // predecessor complete
         if (prm.work_ctr) *prm.work_ctr = 0u;                   // re-arm K1's counter
     }
+    if (prm.xlocal) {
+        // S10: wait until every rank has published this epoch's partials (acquire, system
+        // scope; bounded: a missing peer raises ST_EXCHANGE instead of hanging the GPU)
+        if (tid == 0) {
+            const uint32_t *fl = reinterpret_cast<const uint32_t *>(prm.xlocal);
+            const uint64_t t0 = globaltimer_ns();
+            for (int g = 0; g < prm.xG; ++g)
+                while ((int)(ld_acquire_sys(fl + g) - prm.xepoch) < 0) {
+                    if (globaltimer_ns() - t0 > kXTimeoutNs) {
+                        atomicOr(&prm.st_ws[p], ST_EXCHANGE);
+                        break;
+                    }
+                    __nanosleep(64);
+                }
+        }
+        __syncthreads();
+    }
 
     // ---- S2: 16 lanes per row, 16 rows per pass, 64 rows per CTA
     {
@@ -1337,6 +1420,14 @@ __global__ void __launch_bounds__(kThreads) k_power_tail(const __grid_constant__
     __syncthreads();
     if (tid == 0) prm.status[p] = sh.st;
     pdl_trigger();
+}
+
+// Exchange-buffer init: flags 0, every partial slot neutral {-inf, 0, -inf, 0}.
+__global__ void k_xinit(char *base, size_t n_parts) {
+    if (blockIdx.x == 0 && threadIdx.x < kXFlagBytes / 4) reinterpret_cast<uint32_t *>(base)[threadIdx.x] = 0u;
+    float4 *parts = reinterpret_cast<float4 *>(base + kXFlagBytes);
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_parts; i += (size_t)gridDim.x * blockDim.x)
+        parts[i] = make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
 }
 
 // Terminal selection: one index per prompt from the normalised weights by the

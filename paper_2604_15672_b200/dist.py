@@ -80,3 +80,84 @@ def tp_weights(logits_p_shard, logits_q_shard, tokens, *, V, v_begin, v_len, gro
     return smc.smcsd_weights_combine(gathered, tokens, V=V, n_drafted=kw.get("n_drafted"),
                                      logw_prev=kw.get("logw_prev"), alpha=kw.get("alpha", 1.0),
                                      out=kw.get("out"), workspace=kw.get("workspace_combine"))
+
+
+# ------------------------------------------------------------------------------------------
+# S10 fused into K1 over peer memory (smcsd_tp_step): the exchange buffers.
+# ------------------------------------------------------------------------------------------
+def share_handles(handle: bytes, group=None) -> list[bytes]:
+    """All ranks' IPC handles in rank order (plumbing over torch.distributed, any backend)."""
+    world = dist.get_world_size(group)
+    got: list = [None] * world
+    dist.all_gather_object(got, handle, group=group)
+    return [bytes(h) for h in got]
+
+
+def peer_table(handles: list[bytes], rank: int, local_ptr: int, open_fn) -> list[int]:
+    """Device addresses of every rank's exchange buffer as seen by this process: our own
+    buffer directly, every peer's through open_fn(handle) (cudaIpcOpenMemHandle)."""
+    return [local_ptr if g == rank else int(open_fn(h)) for g, h in enumerate(handles)]
+
+
+def xnseg_for(V: int, world: int, align: int = 8) -> int:
+    """Segment slots per rank: the widest shard's ceil(width / SMCSD_SEGMENT), same on all ranks."""
+    seg = 8192
+    return max((e - b + seg - 1) // seg for b, e in (vocab_shard(V, world, g, align) for g in range(world)))
+
+
+class TPExchange:
+    """One rank's exchange buffer plus the peer address table for smcsd_tp_step.
+
+    Multi-process: TPExchange(P, N, K, V, group=...) exports this rank's buffer, gathers every
+    rank's handle (torch.distributed) and opens the peers' buffers (CUDA IPC, NVLink P2P).
+    Single process: TPExchange.local_group(...) returns G exchanges whose tables point at each
+    other's buffers on one device (G simulated ranks; run each on its own stream)."""
+
+    def __init__(self, P, N, K, V, *, group=None, device=None, world=None, rank=None, _buf=None):
+        import paper_2604_15672_b200 as smc
+        self.smc = smc
+        self.device = torch.device("cuda" if device is None else device)
+        self.G = dist.get_world_size(group) if world is None else world
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.P, self.N, self.K, self.V = P, N, K, V
+        self.xnseg = xnseg_for(V, self.G)
+        self.v_begin, v_end = vocab_shard(V, self.G, self.rank)
+        self.v_len = v_end - self.v_begin
+        self.nbytes = smc.smcsd_tp_exchange_bytes(P, N, K, self.G, self.xnseg)
+        self.buf = _buf if _buf is not None else torch.empty(self.nbytes, dtype=torch.uint8, device=self.device)
+        smc.smcsd_tp_exchange_init(self.buf)
+        self.epoch = 0
+        self._opened: list[int] = []
+        self.xpeer = None
+        if world is None:                      # multi-process: share handles, open peers
+            torch.cuda.synchronize(self.device)
+            handles = share_handles(smc.smcsd_ipc_export(self.buf), group)
+            ptrs = peer_table(handles, self.rank, self.buf.data_ptr(), smc.smcsd_ipc_open)
+            self._opened = [(p, handles[g]) for g, p in enumerate(ptrs) if g != self.rank]
+            self.set_peers(ptrs)
+            dist.barrier(group)                # every buffer initialised before any push
+
+    def set_peers(self, ptrs: list[int]):
+        self.xpeer = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
+
+    @classmethod
+    def local_group(cls, P, N, K, V, G, device=None):
+        ex = [cls(P, N, K, V, device=device, world=G, rank=g) for g in range(G)]
+        ptrs = [e.buf.data_ptr() for e in ex]
+        for e in ex:
+            e.set_peers(ptrs)
+        torch.cuda.synchronize(ex[0].device)
+        return ex
+
+    def step(self, logits_p_shard, logits_q_shard, tokens, **kw):
+        """One smcsd_tp_step (epoch advanced here, identical on every rank)."""
+        self.epoch += 1
+        return self.smc.smcsd_tp_step(logits_p_shard, logits_q_shard, tokens, V=self.V,
+                                      v_begin=self.v_begin, v_len=self.v_len, rank=self.rank,
+                                      G=self.G, xnseg=self.xnseg, epoch=self.epoch,
+                                      xpeer=self.xpeer, xlocal=self.buf, **kw)
+
+    def close(self):
+        for p, h in self._opened:
+            self.smc.smcsd_ipc_close(p, h)
+        self._opened = []

@@ -29,7 +29,7 @@ def lib():
 
 def test_every_declared_symbol_is_exported(lib):
     names = _declared()
-    assert len(names) == 13, names
+    assert len(names) == 20, names
     for n in names:
         assert hasattr(lib, n), n
 

@@ -104,3 +104,32 @@ def test_tp_vocab_exchange_gloo():
     res = _run(_tp_job)
     assert res[0][0] and res[1][0]
     assert res[0][1] == res[1][1]            # every rank holds the same gathered bytes
+
+
+def _handles_fn(rank, world):
+    # S10 fused path plumbing: every rank's (fake) IPC handle reaches every rank in rank order,
+    # and the peer table keeps our own buffer and opens only the peers'
+    from paper_2604_15672_b200.dist import peer_table, share_handles
+    h = bytes([rank]) * 64
+    hs = share_handles(h)
+    opened = []
+    tab = peer_table(hs, rank, 1000 + rank, lambda b: opened.append(b[0]) or 5000 + b[0])
+    return hs, tab, opened
+
+
+def test_tp_exchange_handle_plumbing_gloo():
+    res = _run(_handles_fn)
+    for r in (0, 1):
+        hs, tab, opened = res[r]
+        assert hs == [bytes([0]) * 64, bytes([1]) * 64]
+        assert tab[r] == 1000 + r and tab[1 - r] == 5000 + (1 - r)
+        assert opened == [1 - r]
+
+
+def test_xnseg_covers_every_shard():
+    from paper_2604_15672_b200.dist import xnseg_for
+    assert xnseg_for(128256, 8) == 2 and xnseg_for(128256, 1) == 16 and xnseg_for(128256, 4) == 4
+    for V in (1000, 8193, 50001):
+        for G in (1, 2, 3, 8):
+            w = max(e - b for b, e in (vocab_shard(V, G, g) for g in range(G)))
+            assert xnseg_for(V, G) * 8192 >= w > (xnseg_for(V, G) - 1) * 8192

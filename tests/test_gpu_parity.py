@@ -541,3 +541,49 @@ def test_bonus_token_frequencies(smc):
     p = np.exp(z.double().numpy()); p /= p.sum()
     chi2 = ((cnt - p * b.size) ** 2 / (p * b.size)).sum()
     assert stats.chi2.sf(chi2, len(hot) - 1) > 1e-3
+
+
+# ------------------------------------------- TP with S10 fused into K1 over peer memory
+def _shard(x, b0, b1, align, dev):
+    w = (b1 - b0 + align - 1) // align * align
+    s = torch.full(x.shape[:-1] + (w,), float("nan"), dtype=x.dtype, device=dev)
+    s[..., :b1 - b0] = x[..., b0:b1]
+    return s
+
+
+@pytest.mark.parametrize("G,P,N,K,V,dtype", [(1, 1, 64, 8, 128256, torch.bfloat16),
+                                             (2, 2, 8, 3, 50001, torch.float32),
+                                             (4, 1, 64, 8, 128256, torch.bfloat16),
+                                             (8, 1, 64, 8, 128256, torch.bfloat16)])
+def test_tp_step_fused_exchange(smc, orc, G, P, N, K, V, dtype):
+    # G simulated ranks on one GPU, each on its own stream: K1 of every rank pushes its
+    # segment partials into every rank's exchange buffer and publishes the epoch; every
+    # rank's tail waits on its flags and merges in rank order.  Two steps (both parity halves).
+    from paper_2604_15672_b200.dist import TPExchange
+    dev = torch.device("cuda")
+    align = 8 if dtype == torch.bfloat16 else 4
+    ex = TPExchange.local_group(P, N, K, V, G, device=dev)
+    streams = [torch.cuda.Stream(dev) for _ in range(G)]
+    for it in range(2):
+        lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=dtype, seed=900 + 7 * G + it)
+        prev = synth.random_logw(P, N, seed=11 + it, sigma=0.5)
+        lpd, lqd, tokd, prevd = lp.to(dev), lq.to(dev), tok.to(dev), prev.to(dev)
+        shards = [(_shard(lpd, e.v_begin, e.v_begin + e.v_len, align, dev),
+                   _shard(lqd, e.v_begin, e.v_begin + e.v_len, align, dev)) for e in ex]
+        torch.cuda.synchronize()
+        outs = []
+        for g, e in enumerate(ex):
+            with torch.cuda.stream(streams[g]):
+                outs.append(e.step(*shards[g], tokd, logw_prev=prevd, eta=math.inf, seed=3,
+                                   step=it, workspace=smc.Workspace(dev), stream=streams[g]))
+        torch.cuda.synchronize()
+        for o in outs:
+            assert np.all(np_(o.status) == 0)
+            for f in ("logw_pre", "logw", "ancestors", "slot_src", "ess", "lse"):
+                assert torch.equal(getattr(o, f), getattr(outs[0], f)), f
+        ref = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, logw_prev=prev.numpy())
+        assert max_abs(np_(outs[0].logw_pre), ref["logw"]) <= TOL_LOGW
+        assert max_abs(np_(outs[0].logp_tok), ref["logp_tok"]) <= TOL_ELL
+        rr = orc.resample(np_(outs[0].logw_pre), eta=np.inf, seed=3, step=it)
+        assert np.array_equal(np_(outs[0].ancestors), rr["ancestors"])
+        assert np.array_equal(np_(outs[0].logw), rr["logw"])
