@@ -546,8 +546,35 @@ def measure_cfg3(dev, hbm_peak, steps=5, warmup=2):
                      "frac_of_measured": round(gbs / hbm_peak, 4), "frac_of_8tbs": round(gbs / 8000.0, 4)}
     del src, dst
     torch.cuda.empty_cache()
+    # NEXT #1, the paper's mechanism: the same ancestors applied to block tables
+    # (16-token pages: 128 per particle, the first 8 = shared prompt pages) + refcounts; no KV
+    # content moves.  Tables double-buffered (swapped every step).
+    PG, shared = S // 16, 8
+    tab = torch.full((1, N, PG), -1, dtype=torch.int32, device=dev)
+    ids = torch.arange(shared, dtype=torch.int32, device=dev)
+    own = shared + torch.arange(N * (PG - shared), dtype=torch.int32, device=dev).view(N, PG - shared)
+    tab[0, :, :shared] = ids
+    tab[0, :, shared:] = own
+    npg = torch.full((1, N), PG, dtype=torch.int32, device=dev)
+    num_pages = shared + N * (PG - shared)
+    refc = torch.ones(num_pages, dtype=torch.int32, device=dev)
+    refc[:shared] = N
+    freed = torch.zeros(num_pages, dtype=torch.uint8, device=dev)
+    bufs = [(tab, npg), (torch.empty_like(tab), torch.empty_like(npg))]
+    lwb = lw.clone()
+
+    def fnp(i):
+        lwb.copy_(lw)
+        r = smc.smcsd_resample(lwb, eta=math.inf, step=i, out=o)
+        (ts, ns), (td, nd) = bufs[i % 2], bufs[(i + 1) % 2]
+        smc.smcsd_kv_reindex_paged(ts, ns, refc, r.ancestors, table_dst=td, n_pages_dst=nd, freed=freed)
+    msp = _time_steps(fnp, 20, 3, 1, dev)
+    res["paged"] = {"us_per_step": round(msp * 1e3, 2), "kv_content_bytes": 0,
+                    "table_bytes": int(2 * N * PG * 4 + num_pages * 5),
+                    "vs_dense_in_place": round(res["in_place"]["ms_per_step"] / msp, 1),
+                    "note": "resample + block-table/refcount reindex (K5); pages of 16 tokens"}
     res["workload"] = ("cfg3: 70B KV, N=32, pinned pattern (16 sources x 2 offspring, 16 dead slots); "
-                       "step = smcsd_resample + smcsd_kv_reindex")
+                       "step = smcsd_resample + smcsd_kv_reindex (dense) or smcsd_kv_reindex_paged")
     return res
 
 

@@ -48,6 +48,8 @@ CASES = [
     (2, 7, 5, 20001, torch.bfloat16, 1.5),        # odd V (bf16 vector straddles V)
     (1, 1, 1, 3, torch.float32, 0.5),             # V < one vector, N = 1, K = 1
     (2, 33, 2, 50000, torch.float32, 0.5),        # N not a multiple of 32
+    (2, 3, 33, 1000, torch.float32, 0.5),         # K > 32: chunks split particles (S3 in last CTA)
+    (1, 7, 7, 3000, torch.bfloat16, 0.5),         # K = 7: 28-pair chunks of whole particles
 ]
 
 
