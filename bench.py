@@ -155,6 +155,7 @@ class Cfg2Step:
         total = args.warmup + args.steps + 4
         mk = lambda dt: torch.zeros((total, P, N), dtype=dt, device=dev)
         self.anc, self.off, self.slot = mk(torch.int32), mk(torch.int32), mk(torch.int32)
+        self.essrec = torch.zeros((total, P), dtype=torch.float64, device=dev)
         self.out = smc.Outputs(logw=self.logw, status=torch.zeros(P, dtype=torch.int32, device=dev),
                                resampled=torch.zeros(P, dtype=torch.uint8, device=dev),
                                ess=torch.zeros(P, dtype=torch.float64, device=dev),
@@ -183,6 +184,7 @@ class Cfg2Step:
         lp, lq, tok = inputs if inputs is not None else self.ring[i % len(self.ring)]
         o = self.out
         o.ancestors, o.offspring, o.slot_src = self.anc[i], self.off[i], self.slot[i]
+        o.ess = self.essrec[i]
         if events: events[0].record()
         smc.smcsd_step(lp, lq, tok, V=self.V, logw_prev=self.logw, eta=math.inf,
                        seed=0x5EED5EED, step=i, prompt_base=self.prompt_base, out=o,
@@ -271,6 +273,7 @@ def run_ours(args, rank, world, local):
     step_gbs = step_bytes / (ms_per_step / 1e3) / 1e9
     anc = wl.anc[timed].cpu()
     dead = statistics.fmean(float((wl.off[s] == 0).sum()) for s in timed)
+    ess_frac = float(wl.essrec[timed].mean().item()) / wl.N
 
     # ---- end to end through the public API with host buffers (H2D of inputs, D2H of result)
     e2e = run_e2e(wl, args, dev, world)
@@ -299,6 +302,7 @@ def run_ours(args, rank, world, local):
             "eta": "inf (resample every step)", "parallelism": f"dp{world} (prompts)",
             "l2": "logits ring of 6 sets (394 MB > 126 MB L2); KV 10.7 GB > L2",
             "kv_mode": "in-place slot plan", "mean_dead_slots": round(dead, 2),
+            "mean_ess_over_n": round(ess_frac, 4),
         },
         "hbm": {"algorithmic_bytes_per_step": int(step_bytes),
                 "achieved_gbs": round(step_gbs, 1),
@@ -495,6 +499,18 @@ def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
         wsf = smc.Workspace(dev)
         fnf = lambda i: ex.step(sp, sq, tok, logw_prev=logw, eta=math.inf, step=i, out=of,
                                 fields=(), workspace=wsf)
+        # one checked step first: a peer mapping that does not work shows up as ST_EXCHANGE
+        # after the bounded wait (20 s), never as a hang; then the path is not timed
+        fnf(0)
+        torch.cuda.synchronize()
+        bad = float((of.status != 0).any().item())
+        if world > 1:
+            import torch.distributed as tdist
+            t = torch.tensor([bad], device=dev if tdist.get_backend() == "nccl" else "cpu")
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            bad = float(t.item())
+        if bad != 0:
+            raise RuntimeError(f"fused exchange check failed: status {of.status.tolist()}")
         msf = _time_steps(fnf, steps, warmup, world, dev)
         torch.cuda.synchronize()
         res["fused_exchange"] = {"ms_per_step": round(msf, 4), "steps_per_s": round(1e3 / msf, 1),

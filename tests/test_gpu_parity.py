@@ -589,3 +589,23 @@ def test_tp_step_fused_exchange(smc, orc, G, P, N, K, V, dtype):
         rr = orc.resample(np_(outs[0].logw_pre), eta=np.inf, seed=3, step=it)
         assert np.array_equal(np_(outs[0].ancestors), rr["ancestors"])
         assert np.array_equal(np_(outs[0].logw), rr["logw"])
+
+
+def test_extreme_and_masked_rows(smc, orc):
+    # SURVEY 8(d) edge rows: +-60 extremes and -inf-masked tails (vocabulary masking), both
+    # dtypes; the drafted token always keeps finite target and draft mass
+    for dtype in (torch.float32, torch.bfloat16):
+        P, N, K, V = 2, 8, 4, 20000
+        lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=dtype, seed=4242)
+        g = torch.Generator().manual_seed(5)
+        ext = torch.rand(lp.shape[:-1] + (V,), generator=g) < 0.002
+        sign = torch.where(torch.rand(ext.shape, generator=g) < 0.5, -60.0, 60.0).to(dtype)
+        lp[..., :V] = torch.where(ext, sign, lp[..., :V])
+        lq[..., :V] = torch.where(ext[:, :, :K], sign[:, :, :K], lq[..., :V])
+        lp[0, :, :, 15000:V] = -float("inf")                # masked tail (prompt 0)
+        lq[0, :, :, 15000:V] = -float("inf")
+        tok[0] = tok[0] % 15000                             # drafted tokens stay unmasked
+        gpu, ref = _run_weights(smc, orc, lp, lq, tok, V)
+        assert np.array_equal(np_(gpu.status).astype(np.uint32), ref["status"])
+        assert max_abs(np_(gpu.logp_tok), ref["logp_tok"]) <= TOL_ELL * 4
+        assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW
