@@ -46,7 +46,7 @@ class SmcsdError(RuntimeError):
 
 def _load():
     if not os.path.exists(lib_path):
-        raise ImportError(f"{lib_path} is missing: run `python -m paper_2604_15672_b200.build` "
+        raise ImportError(f"{lib_path} is missing: run `python paper_2604_15672_b200/build.py` "
                           "(or __graft_entry__.build()) -- there is no fallback path")
     L = ctypes.CDLL(lib_path)
     vp, i32, i64, f32, u64, sz = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_float,

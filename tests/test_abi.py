@@ -22,7 +22,11 @@ def _declared():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_2604_15672_b200 import build as b
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_smcsd_build", os.path.join(ROOT, "paper_2604_15672_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)  # by path: the package __init__ needs the library to exist
     b.build()
     return ctypes.CDLL(b.LIB)
 
