@@ -80,9 +80,12 @@ typedef enum { SMCSD_SYSTEMATIC = 0, SMCSD_MULTINOMIAL = 1 } smcsd_scheme;
  * columns per row (V, or the shard width for the partial call). */
 SMCSD_API size_t smcsd_workspace_bytes(int P, int N, int K, int64_t v_len);
 
-/* Zero a workspace (enqueued).  Required once after allocation: the kernels use per-prompt
- * completion counters inside the workspace and leave them zero on exit, so a workspace
- * stays valid across calls and CUDA-graph replays. */
+/* Zero a workspace (enqueued).  Required after allocation AND whenever the workspace is next
+ * used with a different (P, N, K, v_len): the kernels keep per-prompt completion counters and
+ * status words inside the workspace at shape-dependent offsets and leave them zero on exit,
+ * so a workspace stays valid across calls and CUDA-graph replays of one shape, but a new
+ * shape may place its counters over an earlier shape's data.  (The Python binding's
+ * Workspace does this re-zeroing on shape change.) */
 SMCSD_API smcsd_rc smcsd_workspace_init(void *workspace, size_t workspace_bytes, void *stream);
 
 /* S1-S4.

@@ -156,12 +156,17 @@ class Workspace:
     def __init__(self, device=None):
         self.device = torch.device("cuda" if device is None else device)
         self.buf = None
+        self.shape = None
 
     def get(self, P, N, K, v_len, stream=None):
         need = smcsd_workspace_bytes(P, N, K, v_len)
         if self.buf is None or self.buf.numel() < need:
             self.buf = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+            self.shape = None
+        if self.shape != (P, N, K, v_len):
+            # counters sit at shape-dependent offsets: re-zero on every shape change (smcsd.h)
             smcsd_workspace_init(self.buf, stream)
+            self.shape = (P, N, K, v_len)
         return self.buf
 
 
