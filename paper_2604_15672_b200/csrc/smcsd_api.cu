@@ -129,8 +129,7 @@ smcsd_rc ensure_tail_attrs() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
     if (!attr_set[dev]) {
-        if (cudaFuncSetAttribute(k_tail_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess ||
-            cudaFuncSetAttribute(k_merge_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess)
+        if (cudaFuncSetAttribute(k_tail_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess)
             return SMCSD_ECUDA;
         attr_set[dev] = true;
     }
@@ -340,8 +339,9 @@ smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_
     cudaStream_t st = as_stream(stream);
     rc = launch_rowstats(prm, dtype, 2ll * P * N * K * prm.nseg, st);
     if (rc != SMCSD_OK) return rc;
-    if (ensure_tail_attrs() != SMCSD_OK) return SMCSD_ECUDA;
-    return launch_pdl(k_merge_rows, (unsigned)P, kTailStageBytes, st, prm);
+    const int64_t grid = (int64_t)P * cdiv(2ll * N * K, kMergeRowsPerCta);
+    if (grid >= (1ll << 31)) return SMCSD_EINVAL;
+    return launch_pdl(k_merge_rows, (unsigned)grid, 0, st, prm);
 }
 
 smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int32_t *tokens,

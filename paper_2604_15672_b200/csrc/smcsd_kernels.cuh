@@ -1213,7 +1213,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
             kn = 0;
         }
         double delta = 0.0;
-        for (int j = 0; j < kn; ++j) delta = __dadd_rn(delta, __ldcg(&terms[n * K + j]));
+        for (int j0 = 0; j0 < kn; j0 += 8) {                // loads first, then the j-order sum
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = j0 + u < kn ? __ldcg(&terms[n * K + j0 + u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (j0 + u < kn) delta = __dadd_rn(delta, t[u]);
+        }
         if (isnan(delta)) bad = true;                       // an invalid pair (flag raised in S2)
         const float prev = prm.logw_prev ? prm.logw_prev[pn] : neglogN;
         if (isnan(prev) || prev == INFINITY) {
@@ -1244,26 +1251,59 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     pdl_trigger();
 }
 
-// K2 (TP partial path): merge each row's segment partials into one {m, s, x, 0}.  grid = P.
-// Coalesced staged merge (tail_rowstats); x = t_d when the drafted token is in this shard.
+// K2 (TP partial path): merge each row's segment partials into one {m, s, x, 0}.  grid =
+// P x ceil(2NK / 64): one CTA per 64 rows, 16 lanes per row (coalesced 16-byte loads, the fixed
+// 16-lane tree of k_tail), 4 passes; x = t_d (when the drafted token is in this shard) read from
+// the logits before griddepcontrol.wait by the row's first thread.
+constexpr int kMergeRowsPerCta = 64;
 __global__ void __launch_bounds__(kThreads) k_merge_rows(const __grid_constant__ Params prm) {
-    extern __shared__ float4 stage[];
-    const int p = blockIdx.x, tid = threadIdx.x, N = prm.N, K = prm.K, NK = N * K;
-    const int rows = 2 * NK;
-    auto row_x = [&](int r) -> float {                        // inputs only: safe before the wait
-        const int model = r / NK, q = r - model * NK, n = q / K, j = q - n * K;
-        const int64_t pn = (int64_t)p * N + n;
-        const int kn = drafted_len(prm, pn);
-        return (kn >= 0 && kn <= K && j < kn) ? load_x(prm, model, pn, j, prm.tokens[pn * K + j])
-                                              : -INFINITY;
-    };
-    const float x_pre = tid < rows ? row_x(tid) : -INFINITY;
+    const int tid = threadIdx.x, N = prm.N, K = prm.K, NK = N * K, rows = 2 * NK;
+    const int chunks = (rows + kMergeRowsPerCta - 1) / kMergeRowsPerCta;
+    const int p = blockIdx.x / chunks, r0 = (blockIdx.x - p * chunks) * kMergeRowsPerCta;
+    __shared__ float xs[kMergeRowsPerCta];
+    if (tid < kMergeRowsPerCta) {                              // inputs only: safe before the wait
+        const int r = r0 + tid;
+        float x = -INFINITY;
+        if (r < rows) {
+            const int model = r / NK, q = r - model * NK, n = q / K, j = q - n * K;
+            const int64_t pn = (int64_t)p * N + n;
+            const int kn = drafted_len(prm, pn);
+            if (kn >= 0 && kn <= K && j < kn) x = load_x(prm, model, pn, j, prm.tokens[pn * K + j]);
+        }
+        xs[tid] = x;
+    }
     pdl_wait();
-    if (tid == 0 && p == 0) *prm.work_ctr = 0u;               // re-arm K1's counter
-    float4 *out = prm.partials_out + (int64_t)p * rows;
-    tail_rowstats(prm, p, out, stage);
+    if (tid == 0 && blockIdx.x == 0) *prm.work_ctr = 0u;      // re-arm K1's counter
     __syncthreads();
-    for (int r = tid; r < rows; r += kThreads) out[r].z = r == tid ? x_pre : row_x(r);
+    const int li = tid & 15, rsub = tid >> 4;
+    float3 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int r = r0 + rsub + 16 * u;
+        const int64_t grow = (int64_t)p * rows + r;
+        q[u] = make_float3(-INFINITY, 0.0f, -INFINITY);
+        if (r < rows) {
+            if (prm.nparts <= 16) {
+                if (li < prm.nparts) {
+                    const float4 t = __ldcg(&prm.parts[grow * prm.part_row_stride + (int64_t)li * prm.part_seg_stride]);
+                    q[u] = make_float3(t.x, t.y, t.z);
+                }
+            } else {
+                q[u] = lane_premerge(prm, grow, li);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        float M = q[u].x;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        float S = q[u].y * (q[u].x == M ? 1.0f : ex2_approx(q[u].x - M));
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+        const int lr = rsub + 16 * u, r = r0 + lr;
+        if (li == 0 && r < rows) prm.partials_out[(int64_t)p * rows + r] = make_float4(M, S, xs[lr], 0.0f);
+    }
     pdl_trigger();
 }
 

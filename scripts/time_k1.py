@@ -42,6 +42,12 @@ if "cfg5" in which:
     part = torch.empty((1, 2, 64, 8, 4), device=dev)
     ms = t(lambda i: smc.smcsd_weights_partial(lp, lq, tok, v_begin=0, v_len=128256, partials=part, workspace=ws), 30)
     res["cfg5-partial-G1"] = (ms, 262668288 / ms / 1e6)
+if "n64" in which:
+    ring = [synth.lm_logits(1, 64, 8, 128256, device=dev, seed=20 + r) for r in range(3)]
+    ws = smc.Workspace(dev); out = smc.Outputs()
+    ms = t(lambda i: smc.smcsd_step(*ring[i % 3], V=128256, step=i, out=out, fields=(), workspace=ws), 30)
+    res["N64-step"] = (ms, 262668288 / ms / 1e6)
+    del ring; torch.cuda.empty_cache()
 if "power" in which:
     PP = int(os.environ.get("POWER_P", "64"))
     lg, _, _ = synth.lm_logits(PP, 32, 1, 128256, device=dev, seed=6, bonus=False)
