@@ -174,10 +174,15 @@ class Cfg2Step:
             self.hist_geom = dict(n_outer=1, outer_stride=0, prompt_stride=N * self.T * 4,
                                   particle_stride=self.T * 4, seg_count=1, seg_bytes=self.T * 4,
                                   seg_stride=self.T * 4)
-        self.kernels = ["smcsd_step(k_rowstats+k_tail)"] + (["k_kv_reindex(kv)", "k_kv_reindex(tokens)"] if kv else [])
+        # S8 + S9 in one launch: the 70B KV blocks and the token history share the slot plan
+        self.kernels = ["smcsd_step(k_rowstats+k_tail)"] + (["k_kv_reindex(kv+tokens)"] if kv else [])
 
     def launches_per_step(self):
         return len(self.kernels)
+
+    def kernel_launches_per_step(self):
+        """CUDA kernel launches per step: smcsd_step is K1 + K2, the reindex one kernel."""
+        return 2 + (1 if self.kv is not None else 0)
 
     def step(self, i, events=None, inputs=None):
         smc = self.smc
@@ -191,10 +196,10 @@ class Cfg2Step:
                        fields=(), workspace=self.ws)
         if events: events[1].record()
         if self.kv is not None:
-            smc.smcsd_kv_reindex(self.kv, self.kv, self.slot[i], **self.kv_geom)
+            smc.smcsd_kv_reindex_multi([smc.kv_tensor(self.kv, self.kv, **self.kv_geom),
+                                        smc.kv_tensor(self.hist, self.hist, **self.hist_geom)],
+                                       self.slot[i])
             if events: events[2].record()
-            smc.smcsd_kv_reindex(self.hist, self.hist, self.slot[i], **self.hist_geom)
-            if events: events[3].record()
 
     # algorithmic bytes
     def logit_bytes(self):
@@ -255,7 +260,7 @@ def run_ours(args, rank, world, local):
     logit_b = wl.logit_bytes()
     kv_avg, tok_avg = statistics.fmean(kvb), statistics.fmean(tokb)
     step_bytes = logit_b + kv_avg + tok_avg
-    bytes_by_kernel = [logit_b, kv_avg, tok_avg]
+    bytes_by_kernel = [logit_b, kv_avg + tok_avg]
     kernels = []
     traffic = traffic_table()
     for name, ms, b in zip(wl.kernels, per_kernel_ms, bytes_by_kernel):
@@ -270,11 +275,12 @@ def run_ours(args, rank, world, local):
                 "frac": round(dk["achieved_gbs"] / hbm_peak, 4),
                 "traffic": tr, "kernel": dk["kernel"], "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": dk["algorithmic_bytes"]}
-    if tr and dk["kernel"] == "k_kv_reindex(kv)" and wl.off.shape[0] > 3:
-        # the ncu capture (scripts/gpu_profile.sh: -k k_kv_reindex -s 6 -c 1 on --warmup 3) is the
-        # KV launch of bench step 3, whose plan (dead slots) differs from the average launch:
+    if tr and dk["kernel"] == "k_kv_reindex(kv+tokens)" and wl.off.shape[0] > 3:
+        # the ncu capture (scripts/gpu_profile.sh: -k k_kv_reindex -s 3 -c 1 on --warmup 3) is the
+        # reindex launch of bench step 3, whose plan (dead slots) differs from the average launch:
         # compare its DRAM bytes with its own algorithmic bytes
-        alg3 = wl.kv_bytes([3])[0][0]
+        kv3, tok3 = wl.kv_bytes([3])
+        alg3 = kv3[0] + tok3[0]
         roofline["traffic_launch"] = {"bench_step": 3, "algorithmic_bytes": int(alg3),
                                       "dram_over_algorithmic": round(tr / alg3, 4) if alg3 else None}
     step_gbs = step_bytes / (ms_per_step / 1e3) / 1e9
@@ -321,7 +327,7 @@ def run_ours(args, rank, world, local):
                       "verify_resample_steps_per_s": round(1e3 / per_kernel_ms[0], 1)},
         "e2e": e2e,
         "secondary": secondary,
-        "gpu_launches": nk * args.steps,
+        "gpu_launches": wl.kernel_launches_per_step() * args.steps,
         "clocks": clk.summary(),
         "library": smc.smcsd_version(),
         "ancestor_sample": anc[-1, 0].tolist(),

@@ -200,6 +200,21 @@ SMCSD_API smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer,
                           int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index,
                           int P, int N, void *stream);
 
+/* S8/S9 over several state tensors in ONE launch, with one src_index: e.g. per-layer K and V
+ * tensors of a serving engine (dst[], src[], n_tensors) plus the token history.
+ * tensors: HOST array of n_tensors (1..256) descriptors, read during the call (caller keeps
+ * ownership; not retained).  Each tensor has its own geometry, with the meaning and the
+ * alignment rules of smcsd_kv_reindex above; dst == src selects in-place per tensor.  Tensors
+ * must not overlap each other.  smcsd_kv_reindex(...) is this call with n_tensors = 1. */
+typedef struct {
+    void *dst;                    /* device base of the destination blocks            */
+    const void *src;              /* device base of the source blocks (== dst: in place) */
+    int64_t n_outer, outer_stride, prompt_stride, particle_stride;   /* bytes */
+    int64_t seg_count, seg_bytes, seg_stride;                        /* bytes */
+} smcsd_kv_tensor;
+SMCSD_API smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
+                                          const int32_t *src_index, int P, int N, void *stream);
+
 /* Terminal selection: "one complete sequence is sampled from the terminal
  * normalized weights".  selected[p] = #{m : C_m <= u} with u = word0(Philox(key = seed,
  * ctr = (step_lo, step_hi, prompt_base + p, 0xFFFFFFFF))) * 2^-32 (or uniforms[p]); -1 and

@@ -21,6 +21,7 @@ __all__ = [
     "SmcsdError", "Workspace", "lib_path",
     "smcsd_workspace_bytes", "smcsd_workspace_init", "smcsd_weights", "smcsd_step",
     "smcsd_resample", "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
+    "smcsd_kv_reindex_multi", "kv_tensor",
     "smcsd_version", "kv_geometry", "smcsd_select", "smcsd_kv_reindex_paged", "ST_BAD_PAGE",
     "smcsd_powersmc_weights", "smcsd_tp_exchange_bytes", "smcsd_tp_exchange_init",
     "smcsd_ipc_handle_bytes", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close", "smcsd_tp_step",
@@ -42,6 +43,14 @@ class SmcsdError(RuntimeError):
     def __init__(self, name, rc):
         super().__init__(f"{name} failed: rc={rc} ({_RC.get(rc, 'unknown')})")
         self.rc = rc
+
+
+class _KvTensor(ctypes.Structure):
+    """include/smcsd.h smcsd_kv_tensor (byte geometry of one state tensor)."""
+    _fields_ = [("dst", ctypes.c_void_p), ("src", ctypes.c_void_p), ("n_outer", ctypes.c_int64),
+                ("outer_stride", ctypes.c_int64), ("prompt_stride", ctypes.c_int64),
+                ("particle_stride", ctypes.c_int64), ("seg_count", ctypes.c_int64),
+                ("seg_bytes", ctypes.c_int64), ("seg_stride", ctypes.c_int64)]
 
 
 def _load():
@@ -66,6 +75,7 @@ def _load():
     L.smcsd_weights_combine.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i64, f32, vp, vp, vp,
                                         vp, vp, vp, vp, vp, sz, vp]
     L.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
+    L.smcsd_kv_reindex_multi.argtypes = [ctypes.POINTER(_KvTensor), i32, vp, i32, i32, vp]
     L.smcsd_select.argtypes = [vp, i32, i32, i64, u64, u64, vp, vp, vp, vp, sz, vp]
     L.smcsd_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
     L.smcsd_powersmc_weights.argtypes = [vp, i64, i32, i32, vp, i32, i32, i64, f32, f32, vp, vp,
@@ -85,7 +95,7 @@ def _load():
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     for name in ("smcsd_workspace_init", "smcsd_weights", "smcsd_resample", "smcsd_step",
                  "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
-                 "smcsd_select", "smcsd_kv_reindex_paged", "smcsd_powersmc_weights",
+                 "smcsd_kv_reindex_multi", "smcsd_select", "smcsd_kv_reindex_paged", "smcsd_powersmc_weights",
                  "smcsd_tp_exchange_init", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close",
                  "smcsd_tp_step"):
         getattr(L, name).restype = i32
@@ -450,6 +460,27 @@ def kv_geometry(kv: torch.Tensor, seq_len: int | None = None) -> dict:
     return dict(n_outer=L * C, outer_stride=P * N * H * S * d * e, prompt_stride=N * H * S * d * e,
                 particle_stride=H * S * d * e, seg_count=H, seg_bytes=seq_len * d * e,
                 seg_stride=S * d * e)
+
+
+def kv_tensor(dst, src, *, n_outer, outer_stride, prompt_stride, particle_stride, seg_count,
+              seg_bytes, seg_stride):
+    """One entry of smcsd_kv_reindex_multi: (dst, src) device tensors and their byte geometry
+    (as kv_geometry returns it); dst is src for the in-place slot plan."""
+    return (dst, src, dict(n_outer=n_outer, outer_stride=outer_stride, prompt_stride=prompt_stride,
+                           particle_stride=particle_stride, seg_count=seg_count, seg_bytes=seg_bytes,
+                           seg_stride=seg_stride))
+
+
+def smcsd_kv_reindex_multi(tensors, src_index, *, stream=None):
+    """S8/S9 over several state tensors in one launch (per-layer K/V tensors, token history):
+    tensors is a list of kv_tensor(...) entries sharing src_index [P][N]."""
+    P, N = src_index.shape
+    arr = (_KvTensor * len(tensors))()
+    for k, (dst, src, g) in enumerate(tensors):
+        arr[k] = _KvTensor(_p(dst), _p(src), g["n_outer"], g["outer_stride"], g["prompt_stride"],
+                           g["particle_stride"], g["seg_count"], g["seg_bytes"], g["seg_stride"])
+    rc = _lib.smcsd_kv_reindex_multi(arr, len(tensors), _p(src_index), P, N, _stream(stream))
+    _check("smcsd_kv_reindex_multi", rc)
 
 
 def smcsd_kv_reindex(dst, src, src_index, *, n_outer, outer_stride, prompt_stride,

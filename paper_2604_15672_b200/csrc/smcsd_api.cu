@@ -369,32 +369,48 @@ smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int32_t *toke
     return launch_tail(prm, 0, as_stream(stream));
 }
 
+smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
+                                const int32_t *src_index, int P, int N, void *stream) {
+    if (!tensors || !src_index || n_tensors < 1 || n_tensors > kMaxKvTensors) return SMCSD_EINVAL;
+    if (P < 1 || N < 1 || N > kTailMaxN) return SMCSD_EINVAL;
+    KvParams prm;
+    std::memset(&prm, 0, sizeof prm);
+    prm.idx = src_index; prm.P = P; prm.N = N; prm.n_tensors = n_tensors;
+    int64_t items = 0;
+    for (int k = 0; k < n_tensors; ++k) {
+        const smcsd_kv_tensor &a = tensors[k];
+        if (!a.dst || !a.src) return SMCSD_EINVAL;
+        if (a.n_outer < 1 || a.seg_count < 1 || a.seg_bytes < 16) return SMCSD_EINVAL;
+        if (!aligned16(a.dst) || !aligned16(a.src)) return SMCSD_EINVAL;
+        if ((a.seg_bytes | a.outer_stride | a.prompt_stride | a.particle_stride | a.seg_stride) & 15)
+            return SMCSD_EINVAL;
+        if (a.outer_stride < 0 || a.prompt_stride < 0 || a.particle_stride < 0 || a.seg_stride < 0)
+            return SMCSD_EINVAL;
+        const uint64_t vps = (uint64_t)a.seg_bytes / 16;
+        if (vps >= (1ull << 32)) return SMCSD_EINVAL;
+        KvTensor &t = prm.t[k];
+        t.dst = static_cast<char *>(a.dst);
+        t.src = static_cast<const char *>(a.src);
+        t.outer_stride = a.outer_stride; t.prompt_stride = a.prompt_stride;
+        t.particle_stride = a.particle_stride; t.seg_stride = a.seg_stride;
+        t.vps = (uint32_t)vps;
+        t.in_place = a.dst == a.src;
+        t.vecs = (uint64_t)a.seg_count * vps;
+        t.nchunks = (int64_t)cdiv((int64_t)t.vecs, kKvChunkVec);
+        items += a.n_outer * P * t.nchunks;
+        if (items >= (1ll << 31)) return SMCSD_EINVAL;
+        t.item_end = items;
+    }
+    return launch_pdl(k_kv_reindex, (unsigned)items, 0, as_stream(stream), prm);
+}
+
 smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_stride,
                           int64_t prompt_stride, int64_t particle_stride, int64_t seg_count,
                           int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index,
                           int P, int N, void *stream) {
-    if (!dst || !src || !src_index) return SMCSD_EINVAL;
-    if (P < 1 || N < 1 || N > kTailMaxN || n_outer < 1 || seg_count < 1 || seg_bytes < 16)
-        return SMCSD_EINVAL;
-    if (!aligned16(dst) || !aligned16(src)) return SMCSD_EINVAL;
-    if ((seg_bytes | outer_stride | prompt_stride | particle_stride | seg_stride) & 15)
-        return SMCSD_EINVAL;
-    if (outer_stride < 0 || prompt_stride < 0 || particle_stride < 0 || seg_stride < 0)
-        return SMCSD_EINVAL;
-    const uint64_t vps = (uint64_t)seg_bytes / 16;
-    if (vps >= (1ull << 32)) return SMCSD_EINVAL;
-    KvParams prm;
-    prm.dst = static_cast<char *>(dst);
-    prm.src = static_cast<const char *>(src);
-    prm.outer_stride = outer_stride; prm.prompt_stride = prompt_stride;
-    prm.particle_stride = particle_stride; prm.seg_stride = seg_stride;
-    prm.vps = (uint32_t)vps;
-    prm.vecs = (uint64_t)seg_count * vps;
-    prm.nchunks = (int64_t)cdiv((int64_t)prm.vecs, kKvChunkVec);
-    prm.idx = src_index; prm.P = P; prm.N = N; prm.in_place = dst == src;
-    const int64_t items = n_outer * P * prm.nchunks;
-    if (items >= (1ll << 31)) return SMCSD_EINVAL;
-    return launch_pdl(k_kv_reindex, (unsigned)items, 0, as_stream(stream), prm);
+    const smcsd_kv_tensor t = {dst, src, n_outer, outer_stride, prompt_stride, particle_stride,
+                               seg_count, seg_bytes, seg_stride};
+    return smcsd_kv_reindex_multi(&t, 1, src_index, P, N, stream);
 }
 
 smcsd_rc smcsd_select(const float *logw, int P, int N, int64_t prompt_base, uint64_t seed,

@@ -1596,26 +1596,46 @@ __global__ void __launch_bounds__(kThreads) k_paged_freed(const __grid_constant_
 constexpr int kKvUnroll = 4;
 constexpr int kKvChunkVec = kThreads * kKvUnroll;             // 16-byte vectors per CTA chunk
 
-struct KvParams {
+// One state tensor of a reindex launch (byte geometry; see smcsd_kv_tensor in smcsd.h).
+struct KvTensor {
     char *dst;
     const char *src;
     int64_t outer_stride, prompt_stride, particle_stride, seg_stride;
     uint32_t vps;                 // 16-byte vectors per segment
+    int in_place;                 // dst == src: apply the slot plan (skip src_index[n] == n)
     uint64_t vecs;                // vectors per block = seg_count * vps
-    int64_t nchunks;
-    const int32_t *idx;
-    int P, N, in_place;
+    int64_t nchunks;              // CTA chunks per block
+    int64_t item_end;             // exclusive prefix of items (n_outer * P * nchunks) over tensors
+};
+constexpr int kMaxKvTensors = 256;        // 256 x 72 B of __grid_constant__ parameters
+
+struct KvParams {
+    const int32_t *idx;           // [P][N] src_index (ancestors, or the slot plan in place)
+    int P, N, n_tensors;
+    KvTensor t[kMaxKvTensors];
 };
 
+// Grid = sum over tensors of n_outer * P * nchunks items; item -> (tensor by binary search over
+// item_end, outer plane, prompt, chunk).  Every CTA builds its prompt's copy plan (destinations
+// grouped by source, counting sort) and copies its chunk source-major: each source vector is
+// loaded once and stored to every destination.
 __global__ void __launch_bounds__(kThreads) k_kv_reindex(const __grid_constant__ KvParams prm) {
     __shared__ int cnt[kTailMaxN], start[kTailMaxN], fill[kTailMaxN], dsts[kTailMaxN], srcs[kTailMaxN];
     __shared__ int wtot[kWarps + 1];
     const int tid = threadIdx.x, N = prm.N;
-    const int64_t item = blockIdx.x;
-    const int64_t chunk = item % prm.nchunks;
-    const int64_t op = item / prm.nchunks;
+    int lo = 0, hi = prm.n_tensors - 1;                        // first tensor with item_end > item
+    const int64_t gitem = blockIdx.x;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (prm.t[mid].item_end > gitem) hi = mid; else lo = mid + 1;
+    }
+    const KvTensor &T = prm.t[lo];
+    const int64_t item = gitem - (lo > 0 ? prm.t[lo - 1].item_end : 0);
+    const int64_t chunk = item % T.nchunks;
+    const int64_t op = item / T.nchunks;
     const int p = (int)(op % prm.P);
     const int64_t o = op / prm.P;
+    const int in_place = T.in_place;
     const int32_t *idx = prm.idx + (int64_t)p * N;
     pdl_wait();                                                // src_index from the tail kernel
 
@@ -1624,7 +1644,7 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex(const __grid_constant__
     __syncthreads();
     for (int n = tid; n < N; n += kThreads) {
         const int s = idx[n];
-        if ((unsigned)s < (unsigned)N && (!prm.in_place || s != n)) atomicAdd(&cnt[s], 1);
+        if ((unsigned)s < (unsigned)N && (!in_place || s != n)) atomicAdd(&cnt[s], 1);
     }
     __syncthreads();
     for (int n = tid; n < N; n += kThreads) {
@@ -1641,7 +1661,7 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex(const __grid_constant__
     __syncthreads();
     for (int n = tid; n < N; n += kThreads) {
         const int s = idx[n];
-        if ((unsigned)s < (unsigned)N && (!prm.in_place || s != n))
+        if ((unsigned)s < (unsigned)N && (!in_place || s != n))
             dsts[start[s] + atomicAdd(&fill[s], 1)] = n;
     }
     __syncthreads();
@@ -1652,21 +1672,21 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex(const __grid_constant__
 #pragma unroll
     for (int i = 0; i < kKvUnroll; ++i) {
         const uint64_t v = (uint64_t)chunk * kKvChunkVec + (uint64_t)i * kThreads + tid;
-        valid[i] = v < prm.vecs;
-        const uint64_t g = v / prm.vps, w = v - g * prm.vps;
-        voff[i] = (int64_t)g * prm.seg_stride + (int64_t)w * 16;
+        valid[i] = v < T.vecs;
+        const uint64_t g = v / T.vps, w = v - g * T.vps;
+        voff[i] = (int64_t)g * T.seg_stride + (int64_t)w * 16;
     }
-    const int64_t pbase = o * prm.outer_stride + (int64_t)p * prm.prompt_stride;
+    const int64_t pbase = o * T.outer_stride + (int64_t)p * T.prompt_stride;
     for (int k = 0; k < nsrc; ++k) {
         const int s = srcs[k];
-        const char *sb = prm.src + pbase + (int64_t)s * prm.particle_stride;
+        const char *sb = T.src + pbase + (int64_t)s * T.particle_stride;
         uint4 r[kKvUnroll];
 #pragma unroll
         for (int i = 0; i < kKvUnroll; ++i)
             if (valid[i]) r[i] = ld_stream(sb + voff[i]);
         const int c = cnt[s], st0 = start[s];
         for (int q = 0; q < c; ++q) {
-            char *db = prm.dst + pbase + (int64_t)dsts[st0 + q] * prm.particle_stride;
+            char *db = T.dst + pbase + (int64_t)dsts[st0 + q] * T.particle_stride;
 #pragma unroll
             for (int i = 0; i < kKvUnroll; ++i)
                 if (valid[i]) st_stream(db + voff[i], r[i]);

@@ -11,6 +11,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_rowstats|k
     python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-secondary > $OUT/ncu_list_bench_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_rowstats -s 3 -c 1 \
     -o $OUT/prof_rowstats_$TAG -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-secondary > $OUT/ncu_rowstats_$TAG.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_kv_reindex -s 6 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:k_kv_reindex -s 3 -c 1 \
     -o $OUT/prof_kv_$TAG -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-secondary > $OUT/ncu_kv_$TAG.log 2>&1
 echo done

@@ -33,7 +33,7 @@ def lib():
 
 def test_every_declared_symbol_is_exported(lib):
     names = _declared()
-    assert len(names) == 20, names
+    assert len(names) == 21, names
     for n in names:
         assert hasattr(lib, n), n
 
@@ -111,3 +111,26 @@ def test_resample_and_kv_einval(lib):
     assert kv(dst=0x10008) == 1         # misaligned
     assert kv(particle=520) == 1
     assert kv(n_outer=0) == 1
+
+
+def test_kv_reindex_multi_rejects_bad_arguments(lib):
+    """smcsd_kv_reindex_multi validates synchronously (EINVAL, nothing enqueued)."""
+    import ctypes as c
+
+    class T(c.Structure):
+        _fields_ = [("dst", c.c_void_p), ("src", c.c_void_p)] + [
+            (n, c.c_int64) for n in ("n_outer", "outer_stride", "prompt_stride", "particle_stride",
+                                     "seg_count", "seg_bytes", "seg_stride")]
+    lib.smcsd_kv_reindex_multi.argtypes = [c.POINTER(T), c.c_int, c.c_void_p, c.c_int, c.c_int, c.c_void_p]
+    lib.smcsd_kv_reindex_multi.restype = c.c_int
+    good = T(0x10000, 0x20000, 4, 4096, 2048, 512, 2, 256, 256)
+    arr = (T * 2)(good, good)
+    assert lib.smcsd_kv_reindex_multi(arr, 0, 0x30000, 1, 4, None) == 1      # no tensors
+    assert lib.smcsd_kv_reindex_multi(arr, 257, 0x30000, 1, 4, None) == 1    # > 256 tensors
+    assert lib.smcsd_kv_reindex_multi(None, 1, 0x30000, 1, 4, None) == 1     # null list
+    assert lib.smcsd_kv_reindex_multi(arr, 2, None, 1, 4, None) == 1         # null src_index
+    arr[1] = T(0x10000, 0x20008, 4, 4096, 2048, 512, 2, 256, 256)            # misaligned 2nd
+    assert lib.smcsd_kv_reindex_multi(arr, 2, 0x30000, 1, 4, None) == 1
+    arr[1] = T(0x10000, 0x20000, 4, 4096, 2048, 512, 2, 100, 256)            # seg_bytes % 16
+    assert lib.smcsd_kv_reindex_multi(arr, 2, 0x30000, 1, 4, None) == 1
+

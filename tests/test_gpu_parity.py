@@ -351,6 +351,39 @@ def test_token_history_reindex(smc, orc):
     assert np.array_equal(dst.cpu().numpy(), want)
 
 
+def test_kv_reindex_multi_per_layer_tensors(smc, orc):
+    """smcsd_kv_reindex_multi: per-layer K and V tensors (separate allocations, a serving
+    engine's layout) + the token history in ONE launch, in place and out of place, against
+    the oracle's gather of the equivalent single tensor."""
+    dev = torch.device("cuda")
+    L, P, N, H, S, d, T = 3, 2, 13, 2, 96, 32, 52          # token rows: 208 B (16-B multiple)
+    kv = synth.kv_bits((L, 2, P, N, H, S, d), seed=21)
+    tok = torch.randint(0, 128256, (P, N, T), dtype=torch.int32)
+    lw = synth.random_logw(P, N, seed=21, sigma=2.0).numpy()
+    r = orc.resample(lw, eta=np.inf, seed=21)
+    for in_place in (True, False):
+        idx = r["slot_src"] if in_place else r["ancestors"]
+        layers = [kv[l, c].contiguous().to(dev) for l in range(L) for c in range(2)]  # [P][N][H][S][d]
+        outs = layers if in_place else [torch.zeros_like(t) for t in layers]
+        tsrc = tok.to(dev)
+        tdst = tsrc if in_place else torch.zeros_like(tsrc)
+        e = kv.element_size()
+        g = dict(n_outer=1, outer_stride=0, prompt_stride=N * H * S * d * e, particle_stride=H * S * d * e,
+                 seg_count=H, seg_bytes=70 * d * e, seg_stride=S * d * e)        # filled rows [0, 70)
+        gt = dict(n_outer=1, outer_stride=0, prompt_stride=N * T * 4, particle_stride=T * 4,
+                  seg_count=1, seg_bytes=T * 4, seg_stride=T * 4)
+        ents = [smc.kv_tensor(o, i, **g) for o, i in zip(outs, layers)] + [smc.kv_tensor(tdst, tsrc, **gt)]
+        smc.smcsd_kv_reindex_multi(ents, torch.from_numpy(idx).to(dev))
+        torch.cuda.synchronize()
+        want = kv.numpy().copy()
+        want_dst = want if in_place else np.zeros_like(want)
+        orc.kv_reindex(want_dst, want, idx, **smc.kv_geometry(kv, 70))
+        got = np.stack([outs[2 * l + c].cpu().numpy() for l in range(L) for c in range(2)]).reshape(want.shape)
+        assert np.array_equal(got, want_dst)
+        want_t = np.stack([tok.numpy()[p][idx[p]] if not in_place else tok.numpy()[p][idx[p]] for p in range(P)])
+        assert np.array_equal(tdst.cpu().numpy(), want_t)
+
+
 def test_kv_identity_is_noop(smc):
     dev = torch.device("cuda")
     kv = synth.kv_bits((2, 2, 1, 8, 2, 32, 16), seed=5).to(dev)
