@@ -20,8 +20,9 @@ lib = ctypes.CDLL(smc.lib_path)
 buf = (ctypes.c_ulonglong * 4096)()
 flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)
 for it in range(12):
-    lp, lq, tok = ring[it % 6]
-    flush_sum = flush.sum()  # read-only L2 flush (no dirty lines)
+    lp, lq, tok = ring[0 if os.environ.get("NOFLUSH") else it % 6]
+    if not os.environ.get("NOFLUSH"):
+        flush_sum = flush.sum()  # read-only L2 flush (no dirty lines)
     torch.cuda.synchronize()
     lib.smcsd_trace_read(buf, 4096)
     out = smc.smcsd_step(lp, lq, tok, V=V, eta=math.inf, step=it, fields=())
