@@ -16,7 +16,8 @@
  * (-ffp-contract=off: no fused multiply-add, so every fp64 op is one IEEE rounding.)
  *
  * Pinned by tests/test_oracle_*.py (see DESIGN.md section 4 for the pin table).
- * Parity unpinned: nothing here -- multi-round trajectories are not part of the oracle.
+ * Parity unpinned: nothing here.  Multi-round composition (R rounds of weights, resample, bonus,
+ * reindex) is pinned statistically by SMC's unbiasedness identity in tests/test_oracle_rounds.py.
  */
 #include <math.h>
 #include <stdint.h>
