@@ -87,8 +87,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 #define SMCSD_TRACE_AT(slot) do { g_trace[(slot)] = gtimer(); } while (0)
+#define SMCSD_CLK_AT(slot) do { g_trace[(slot)] = clock64(); } while (0)
 #else
 #define SMCSD_TRACE_AT(slot) do { } while (0)
+#define SMCSD_CLK_AT(slot) do { } while (0)
 #endif
 
 // ---- mbarrier + bulk async copy (TMA 1-D) --------------------------------------------------

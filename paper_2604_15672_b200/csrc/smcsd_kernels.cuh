@@ -1088,6 +1088,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     pdl_wait();
     if (tid == 0 && blockIdx.x == 0) {
         SMCSD_TRACE_AT(2049);                                   // predecessor complete
+        SMCSD_CLK_AT(2200);
         if (prm.work_ctr) *prm.work_ctr = 0u;                   // re-arm K1's counter
     }
     if (prm.xlocal) {
@@ -1109,6 +1110,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     }
 
     // ---- S2: 16 lanes per row, 16 rows per pass, 64 rows per CTA
+    if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2201);
     {
         const int li = tid & 15, rsub = tid >> 4;
         float3 q[4];
@@ -1144,6 +1146,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         }
     }
     __syncthreads();
+    if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2202);
     // ---- ell per row (thread = local row), then terms per pair
     uint32_t st = 0;
     if (row_thread) {
@@ -1168,6 +1171,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         if (outp) outp[lr_pn * K + j] = (float)ell;
     }
     __syncthreads();
+    if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2203);
     if (tid < nq) {
         const int qq = q0 + tid, j = qq - (qq / K) * K;
         const int kn = drafted_len(prm, (int64_t)p * N + qq / K);
@@ -1186,13 +1190,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         __stcg(&prm.ell_ws[(int64_t)p * NK + qq], term);
     }
     if (st) atomicOr(&prm.st_ws[p], st);
-    if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2053);      // chunk 0 S2 done
+    if (tid == 0 && blockIdx.x == 0) { SMCSD_TRACE_AT(2053); SMCSD_CLK_AT(2204); }      // chunk 0 S2 done
     }
     // ---- completion: the last CTA of the prompt finishes it
     __threadfence();
     __syncthreads();
+    if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2205);
     if (tid == 0) s_last = atomicAdd(&prm.prompt_ctr[p], 1u) == (unsigned)(per_prompt - 1);
     __syncthreads();
+    if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2206);
     if (!s_last) {
         pdl_trigger();
         return;

@@ -41,3 +41,7 @@ names = {2048: "tail CTA resident", 2049: "tail after pdl_wait", 2053: "chunk 0 
          2052: "after S4-S7"}
 for k, nm in names.items():
     print(f"{nm:22s} {us(t[k]):8.2f} us")
+ck = t[2200:2207]
+if ck[0]:
+    print("chunk 0 clocks after pdl_wait: " + "  ".join(
+        f"{nm} {ck[i] - ck[0]}" for i, nm in enumerate(["wait", "flags", "S2 merge", "ell", "terms", "fence", "counter"]) if ck[i]))
