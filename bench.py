@@ -406,10 +406,13 @@ def measure_cfg2_verify(dev, hbm_peak, steps=120, warmup=6):
     ring = [synth.lm_logits(P, N, K, V, device=dev, seed=synth.GEN_SEED_BASE + 200 + r) for r in range(6)]
     ws = smc.Workspace(dev)
     out = smc.Outputs()
-    res = {"workload": "cfg2 verify: smcsd_step S1-S7, P=1 N=16 K=8 V=128256 bf16, ring of 6"}
+    res = {"workload": "cfg2 verify: smcsd_step S1-S7, P=1 N=16 K=8 V=128256 bf16, ring of 6 "
+                       "(prepared calls: smc.StepPlan)"}
     for bonus in (False, True):
-        fn = lambda i: smc.smcsd_step(*ring[i % 6], V=V, eta=math.inf, step=i, out=out, fields=(),
-                                      workspace=ws, bonus=bonus)
+        # a prepared call (smc.StepPlan, ~9 us of host time) so the host does not pace a
+        # ~24 us device step; the plain binding call costs ~27 us of host time per step
+        plan = smc.StepPlan(*ring[0], V=V, eta=math.inf, out=out, fields=(), workspace=ws, bonus=bonus)
+        fn = lambda i, plan=plan: plan.run(*ring[i % 6], step=i)
         ms = _time_steps(fn, steps, warmup, 1, dev)
         byts = 2 * N * K * V * 2 + (N * V * 2 if bonus else 0)
         res["with_bonus" if bonus else "plain"] = {

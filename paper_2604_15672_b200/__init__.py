@@ -18,7 +18,7 @@ import torch
 __all__ = [
     "SMCSD_F32", "SMCSD_BF16", "SMCSD_SYSTEMATIC", "SMCSD_MULTINOMIAL", "SEGMENT",
     "ST_DEGENERATE", "ST_NOT_ABSCONT", "ST_BAD_TOKEN", "ST_NONFINITE",
-    "SmcsdError", "Workspace", "lib_path",
+    "SmcsdError", "Workspace", "StepPlan", "lib_path",
     "smcsd_workspace_bytes", "smcsd_workspace_init", "smcsd_weights", "smcsd_step",
     "smcsd_resample", "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
     "smcsd_kv_reindex_multi", "kv_tensor",
@@ -252,13 +252,11 @@ def smcsd_weights(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_pr
     return out
 
 
-def smcsd_step(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=None,
+def _step_args(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=None,
                alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, eta=math.inf,
                scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
-               out: Outputs | None = None, fields=_ALL_S, workspace=None,
-               stream=None, bonus=False) -> Outputs:
-    """Fused S1-S7 (one launch).  bonus=True also draws the bonus token x+ of every particle
-    from target row k_n (NEXT #2; logits_p needs K+1 rows) into out.bonus [P][N]."""
+               out: Outputs | None = None, fields=_ALL_S, workspace=None, stream=None, bonus=False):
+    """Validated smcsd_step argument list (in ABI order) and the Outputs it writes."""
     ld_p, rpp_p = _logits_geom(logits_p, "logits_p")
     ld_q, rpp_q = _logits_geom(logits_q, "logits_q")
     if logits_p.dtype != logits_q.dtype:
@@ -270,17 +268,65 @@ def smcsd_step(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=
                  ("logw", "status", "ancestors", "resampled") + tuple(fields)
                  + (("bonus",) if bonus else ()))
     ws = _ws(workspace, dev, P, N, K, V, stream)
-    rc = _lib.smcsd_step(_p(logits_p), ld_p, rpp_p, _p(logits_q), ld_q, rpp_q,
-                         _dtype_code(logits_p), _p(tokens), _p(n_drafted), _p(logw_prev),
-                         P, N, K, V, alpha, inv_temp_p, inv_temp_q, eta, scheme,
-                         seed & (2 ** 64 - 1), step & (2 ** 64 - 1), prompt_base, _p(uniforms),
-                         _p(out.logw), _p(out.logw_pre), _p(out.logp_tok), _p(out.logq_tok),
-                         _p(out.lse), _p(out.ess), _p(out.wnorm), _p(out.status),
-                         _p(out.ancestors), _p(out.offspring), _p(out.slot_src),
-                         _p(out.resampled), _p(out.n_ties), _p(out.bonus) if bonus else None,
-                         _p(ws), ws.numel(), _stream(stream))
-    _check("smcsd_step", rc)
+    args = [_p(logits_p), ld_p, rpp_p, _p(logits_q), ld_q, rpp_q,
+            _dtype_code(logits_p), _p(tokens), _p(n_drafted), _p(logw_prev),
+            P, N, K, V, alpha, inv_temp_p, inv_temp_q, eta, scheme,
+            seed & (2 ** 64 - 1), step & (2 ** 64 - 1), prompt_base, _p(uniforms),
+            _p(out.logw), _p(out.logw_pre), _p(out.logp_tok), _p(out.logq_tok),
+            _p(out.lse), _p(out.ess), _p(out.wnorm), _p(out.status),
+            _p(out.ancestors), _p(out.offspring), _p(out.slot_src),
+            _p(out.resampled), _p(out.n_ties), _p(out.bonus) if bonus else None,
+            _p(ws), ws.numel(), _stream(stream)]
+    return args, out
+
+
+def smcsd_step(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=None,
+               alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, eta=math.inf,
+               scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
+               out: Outputs | None = None, fields=_ALL_S, workspace=None,
+               stream=None, bonus=False) -> Outputs:
+    """Fused S1-S7 (one launch).  bonus=True also draws the bonus token x+ of every particle
+    from target row k_n (NEXT #2; logits_p needs K+1 rows) into out.bonus [P][N]."""
+    args, out = _step_args(logits_p, logits_q, tokens, V=V, n_drafted=n_drafted,
+                           logw_prev=logw_prev, alpha=alpha, inv_temp_p=inv_temp_p,
+                           inv_temp_q=inv_temp_q, eta=eta, scheme=scheme, seed=seed, step=step,
+                           prompt_base=prompt_base, uniforms=uniforms, out=out, fields=fields,
+                           workspace=workspace, stream=stream, bonus=bonus)
+    _check("smcsd_step", _lib.smcsd_step(*args))
     return out
+
+
+class StepPlan:
+    """smcsd_step with its argument list prepared once (plumbing for tight decode loops: the
+    binding's per-call validation and marshalling cost ~25 us of host time, more than a cfg2
+    step on the GPU).  run() swaps in new logits / tokens of the SAME shape, dtype and device
+    and the step counter, then makes the one C call.  Outputs land in plan.out."""
+    _I_LP, _I_LQ, _I_TOK, _I_STEP = 0, 3, 7, 20
+
+    def __init__(self, logits_p, logits_q, tokens, **kw):
+        self._args, self.out = _step_args(logits_p, logits_q, tokens, **kw)
+        self._sig = (tuple(logits_p.shape), tuple(logits_q.shape), tuple(tokens.shape),
+                     logits_p.dtype, logits_p.device)
+        ctypes_types = _lib.smcsd_step.argtypes
+        # pre-convert every argument to its ctypes type once
+        self._c = [t(a) if a is not None else None for t, a in zip(ctypes_types, self._args)]
+        self._fn = _lib.smcsd_step
+
+    def run(self, logits_p=None, logits_q=None, tokens=None, *, step=None):
+        c = self._c
+        if logits_p is not None:
+            if (tuple(logits_p.shape), tuple(logits_q.shape), tuple(tokens.shape),
+                    logits_p.dtype, logits_p.device) != self._sig or logits_q.dtype != logits_p.dtype:
+                raise ValueError("StepPlan.run: inputs differ in shape/dtype/device from the plan")
+            if not (logits_p.is_contiguous() and logits_q.is_contiguous() and tokens.is_contiguous()):
+                raise ValueError("StepPlan.run: inputs must be contiguous")
+            c[self._I_LP] = ctypes.c_void_p(logits_p.data_ptr())
+            c[self._I_LQ] = ctypes.c_void_p(logits_q.data_ptr())
+            c[self._I_TOK] = ctypes.c_void_p(tokens.data_ptr())
+        if step is not None:
+            c[self._I_STEP] = ctypes.c_uint64(step & (2 ** 64 - 1))
+        _check("smcsd_step", self._fn(*c))
+        return self.out
 
 
 def smcsd_resample(logw, *, eta=math.inf, scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0,

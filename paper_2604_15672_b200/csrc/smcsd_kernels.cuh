@@ -1109,41 +1109,66 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         __syncthreads();
     }
 
-    // ---- S2: 16 lanes per row, 16 rows per pass, 64 rows per CTA
+    // ---- S2: 4 lanes per row, 64 rows per CTA in one pass.  Lane l4 of a row merges parts
+    // 4 l4 .. 4 l4 + 3 (+ 16 c for rows with more than 16 parts) in index order in registers
+    // (coalesced: a row's 16 parts are 256 contiguous bytes), then a fixed 2-step shuffle tree
+    // (xor 2, xor 1).  x = t_d is taken from the logits (x_from_logits) or as the max of the
+    // parts' x (TP combine).
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2201);
     {
-        const int li = tid & 15, rsub = tid >> 4;
-        float3 q[4];
+        const int l4 = tid & 3, lr = tid >> 2;                  // local row: model = lr / 32
+        const int qq = lr & (kPairsPerCta - 1);
+        const int64_t grow = (int64_t)p * rows + (int64_t)(lr / kPairsPerCta) * NK + q0 + qq;
+        const float4 *pr = prm.parts + grow * prm.part_row_stride;
+        float Ml = -INFINITY, Sl = 0.0f, Xl = -INFINITY;
+        if (qq < nq) {
+            if (prm.nparts <= 16) {
+                float4 t[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int lr = rsub + 16 * u;                       // local row: model = lr / 32
-            const int qq = lr & (kPairsPerCta - 1);
-            const int64_t grow = (int64_t)p * rows + (int64_t)(lr / kPairsPerCta) * NK + q0 + qq;
-            q[u] = make_float3(-INFINITY, 0.0f, -INFINITY);
-            if (qq < nq) {
-                if (prm.nparts <= 16) {
-                    if (li < prm.nparts) {
-                        const float4 t = __ldcg(&prm.parts[grow * prm.part_row_stride + (int64_t)li * prm.part_seg_stride]);
-                        q[u] = make_float3(t.x, t.y, t.z);
-                    }
-                } else {
-                    q[u] = lane_premerge(prm, grow, li);
+                for (int k = 0; k < 4; ++k) {
+                    const int pi = 4 * l4 + k;
+                    t[k] = pi < prm.nparts ? __ldcg(pr + (int64_t)pi * prm.part_seg_stride)
+                                           : make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
                 }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    Ml = fmaxf(Ml, t[k].x);
+                    Xl = fmaxf(Xl, t[k].z);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    Sl = __fmaf_rn(t[k].y, t[k].x == Ml ? 1.0f : ex2_approx(t[k].x - Ml), Sl);
+            } else {
+                for (int c = 0; 4 * l4 + 16 * c < prm.nparts; ++c)
+                    for (int k = 0; k < 4; ++k) {
+                        const int pi = 4 * l4 + 16 * c + k;
+                        if (pi < prm.nparts) {
+                            const float4 t = __ldcg(pr + (int64_t)pi * prm.part_seg_stride);
+                            Ml = fmaxf(Ml, t.x);
+                            Xl = fmaxf(Xl, t.z);
+                        }
+                    }
+                for (int c = 0; 4 * l4 + 16 * c < prm.nparts; ++c)
+                    for (int k = 0; k < 4; ++k) {
+                        const int pi = 4 * l4 + 16 * c + k;
+                        if (pi < prm.nparts) {
+                            const float4 t = __ldcg(pr + (int64_t)pi * prm.part_seg_stride);
+                            Sl = __fmaf_rn(t.y, t.x == Ml ? 1.0f : ex2_approx(t.x - Ml), Sl);
+                        }
+                    }
             }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            float M = q[u].x, X = q[u].z;
-#pragma unroll
-            for (int o = 8; o > 0; o >>= 1) {
-                M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-                X = fmaxf(X, __shfl_xor_sync(0xffffffffu, X, o));
-            }
-            float S = q[u].y * (q[u].x == M ? 1.0f : ex2_approx(q[u].x - M));
-#pragma unroll
-            for (int o = 8; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
-            if (li == 0) rs[rsub + 16 * u] = make_float4(M, S, X, 0.0f);
+        float M = fmaxf(Ml, __shfl_xor_sync(0xffffffffu, Ml, 2));
+        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
+        float X = Xl;
+        if (!prm.x_from_logits) {                               // uniform branch
+            X = fmaxf(X, __shfl_xor_sync(0xffffffffu, X, 2));
+            X = fmaxf(X, __shfl_xor_sync(0xffffffffu, X, 1));
         }
+        float S = __fmul_rn(Sl, Ml == M ? 1.0f : ex2_approx(Ml - M));
+        S = __fadd_rn(S, __shfl_xor_sync(0xffffffffu, S, 2));
+        S = __fadd_rn(S, __shfl_xor_sync(0xffffffffu, S, 1));
+        if (l4 == 0) rs[lr] = make_float4(M, S, X, 0.0f);
     }
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2202);

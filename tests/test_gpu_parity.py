@@ -642,3 +642,23 @@ def test_extreme_and_masked_rows(smc, orc):
         assert np.array_equal(np_(gpu.status).astype(np.uint32), ref["status"])
         assert max_abs(np_(gpu.logp_tok), ref["logp_tok"]) <= TOL_ELL * 4
         assert max_abs(np_(gpu.logw), ref["logw"]) <= TOL_LOGW
+
+
+def test_step_plan_matches_step(smc):
+    """smc.StepPlan (prepared argument list) gives exactly smcsd_step's outputs, input swaps
+    included, and rejects inputs of another shape."""
+    dev = torch.device("cuda")
+    sets = [synth.lm_logits(2, 8, 4, 20001, dtype=torch.bfloat16, seed=900 + r) for r in range(2)]
+    sets = [tuple(t.to(dev) for t in s_) for s_ in sets]
+    ws = smc.Workspace(dev)
+    plan = smc.StepPlan(*sets[0], V=20001, out=smc.Outputs(), workspace=ws, bonus=True)
+    for i in range(4):
+        got = plan.run(*sets[i % 2], step=i)
+        torch.cuda.synchronize()
+        ref = smc.smcsd_step(*sets[i % 2], V=20001, step=i, bonus=True)
+        torch.cuda.synchronize()
+        for f in ("logw", "logw_pre", "ancestors", "slot_src", "ess", "bonus", "status"):
+            assert torch.equal(getattr(got, f), getattr(ref, f)), (i, f)
+    bad = synth.lm_logits(2, 8, 4, 20050, dtype=torch.bfloat16, seed=1)      # another row pitch
+    with pytest.raises(ValueError):
+        plan.run(*(t.to(dev) for t in bad), step=9)
