@@ -39,6 +39,28 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
     return upk2(r);
 }
 
+// 2^x on the FMA pipe (packed fp32x2), x <= 0: x = n + f with n = round(x) by the 1.5 * 2^23
+// trick (f in [-1/2, 1/2], exact), 2^f by a degree-4 minimax polynomial (max relative error
+// 2.7e-6 in fp32 Horner), times 2^n built from exponent bits (exact).  x is clamped at -127
+// first, so -inf (masked columns) gives exactly 0; NaN is NOT propagated (callers must detect
+// NaN elsewhere).  Used for the PowerSMC second sum only, where the MUFU pipe is the limit
+// (two ex2 per element); the plain exp-sum measured slower with it (profiles/r01f_ab_poly_exp2.txt).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -127.0f);
+    x.y = fmaxf(x.y, -127.0f);
+    const float2 y = fadd2(x, make_float2(12582912.0f, 12582912.0f));     // 1.5 * 2^23 + round(x)
+    const float2 r = fadd2(y, make_float2(-12582912.0f, -12582912.0f));   // round(x)
+    const float2 f = fadd2(x, make_float2(-r.x, -r.y));                   // x - round(x)
+    float2 p = ffma2(make_float2(0.009570609778165817f, 0.009570609778165817f), f,
+                     make_float2(0.055917903780937195f, 0.055917903780937195f));
+    p = ffma2(p, f, make_float2(0.24024732410907745f, 0.24024732410907745f));
+    p = ffma2(p, f, make_float2(0.6931217908859253f, 0.6931217908859253f));
+    p = ffma2(p, f, make_float2(0.9999992847442627f, 0.9999992847442627f));
+    const float sx = __uint_as_float((__float_as_uint(y.x) - 0x4B3FFF81u) << 23);   // 2^n
+    const float sy = __uint_as_float((__float_as_uint(y.y) - 0x4B3FFF81u) << 23);
+    return fmul2(p, make_float2(sx, sy));
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
 #ifdef SMCSD_EXPERIMENT_NO_EX2          // timing experiment only: wrong numerics
     return x * 0.5f;

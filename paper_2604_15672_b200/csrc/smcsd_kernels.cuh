@@ -159,11 +159,16 @@ __device__ __forceinline__ float load_x(const Params &prm, int model, int64_t pn
 // with s2 = sum 2^(alpha (t - m)) for PowerSMC (PW != 0), 0 otherwise.  PW = -1: general alpha,
 // a second ex2 per element; PW = k in 1..4: alpha == k, 2^(k t') = (2^t')^k by k-1 multiplies of
 // the ex2 already taken for s (no second MUFU op; keeps the power sum at the HBM roofline).
+#ifndef SMCSD_POW_POLY_K
+#define SMCSD_POW_POLY_K 2            // pairs k >= this (of 4 per 16-byte vector) on the FMA pipe
+#endif
 template <int PW>
-__device__ __forceinline__ float2 pow_acc(float2 acc, float2 e, float2 t, float alpha) {
+__device__ __forceinline__ float2 pow_acc(float2 acc, float2 e, float2 t, float alpha, bool fma_pipe = false) {
     if (PW == -1) {
+        // general alpha: a second exp per element (MUFU-bound); fma_pipe moves it to the FMA
+        // pipe (polynomial) for the caller's share of the elements
         const float2 ta = fmul2(t, make_float2(alpha, alpha));
-        return fadd2(acc, make_float2(ex2_approx(ta.x), ex2_approx(ta.y)));
+        return fadd2(acc, fma_pipe ? ex2_poly2(ta) : make_float2(ex2_approx(ta.x), ex2_approx(ta.y)));
     }
     if (PW == 1) return fadd2(acc, e);
     if (PW == 2) return ffma2(e, e, acc);
@@ -228,7 +233,7 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
             const float2 t = ffma2(z, cc, mo);
             const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
             a = fadd2(a, e);
-            if (PW) a2 = pow_acc<PW>(a2, e, t, alpha);
+            if (PW) a2 = pow_acc<PW>(a2, e, t, alpha, PW == -1 && DT == 1 && k >= SMCSD_POW_POLY_K);
         }
         acc[i] = a;
         acc2[i] = a2;
