@@ -121,8 +121,8 @@ smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     return launch_pdl_b(k_rowstats<DT, PW>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
 }
 
-// K2 tail: one CTA per prompt; the per-row S2 statistics live in dynamic shared memory when
-// they fit (k_tail<true>), else in the workspace (k_tail<false>).
+// K2 tail: one CTA per 32 (particle, position) pairs of each prompt (k_tail), or one CTA per
+// prompt with the rows' statistics in the workspace for N > kTailMaxN (k_tail_large).
 // One-time (per device) opt-in to the dynamic shared memory the K2 kernels stage through.
 smcsd_rc ensure_tail_attrs() {
     static bool attr_set[64] = {false};

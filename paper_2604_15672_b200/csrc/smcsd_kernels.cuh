@@ -1,14 +1,19 @@
 // smcsd_kernels.cuh -- the sm_100a kernels of libsmcsd.
 //
-//  K1  k_rowstats<DT>       S1: per (logit row, fixed 8192-element segment) work item, one
-//                            streaming pass: m = max t, s = sum 2^(t - m), x = t_d, with
-//                            t = inv_temp * z * log2(e)  (Eq. 1a).
-//                            Persistent CTAs over contiguous item ranges, 16-byte streaming
-//                            loads with a one-item register prefetch.
-//  K2  k_tail                one CTA per prompt, PDL-launched behind K1: S2 merge segments in
-//                            fixed order -> ell, S3 reweight, S4 fp64 normalise + ESS, S5-S7
-//                            systematic resampling from Philox, reset.
-//  K3  k_kv_reindex          S8/S9 source-major bitwise gather of per-particle blocks.
+//  K1  k_rowstats<DT, PW>    S1: per (logit row, fixed 8192-element segment) work item, one
+//                            streaming pass: m = max t, s = sum 2^(t - m) (PowerSMC: and
+//                            s2 = sum 2^(alpha (t - m))), t = inv_temp * z * log2(e)
+//                            (Eq. 1a).  Persistent warp-specialised
+//                            CTAs: a producer warp streams items into a 2-stage shared-memory
+//                            ring with cp.async.bulk (TMA), 8 consumer warps reduce them.
+//  K2  k_tail                PDL-launched behind K1, one CTA per 32 (particle, position) pairs
+//                            of a prompt: S2 merge segments in fixed order -> ell and the S3
+//                            terms; the prompt's last CTA (completion counter) runs S3, S4 fp64
+//                            normalise + ESS, S5-S7 resampling from Philox, reset.  Bonus-token
+//                            CTAs (NEXT #2) in the same grid.
+//  K3  k_kv_reindex          S8/S9 source-major bitwise gather of per-particle blocks of up to
+//                            256 state tensors.
+//  and k_merge_rows / k_tail_large / k_resample / k_power_tail / k_select / k_paged_* (see each).
 //
 // Determinism (reading G17): every row uses the same segment boundaries and the same
 // element->thread->warp->segment reduction order, so bitwise-equal p and q rows give
