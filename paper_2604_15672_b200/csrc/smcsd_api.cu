@@ -103,7 +103,7 @@ smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaSt
 }
 
 // K1 persistent grid: SMs x resident CTAs (shared-memory ring), capped by the work items.
-template <int DT, int PW>
+template <int DT, int PW, bool XP = false>
 smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     static int ctas[64] = {0};
     int dev = 0;
@@ -111,14 +111,14 @@ smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     const size_t smem = rowstats_smem_bytes<DT>();
     if (ctas[dev] == 0) {
         int occ = 0, sms = 0;
-        if (cudaFuncSetAttribute(k_rowstats<DT, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT, PW>, kK1Threads, smem) != cudaSuccess ||
+        if (cudaFuncSetAttribute(k_rowstats<DT, PW, XP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT, PW, XP>, kK1Threads, smem) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || occ < 1)
             return SMCSD_ECUDA;
         ctas[dev] = occ * sms;
     }
     const int64_t grid = items < ctas[dev] ? items : ctas[dev];
-    return launch_pdl_b(k_rowstats<DT, PW>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
+    return launch_pdl_b(k_rowstats<DT, PW, XP>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
 }
 
 // K2 tail: one CTA per 32 (particle, position) pairs of each prompt (k_tail), or one CTA per
@@ -156,6 +156,9 @@ smcsd_rc launch_rowstats_pw(const Params &prm, int dtype, int64_t items, cudaStr
 // 1..4 taken by repeated multiplication of the first sum's ex2 (see pow_term).
 smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st,
                          bool power = false) {
+    if (prm.xpeer)                                             // S10 fused exchange
+        return dtype == SMCSD_BF16 ? launch_rowstats_dt<1, 0, true>(prm, items, st)
+                                   : launch_rowstats_dt<0, 0, true>(prm, items, st);
     if (!power) return launch_rowstats_pw<0>(prm, dtype, items, st);
     const float a = prm.alpha_f;
     if (a == 1.0f) return launch_rowstats_pw<1>(prm, dtype, items, st);

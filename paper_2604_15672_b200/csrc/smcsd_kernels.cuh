@@ -266,6 +266,8 @@ struct ItemInfo {
     int nv;                 // valid elements in the segment
     float c;                // inv_temp * log2(e) of the row's model
     int valid;              // row is read (j < k_n)
+    int64_t tok;            // index of the row's drafted token in tokens[] (weight rows), else -1
+    int64_t v0;             // first column of the segment (shard-local)
 };
 
 template <int DT>
@@ -282,6 +284,8 @@ __device__ __forceinline__ ItemInfo item_info(const Params &prm, long long item)
         f.seg = prm.lp + (((int64_t)pn * prm.rpp_p + (f.valid ? kn : 0)) * prm.ld_p + v0) * kEsz0;
         f.nv = (int)min((int64_t)kSeg, prm.v_len - v0);
         f.c = prm.c_p;
+        f.tok = -1;
+        f.v0 = v0;
         return f;
     }
     const unsigned u = (unsigned)item;                      // total < 2^31 (validated)
@@ -302,6 +306,8 @@ __device__ __forceinline__ ItemInfo item_info(const Params &prm, long long item)
     f.seg = row_ptr + v0 * kEsz;
     f.nv = (int)min((int64_t)kSeg, prm.v_len - v0);
     f.c = model == 0 ? prm.c_p : prm.c_q;
+    f.tok = pn * prm.K + j;
+    f.v0 = v0;
     return f;
 }
 
@@ -347,6 +353,7 @@ struct StageMeta {
     int nv;                 // valid elements in the segment
     float c;                // inv_temp * log2(e) of the row's model
     int valid;              // row is read (j < k_n)
+    int dloc;               // S10 exchange: drafted token's column in this segment, else -1
 };
 
 template <int DT>
@@ -360,7 +367,9 @@ constexpr size_t rowstats_smem_bytes() {
 template <int DT, int PW>
 constexpr int k1_min_blocks() { return DT != 1 ? 1 : (PW == -1 || PW == 3) ? SMCSD_K1_MINB - 1 : SMCSD_K1_MINB; }
 
-template <int DT, int PW>
+// XP: the S10 fused-exchange variant (smcsd_tp_step), a separate instance so that the plain
+// kernel carries none of its code.
+template <int DT, int PW, bool XP = false>
 __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstats(const __grid_constant__ Params prm) {
     using T = ItemTraits<DT>;
     constexpr uint32_t kStageBytes = (uint32_t)kSeg * T::kEsz;
@@ -405,6 +414,7 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                 m.valid = 0;
                 m.nv = 0;
                 m.c = 0.0f;
+                m.dloc = -1;
                 const char *src = nullptr;
                 if (item < total) {
                     const ItemInfo f = item_info<DT>(prm, item);
@@ -412,6 +422,12 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                     m.nv = f.nv;
                     m.c = f.c;
                     src = f.seg;
+                    if (XP && f.valid && f.tok >= 0) {
+                        // S10: x = t_d comes from the staged segment; locate d here, off the
+                        // consumers' slot-release path
+                        const int64_t dl = (int64_t)prm.tokens[f.tok] - prm.v_begin - f.v0;
+                        m.dloc = dl >= 0 && dl < f.nv ? (int)dl : -1;
+                    }
                 }
                 meta[s] = m;
                 if (m.valid) {
@@ -472,21 +488,16 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                     }
                     out = make_float4(M, t, -INFINITY, t2);
                 }
-                if (prm.xpeer) {
+                if (XP) {
                     // S10 fused exchange: x = t_d when the drafted token is in this segment
                     // (taken from the staged segment), then one 16-byte store per rank
                     const unsigned row = fastdiv((unsigned)m.item, prm.mg_nseg, prm.sh_nseg);
                     const int sg = (int)((unsigned)m.item - row * (unsigned)prm.nseg);
-                    if (m.valid) {
-                        const int64_t d = prm.tokens[(int64_t)row % ((int64_t)prm.N * prm.K) +
-                                                     (int64_t)(row / (2u * prm.N * prm.K)) * prm.N * prm.K];
-                        const int64_t loc = d - prm.v_begin - (int64_t)sg * kSeg;
-                        if (loc >= 0 && loc < m.nv) {
-                            const char *sl = smem + (size_t)s * kStageBytes;
-                            const float z = DT == 1 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(sl)[loc] << 16)
-                                                    : reinterpret_cast<const float *>(sl)[loc];
-                            out.z = z * m.c;
-                        }
+                    if (m.valid && m.dloc >= 0) {
+                        const char *sl = smem + (size_t)s * kStageBytes;
+                        const float z = DT == 1 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t *>(sl)[m.dloc] << 16)
+                                                : reinterpret_cast<const float *>(sl)[m.dloc];
+                        out.z = z * m.c;
                     }
                     if (lane < prm.xG) {
                         float4 *dst = x_parts(prm.xpeer[lane], 2 * prm.P * prm.N * prm.K, prm.xG, prm.xnseg, prm.xepoch);
@@ -503,7 +514,7 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
         }
     }
     if (tid == 0) SMCSD_TRACE_AT(1024 + (blockIdx.x & 1023));    // K1 CTA done
-    if (prm.xpeer) {
+    if (XP) {
         // every pushed partial is visible system-wide before this CTA counts as done; the last
         // CTA then publishes the epoch in every rank's flags (release, system scope)
         __threadfence_system();

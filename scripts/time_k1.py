@@ -10,6 +10,17 @@ import synth
 dev = torch.device("cuda")
 which = os.environ.get("WHICH", "cfg4,cfg2,cfg5,power").split(",")
 
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    _h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    def _clk():
+        return (pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_SM), pynvml.nvmlDeviceGetClockInfo(_h, pynvml.NVML_CLOCK_MEM),
+                hex(pynvml.nvmlDeviceGetCurrentClocksEventReasons(_h)))
+except Exception:
+    _clk = lambda: None
+
+
 def t(fn, reps, warm=3):
     for i in range(warm): fn(i)
     torch.cuda.synchronize()
@@ -48,6 +59,15 @@ if "n64" in which:
     ms = t(lambda i: smc.smcsd_step(*ring[i % 3], V=128256, step=i, out=out, fields=(), workspace=ws), 30)
     res["N64-step"] = (ms, 262668288 / ms / 1e6)
     del ring; torch.cuda.empty_cache()
+if "tp" in which:
+    # S10 fused exchange at G = 1 (smcsd_tp_step: K1 pushes partials, tail waits on the flag)
+    from paper_2604_15672_b200.dist import TPExchange
+    lp, lq, tok = synth.lm_logits(1, 64, 8, 128256, device=dev, seed=5)
+    ex = TPExchange.local_group(1, 64, 8, 128256, 1, device=dev)[0]
+    ws = smc.Workspace(dev); out = smc.Outputs()
+    ms = t(lambda i: ex.step(lp, lq, tok, step=i, out=out, fields=(), workspace=ws), 30)
+    res["tp-fused-G1"] = (ms, 262668288 / ms / 1e6)
+    del lp, lq, tok; torch.cuda.empty_cache()
 if "power" in which:
     PP = int(os.environ.get("POWER_P", "64"))
     lg, _, _ = synth.lm_logits(PP, 32, 1, 128256, device=dev, seed=6, bonus=False)
@@ -57,4 +77,4 @@ if "power" in which:
         res[f"power-P{PP}-a{al}"] = (ms, PP * 32 * 128256 * 2 / ms / 1e6)
     del lg; torch.cuda.empty_cache()
 for k, (ms, gbs) in res.items():
-    print(f"{os.path.basename(smc.lib_path):24s} {k:16s} {ms * 1e3:9.2f} us  {gbs:8.1f} GB/s  ({gbs / 6543.7:.3f} of measured)")
+    print(f"{os.path.basename(smc.lib_path):24s} {k:16s} {ms * 1e3:9.2f} us  {gbs:8.1f} GB/s  ({gbs / 6543.7:.3f} of measured)  clk {_clk()}")
