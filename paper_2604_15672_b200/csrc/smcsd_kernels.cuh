@@ -384,6 +384,9 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
 
     if (tid == 0) {
         SMCSD_TRACE_AT(blockIdx.x & 1023);                      // K1 CTA start
+#ifdef SMCSD_TRACE
+        { unsigned smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid)); g_trace[3072 + (blockIdx.x & 1023)] = smid; }
+#endif
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kWarps);
