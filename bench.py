@@ -506,6 +506,23 @@ def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
            "partial_ms": round(part_ms, 4), "exchange_ms": round(phases[1] / steps, 4),
            "combine_resample_ms": round(phases[2] / steps, 4), "bytes_per_rank": int(byts),
            "partial_achieved_gbs": round(gbs, 1), "partial_frac_of_measured": round(gbs / hbm_peak, 4)}
+    # S10 in the north star's all-reduce form: all_reduce(MAX) of {m, x}, smcsd_partials_rescale,
+    # all_reduce(SUM) of the rescaled sums, combine with G = 1
+    from paper_2604_15672_b200.dist import exchange_partials_allreduce
+    oa = smc.Outputs(logw=torch.empty_like(logw))
+
+    def fna(i):
+        smc.smcsd_weights_partial(sp, sq, tok, v_begin=b, v_len=w, partials=part, workspace=ws_p)
+        if world > 1:
+            merged = exchange_partials_allreduce(part)
+        else:
+            merged = smc.smcsd_partials_rescale(part, part.clone()).unsqueeze(0)
+        smc.smcsd_weights_combine(merged, tok, V=V, logw_prev=logw, out=oa, fields=(), workspace=ws_c)
+        smc.smcsd_resample(oa.logw, eta=math.inf, step=i, out=orr, fields=())
+    msa = _time_steps(fna, steps, warmup, world, dev)
+    res["allreduce_exchange"] = {"ms_per_step": round(msa, 4), "steps_per_s": round(1e3 / msa, 1),
+                                 "path": "partial -> all_reduce(MAX) -> smcsd_partials_rescale -> "
+                                         "all_reduce(SUM) -> combine (G = 1) -> resample"}
     # S10 fused into K1 (smcsd_tp_step): partials pushed to every rank's exchange buffer over
     # peer memory, epoch flags, tail merges in rank order -- 2 launches, no collective call
     try:

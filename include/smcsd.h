@@ -182,6 +182,20 @@ SMCSD_API smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int
                                uint32_t *status, void *workspace, size_t workspace_bytes,
                                void *stream);
 
+/* S10 in the all-reduce form of the north star ("NCCL over NVLink all-reduces the per-row
+ * max/sum-exp"), the alternative to the rank-ordered all-gather above:
+ *   1. smcsd_weights_partial on each rank -> partials [rows][4] {m, s, x, 0};
+ *   2. all_reduce(MAX) of a copy of the partials -> max_partials (fields 0 and 2 used: M, X);
+ *   3. this call: out[r] = {M_r, s_r 2^(m_r - M_r), X_r, 0} (rows = 2 P N K; device, 16-byte
+ *      aligned; out may alias partials);
+ *   4. all_reduce(SUM) of field 1 of out across ranks -> {M, S, X} per row;
+ *   5. smcsd_weights_combine with G = 1.
+ * Every rank ends with the same weights (the collectives give every rank the same values) but
+ * S is summed in NCCL's order, not rank order, so it need not be bit-identical to the
+ * unsharded result (the all-gather path is).  Enqueued on stream; EINVAL on null/misaligned. */
+SMCSD_API smcsd_rc smcsd_partials_rescale(const float *partials, const float *max_partials, float *out,
+                                          int64_t rows, void *stream);
+
 /* S8/S9: reindex per-particle state blocks (dense analogue of the paged
  * pointer copy of PAPER.md:489).  Block (o, p, n), o < n_outer (e.g. L*2 layer K/V planes),
  * is seg_count segments of seg_bytes bytes at

@@ -21,7 +21,7 @@ __all__ = [
     "SmcsdError", "Workspace", "StepPlan", "lib_path",
     "smcsd_workspace_bytes", "smcsd_workspace_init", "smcsd_weights", "smcsd_step",
     "smcsd_resample", "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
-    "smcsd_kv_reindex_multi", "kv_tensor",
+    "smcsd_kv_reindex_multi", "kv_tensor", "smcsd_partials_rescale",
     "smcsd_version", "kv_geometry", "smcsd_select", "smcsd_kv_reindex_paged", "ST_BAD_PAGE",
     "smcsd_powersmc_weights", "smcsd_tp_exchange_bytes", "smcsd_tp_exchange_init",
     "smcsd_ipc_handle_bytes", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close", "smcsd_tp_step",
@@ -76,6 +76,7 @@ def _load():
                                         vp, vp, vp, vp, vp, sz, vp]
     L.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
     L.smcsd_kv_reindex_multi.argtypes = [ctypes.POINTER(_KvTensor), i32, vp, i32, i32, vp]
+    L.smcsd_partials_rescale.argtypes = [vp, vp, vp, i64, vp]
     L.smcsd_select.argtypes = [vp, i32, i32, i64, u64, u64, vp, vp, vp, vp, sz, vp]
     L.smcsd_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
     L.smcsd_powersmc_weights.argtypes = [vp, i64, i32, i32, vp, i32, i32, i64, f32, f32, vp, vp,
@@ -95,7 +96,7 @@ def _load():
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     for name in ("smcsd_workspace_init", "smcsd_weights", "smcsd_resample", "smcsd_step",
                  "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
-                 "smcsd_kv_reindex_multi", "smcsd_select", "smcsd_kv_reindex_paged", "smcsd_powersmc_weights",
+                 "smcsd_kv_reindex_multi", "smcsd_partials_rescale", "smcsd_select", "smcsd_kv_reindex_paged", "smcsd_powersmc_weights",
                  "smcsd_tp_exchange_init", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close",
                  "smcsd_tp_step"):
         getattr(L, name).restype = i32
@@ -506,6 +507,16 @@ def kv_geometry(kv: torch.Tensor, seq_len: int | None = None) -> dict:
     return dict(n_outer=L * C, outer_stride=P * N * H * S * d * e, prompt_stride=N * H * S * d * e,
                 particle_stride=H * S * d * e, seg_count=H, seg_bytes=seq_len * d * e,
                 seg_stride=S * d * e)
+
+
+def smcsd_partials_rescale(partials, max_partials, out=None, *, stream=None):
+    """S10 all-reduce form, step 3: {M, s 2^(m - M), X, 0} per row from this rank's partials
+    [..., 4] and their all_reduce(MAX) (see include/smcsd.h)."""
+    out = torch.empty_like(partials) if out is None else out
+    rows = partials.numel() // 4
+    _check("smcsd_partials_rescale", _lib.smcsd_partials_rescale(_p(partials), _p(max_partials), _p(out),
+                                                                 rows, _stream(stream)))
+    return out
 
 
 def kv_tensor(dst, src, *, n_outer, outer_stride, prompt_stride, particle_stride, seg_count,

@@ -372,6 +372,17 @@ smcsd_rc smcsd_weights_combine(const float *gathered, int G, const int32_t *toke
     return launch_tail(prm, 0, as_stream(stream));
 }
 
+smcsd_rc smcsd_partials_rescale(const float *partials, const float *max_partials, float *out,
+                                int64_t rows, void *stream) {
+    if (!partials || !max_partials || !out || rows < 1) return SMCSD_EINVAL;
+    if (!aligned16(partials) || !aligned16(max_partials) || !aligned16(out)) return SMCSD_EINVAL;
+    const int64_t grid = std::min<int64_t>(cdiv(rows, kThreads), 4 * 148);
+    k_partials_rescale<<<(unsigned)grid, kThreads, 0, as_stream(stream)>>>(
+        reinterpret_cast<const float4 *>(partials), reinterpret_cast<const float4 *>(max_partials),
+        reinterpret_cast<float4 *>(out), rows);
+    return cudaGetLastError() == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
+}
+
 smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
                                 const int32_t *src_index, int P, int N, void *stream) {
     if (!tensors || !src_index || n_tensors < 1 || n_tensors > kMaxKvTensors) return SMCSD_EINVAL;

@@ -1517,6 +1517,21 @@ __global__ void __launch_bounds__(kThreads) k_power_tail(const __grid_constant__
     pdl_trigger();
 }
 
+// S10, all-reduce form (the north star's literal "NCCL all-reduces the per-row max/sum-exp"):
+// between all_reduce(MAX) of {m, s, x, 0} (only m and x are used) and all_reduce(SUM) of the
+// rescaled sums, each rank maps its local row sum to the global max:
+//   s'_r = s_r 2^(m_r - M_r)   (s_r when m_r == M_r; 0 when s_r == 0; NaN propagates)
+// and writes {M_r, s'_r, X_r, 0} so that after the SUM of field 1 across ranks the row holds the
+// merged {M, S, X} that smcsd_weights_combine takes with G = 1.
+__global__ void __launch_bounds__(kThreads) k_partials_rescale(const float4 *local, const float4 *mx,
+                                                              float4 *out, int64_t rows) {
+    for (int64_t r = (int64_t)blockIdx.x * kThreads + threadIdx.x; r < rows; r += (int64_t)gridDim.x * kThreads) {
+        const float4 l = local[r], g = mx[r];
+        const float sc = l.y == 0.0f ? 0.0f : __fmul_rn(l.y, l.x == g.x ? 1.0f : ex2_approx(l.x - g.x));
+        out[r] = make_float4(g.x, sc, g.z, 0.0f);
+    }
+}
+
 // Exchange-buffer init: flags 0, every partial slot neutral {-inf, 0, -inf, 0}.
 __global__ void k_xinit(char *base, size_t n_parts) {
     if (blockIdx.x == 0 && threadIdx.x < kXFlagBytes / 4) reinterpret_cast<uint32_t *>(base)[threadIdx.x] = 0u;

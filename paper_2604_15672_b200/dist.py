@@ -57,6 +57,35 @@ def exchange_partials_into(out: torch.Tensor, partials: torch.Tensor, group=None
     out.copy_(torch.stack(bufs))
 
 
+def _all_reduce(t: torch.Tensor, op, group=None) -> None:
+    """In-place all-reduce (NCCL on device; gloo stages through host memory -- tests only)."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, op=op, group=group)
+        return
+    host = t.detach().cpu().contiguous()
+    dist.all_reduce(host, op=op, group=group)
+    t.copy_(host)
+
+
+def exchange_partials_allreduce(partials: torch.Tensor, group=None, rescale=None) -> torch.Tensor:
+    """S10 in the north star's all-reduce form (include/smcsd.h, smcsd_partials_rescale):
+    all_reduce(MAX) of the partials {m, s, x, 0} (m and x used), this rank's sums rescaled to
+    the global max by our kernel, all_reduce(SUM) of the rescaled sums.  Returns [1][...][4]
+    merged rows {M, S, X, 0} for smcsd_weights_combine with G = 1 -- identical on every rank,
+    but S summed in NCCL's order (the all-gather path merges in rank order instead).
+    rescale: the step-3 function (default: the CUDA kernel; CPU tests pass a reference)."""
+    if rescale is None:
+        import paper_2604_15672_b200 as smc
+        rescale = smc.smcsd_partials_rescale
+    mx = partials.clone()
+    _all_reduce(mx, dist.ReduceOp.MAX, group)
+    out = rescale(partials, mx)
+    s = out[..., 1].contiguous()
+    _all_reduce(s, dist.ReduceOp.SUM, group)
+    out[..., 1] = s
+    return out.unsqueeze(0)
+
+
 def max_over_ranks(value: float, device, group=None) -> float:
     """Max of a host float over ranks (timing: the slowest rank sets the step time)."""
     if not dist.is_initialized() or dist.get_world_size(group) == 1:
@@ -69,14 +98,16 @@ def max_over_ranks(value: float, device, group=None) -> float:
 
 
 def tp_weights(logits_p_shard, logits_q_shard, tokens, *, V, v_begin, v_len, group=None, **kw):
-    """Tensor-parallel S1-S4: partial on this rank's shard, gather, combine (rank order)."""
+    """Tensor-parallel S1-S4: partial on this rank's shard, exchange (exchange="allgather":
+    rank-order merge, bit-identical to one GPU; "allreduce": MAX + rescale + SUM), combine."""
     import paper_2604_15672_b200 as smc
     part = smc.smcsd_weights_partial(logits_p_shard, logits_q_shard, tokens, v_begin=v_begin,
                                      v_len=v_len, n_drafted=kw.get("n_drafted"),
                                      inv_temp_p=kw.get("inv_temp_p", 1.0),
                                      inv_temp_q=kw.get("inv_temp_q", 1.0),
                                      workspace=kw.get("workspace"))
-    gathered = exchange_partials(part, group)
+    gathered = (exchange_partials_allreduce(part, group) if kw.get("exchange") == "allreduce"
+                else exchange_partials(part, group))
     return smc.smcsd_weights_combine(gathered, tokens, V=V, n_drafted=kw.get("n_drafted"),
                                      logw_prev=kw.get("logw_prev"), alpha=kw.get("alpha", 1.0),
                                      out=kw.get("out"), workspace=kw.get("workspace_combine"))

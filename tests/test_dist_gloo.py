@@ -106,6 +106,42 @@ def test_tp_vocab_exchange_gloo():
     assert res[0][1] == res[1][1]            # every rank holds the same gathered bytes
 
 
+def _tp_allreduce_job(rank, world):
+    # S10 all-reduce form (north star: "all-reduces the per-row max/sum-exp"): MAX of {m, x},
+    # rescale to the global max (a CPU reference of smcsd_partials_rescale, natural-log units as
+    # the oracle's partials), SUM of s; the merged row gives the unsharded log-prob
+    import oracle
+    from paper_2604_15672_b200.dist import exchange_partials_allreduce
+    oracle.build()
+    rng = np.random.default_rng(9)
+    V, rows = 1000, 6
+    z = (rng.standard_normal((rows, V)) * 3).astype(np.float32)
+    d = rng.integers(0, V, rows)
+    b, e = vocab_shard(V, world, rank)
+    p3 = np.stack([oracle.row_partial(z[r, b:e], b, int(d[r]))[0] for r in range(rows)])
+    part = torch.from_numpy(np.concatenate([p3, np.zeros((rows, 1))], axis=1))   # {m, s, x, 0}
+
+    def rescale_ref(local, mx):
+        out = mx.clone()
+        s = local[:, 1] * torch.exp(local[:, 0] - mx[:, 0])
+        out[:, 1] = torch.where(local[:, 1] == 0, torch.zeros_like(s), s)
+        out[:, 3] = 0
+        return out
+    merged = exchange_partials_allreduce(part, rescale=rescale_ref).numpy()       # [1][rows][4]
+    ok = True
+    for r in range(rows):
+        ell, flag = oracle.combine_partials(merged[:, r, :3])
+        ref, _ = oracle.row_logprob(z[r], int(d[r]))
+        ok &= flag == 0 and abs(ell - ref) <= 1e-12
+    return bool(ok), merged.tobytes()
+
+
+def test_tp_vocab_allreduce_gloo():
+    res = _run(_tp_allreduce_job)
+    assert res[0][0] and res[1][0]
+    assert res[0][1] == res[1][1]            # every rank holds the same merged rows
+
+
 def _handles_fn(rank, world):
     # S10 fused path plumbing: every rank's (fake) IPC handle reaches every rank in rank order,
     # and the peer table keeps our own buffer and opens only the peers'

@@ -303,6 +303,17 @@ def test_tp_vocab_sharded_simulated(smc, orc, G):
     ref = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V)
     assert max_abs(np_(c1.logw), ref["logw"]) <= TOL_LOGW
     assert np.array_equal(np_(c1.status).astype(np.uint32), ref["status"])
+    # S10 all-reduce form (north-star literal): MAX over ranks (emulated by a stack max),
+    # smcsd_partials_rescale on every rank, SUM over ranks, combine with G = 1
+    mx = gathered.amax(dim=0)
+    resc = [smc.smcsd_partials_rescale(parts[g], mx) for g in range(G)]
+    merged = resc[0].clone()
+    merged[..., 1] = torch.stack([r[..., 1] for r in resc]).sum(dim=0)
+    assert all(torch.equal(r[..., 0], mx[..., 0]) and torch.equal(r[..., 2], mx[..., 2]) for r in resc)
+    c3 = smc.smcsd_weights_combine(merged.unsqueeze(0).contiguous(), tokd, V=V)
+    assert (c3.logw - c1.logw).abs().max().item() <= 1e-5
+    assert max_abs(np_(c3.logw), ref["logw"]) <= TOL_LOGW
+    assert np.array_equal(np_(c3.status).astype(np.uint32), ref["status"])
 
 
 # ----------------------------------------------------------------------------- KV (S8/S9)
