@@ -643,21 +643,25 @@ def run_e2e(wl, args, dev, world):
     steps = max(3, min(args.steps, 50))
     base = args.warmup + args.steps
     comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
-    h2d_done = [torch.cuda.Event() for _ in range(2)]
+    n_copy = int(os.environ.get("SMCSD_E2E_COPY_STREAMS", "2"))
+    copies = [torch.cuda.Stream(dev) for _ in range(n_copy)]    # one copy engine each
+    h2d_done = [[torch.cuda.Event() for _ in range(n_copy)] for _ in range(2)]
     used = [torch.cuda.Event() for _ in range(2)]
 
     def h2d(i):
         b = i % 2
-        copy.wait_event(used[b])                              # buffer b free again
-        with torch.cuda.stream(copy):
-            for s_, t in zip(stages[b], host[i % len(host)]):
-                s_.copy_(t, non_blocking=True)
-            h2d_done[b].record(copy)
+        for k, cs in enumerate(copies):                       # lp | lq + tokens
+            cs.wait_event(used[b])                            # buffer b free again
+            with torch.cuda.stream(cs):
+                for j, (s_, t) in enumerate(zip(stages[b], host[i % len(host)])):
+                    if min(j, n_copy - 1) == k:
+                        s_.copy_(t, non_blocking=True)
+                h2d_done[b][k].record(cs)
 
     def compute(i):
         b = i % 2
-        comp.wait_event(h2d_done[b])
+        for ev in h2d_done[b]:
+            comp.wait_event(ev)
         wl.logw.copy_(prior_h, non_blocking=True)
         wl.step(base + (i % 4), inputs=stages[b])
         used[b].record(comp)
@@ -666,7 +670,8 @@ def run_e2e(wl, args, dev, world):
 
     def run(n, t_start=None):
         if t_start is not None:
-            copy.wait_event(t_start)                          # step 0's copy inside the region
+            for cs in copies:
+                cs.wait_event(t_start)                        # step 0's copy inside the region
         h2d(0)
         for i in range(n):
             if i + 1 < n:
@@ -691,7 +696,8 @@ def run_e2e(wl, args, dev, world):
     return {"value": round(world * wl.P * steps / (ms / 1e3), 3), "unit": "steps/s",
             "h2d_bytes_per_step": int(h2d_b), "d2h_bytes_per_step": int(d2h),
             "steps": steps, "wall_s": round(wall, 4),
-            "note": "inputs H2D on a copy stream, double-buffered (step i+1's copy overlaps step i)"}
+            "note": f"inputs H2D on {n_copy} copy stream(s), double-buffered (step i+1's copy "
+                    "overlaps step i)"}
 
 
 # ------------------------------------------------------------------------------ CPU legs
