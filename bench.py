@@ -643,7 +643,7 @@ def run_e2e(wl, args, dev, world):
     steps = max(3, min(args.steps, 50))
     base = args.warmup + args.steps
     comp = torch.cuda.current_stream(dev)
-    n_copy = int(os.environ.get("SMCSD_E2E_COPY_STREAMS", "2"))
+    n_copy = int(os.environ.get("SMCSD_E2E_COPY_STREAMS", "1"))
     copies = [torch.cuda.Stream(dev) for _ in range(n_copy)]    # one copy engine each
     h2d_done = [[torch.cuda.Event() for _ in range(n_copy)] for _ in range(2)]
     used = [torch.cuda.Event() for _ in range(2)]
