@@ -8,7 +8,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SMCSD_LIB_OVERRIDE"] = os.path.join(ROOT, "paper_2604_15672_b200", "libsmcsd_trace.so")
+os.environ["SMCSD_LIB_OVERRIDE"] = os.environ.get("TRACE_LIB") or os.path.join(ROOT, "paper_2604_15672_b200", "libsmcsd_trace.so")
 import torch  # noqa: E402
 import paper_2604_15672_b200 as smc  # noqa: E402
 import synth  # noqa: E402
