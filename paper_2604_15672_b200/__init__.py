@@ -301,7 +301,9 @@ class StepPlan:
     """smcsd_step with its argument list prepared once (plumbing for tight decode loops: the
     binding's per-call validation and marshalling cost ~25 us of host time, more than a cfg2
     step on the GPU).  run() swaps in new logits / tokens of the SAME shape, dtype and device
-    and the step counter, then makes the one C call.  Outputs land in plan.out."""
+    and the step counter, then makes the one C call.  Outputs land in plan.out.  Everything
+    else -- output buffers, workspace, scalars and the CUDA stream (the current one at
+    construction unless stream= is given) -- is fixed at construction."""
     _I_LP, _I_LQ, _I_TOK, _I_STEP = 0, 3, 7, 20
 
     def __init__(self, logits_p, logits_q, tokens, **kw):

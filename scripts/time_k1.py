@@ -59,6 +59,15 @@ if "n64" in which:
     ms = t(lambda i: smc.smcsd_step(*ring[i % 3], V=128256, step=i, out=out, fields=(), workspace=ws), 30)
     res["N64-step"] = (ms, 262668288 / ms / 1e6)
     del ring; torch.cuda.empty_cache()
+if "fp32" in which:
+    # cfg2 / cfg4 shapes with fp32 logits (2x the bytes of bf16)
+    for nm, P_ in (("fp32-cfg2", 1), ("fp32-cfg4", 16)):
+        lp, lq, tok = synth.lm_logits(P_, 32 if P_ > 1 else 16, 8, 128256, dtype=torch.float32, device=dev, seed=8)
+        ws = smc.Workspace(dev); out = smc.Outputs()
+        ms = t(lambda i: smc.smcsd_step(lp, lq, tok, V=128256, step=i, out=out, fields=(), workspace=ws), 10)
+        byts = 2 * lp.shape[0] * lp.shape[1] * 8 * 128256 * 4
+        res[nm] = (ms, byts / ms / 1e6)
+        del lp, lq, tok; torch.cuda.empty_cache()
 if "tp" in which:
     # S10 fused exchange at G = 1 (smcsd_tp_step: K1 pushes partials, tail waits on the flag)
     from paper_2604_15672_b200.dist import TPExchange
