@@ -295,12 +295,22 @@ def run_ours(args, rank, world, local):
         del wl.kv
         wl.kv = None
         torch.cuda.empty_cache()
-        secondary["cfg4"] = measure_cfg4(dev, rank, world, hbm_peak)
-        secondary["cfg5"] = measure_cfg5(dev, rank, world, hbm_peak)
+        # Each secondary measurement starts after a short idle (the GPU's power controller caps
+        # sustained compute-heavy streams at ~1000 W / ~1620 MHz -- DESIGN.md section 8b) and
+        # records the SM clock and clock-event reasons seen during it.
+        def settled(fn, *a):
+            barrier(world)
+            time.sleep(args.settle_s)
+            with ClockSampler(dev.index if dev.index is not None else 0) as cs:
+                r = fn(*a)
+            r["clocks"] = cs.summary()
+            return r
+        secondary["cfg4"] = settled(measure_cfg4, dev, rank, world, hbm_peak)
+        secondary["cfg5"] = settled(measure_cfg5, dev, rank, world, hbm_peak)
         if world == 1:
-            secondary["cfg3"] = measure_cfg3(dev, hbm_peak)
-            secondary["cfg2_verify"] = measure_cfg2_verify(dev, hbm_peak)
-            secondary["powersmc"] = measure_power(dev, hbm_peak)
+            secondary["cfg3"] = settled(measure_cfg3, dev, hbm_peak)
+            secondary["cfg2_verify"] = settled(measure_cfg2_verify, dev, hbm_peak)
+            secondary["powersmc"] = settled(measure_power, dev, hbm_peak)
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
@@ -380,6 +390,7 @@ def measure_cfg4(dev, rank, world, hbm_peak, steps=20, warmup=3):
     # NEXT #2: the same step plus the bonus token (target row K streamed in K1, bonus CTAs)
     fnb = lambda i: smc.smcsd_step(lp, lq, tok, V=V, logw_prev=logw, eta=math.inf, step=i,
                                    prompt_base=b, out=out, fields=(), workspace=ws, bonus=True)
+    time.sleep(1.0)                                        # power-state settle (see settled())
     msb = _time_steps(fnb, steps, warmup, world, dev)
     bytb = byts + P * N * V * 2
     gbb = bytb / (msb / 1e3) / 1e9
@@ -790,6 +801,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--settle-s", type=float, default=1.0,
+                    help="idle seconds before each secondary measurement (power-state settle)")
     ap.add_argument("--no-secondary", action="store_true", help="skip the cfg3/cfg4 measurements")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
