@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(kThreads) k_probe(const __grid_constant__ Para
         tail_rowstats(prm, 0, rowstat, stage);
         __syncthreads();
         long long t1 = clock64();
-        tail_scores(prm, 0, rowstat, sh.e, &sh.st);
+        tail_scores(prm, 0, rowstat, sh.e, &sh.st, -INFINITY);
         __syncthreads();
         long long t2 = clock64();
         for (int n = tid; n < prm.N; n += kThreads) sh.lam[n] = -1.0f - n * 0.01f;
@@ -84,7 +84,7 @@ int main() {
     prm.parts = parts; prm.part_row_stride = nseg; prm.part_seg_stride = 1; prm.nparts = nseg;
     prm.ell_ws = ell;
     for (int launch = 0; launch < 3; ++launch) {
-        const int smem = (int)(kStageBytes + rows * 16);
+        const int smem = (int)(kTailStageBytes + rows * 16);
         CK(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         k_probe<<<1, kThreads, smem>>>(prm, clk);
         CK(cudaDeviceSynchronize());
