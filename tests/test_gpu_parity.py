@@ -673,3 +673,41 @@ def test_step_plan_matches_step(smc):
     bad = synth.lm_logits(2, 8, 4, 20050, dtype=torch.bfloat16, seed=1)      # another row pitch
     with pytest.raises(ValueError):
         plan.run(*(t.to(dev) for t in bad), step=9)
+
+
+# ------------------------------------------------------------- limits the ABI accepts
+@pytest.mark.parametrize("P,N,K,V,dtype", [(2, 1024, 2, 3000, torch.float32),    # N at kTailMaxN
+                                           (2, 8, 64, 5000, torch.bfloat16),     # K = 64 (paper max)
+                                           (1, 100, 8, 20001, torch.bfloat16)])  # N between 64 and 1024
+def test_step_at_abi_limits(smc, orc, P, N, K, V, dtype):
+    dev = torch.device("cuda")
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=dtype, sigma_d=0.5, seed=700 + N + K)
+    prev = synth.random_logw(P, N, seed=13, sigma=0.5)
+    g = torch.Generator().manual_seed(3)
+    ndr = torch.randint(0, K + 1, (P, N), generator=g, dtype=torch.int32)
+    out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, n_drafted=ndr.to(dev),
+                         logw_prev=prev.to(dev), step=4, seed=synth.PHILOX_SEED)
+    torch.cuda.synchronize()
+    ref = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, n_drafted=ndr.numpy(),
+                      logw_prev=prev.numpy())
+    assert max_abs(np_(out.logw_pre), ref["logw"]) <= TOL_LOGW
+    assert np.array_equal(np_(out.status).astype(np.uint32), ref["status"])
+    rr = orc.resample(np_(out.logw_pre), eta=np.inf, seed=synth.PHILOX_SEED, step=4)
+    assert rr["n_ties"].sum() == 0
+    assert np.array_equal(np_(out.ancestors), rr["ancestors"])
+    assert np.array_equal(np_(out.slot_src), rr["slot_src"])
+    assert np.array_equal(np_(out.offspring), rr["offspring"])
+
+
+def test_bonus_at_max_vocab(smc, orc):
+    """Bonus token at V = 2^21 (256 segments: the sampler's shared-memory limit)."""
+    dev = torch.device("cuda")
+    P, N, K, V = 1, 4, 2, 1 << 21
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=71)
+    out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, step=1, bonus=True)
+    torch.cuda.synchronize()
+    assert int(out.status.abs().sum()) == 0
+    ref = orc.bonus(to_host(lp), K=K, V=V, step=1)
+    _bonus_check(np_(out.bonus), ref)
+    w = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V)
+    assert max_abs(np_(out.logw_pre), w["logw"]) <= TOL_LOGW
