@@ -426,9 +426,37 @@ def measure_cfg2_verify(dev, hbm_peak, steps=120, warmup=6):
         fn = lambda i, plan=plan: plan.run(*ring[i % 6], step=i)
         ms = _time_steps(fn, steps, warmup, 1, dev)
         byts = 2 * N * K * V * 2 + (N * V * 2 if bonus else 0)
+        # SURVEY.md 8(d) protocol: the 6 ring steps captured in one CUDA graph, median of 7
+        # replays (no host in the loop)
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(torch.cuda.current_stream(dev))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            for i in range(6):
+                smc.smcsd_step(*ring[i], V=V, eta=math.inf, step=i, out=out, fields=(),
+                               workspace=ws, stream=gs, bonus=bonus)
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(graph, stream=gs):
+                for i in range(6):
+                    smc.smcsd_step(*ring[i], V=V, eta=math.inf, step=i, out=out, fields=(),
+                                   workspace=ws, stream=gs, bonus=bonus)
+        graph.replay()
+        torch.cuda.synchronize(dev)
+        reps = []
+        for _ in range(7):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            graph.replay()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            reps.append(e0.elapsed_time(e1) / 6)
+        gms = statistics.median(reps)
+        del graph
         res["with_bonus" if bonus else "plain"] = {
             "us_per_step": round(ms * 1e3, 2), "bytes": byts,
-            "frac_of_measured": round(byts / (ms / 1e3) / 1e9 / hbm_peak, 4)}
+            "frac_of_measured": round(byts / (ms / 1e3) / 1e9 / hbm_peak, 4),
+            "graph_us_per_step": round(gms * 1e3, 2),
+            "graph_frac_of_measured": round(byts / (gms / 1e3) / 1e9 / hbm_peak, 4)}
     del ring
     torch.cuda.empty_cache()
     return res
