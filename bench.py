@@ -326,6 +326,10 @@ def run_ours(args, rank, world, local):
             "l2": "logits ring of 6 sets (394 MB > 126 MB L2); KV 10.7 GB > L2",
             "kv_mode": "in-place slot plan", "mean_dead_slots": round(dead, 2),
             "mean_ess_over_n": round(ess_frac, 4),
+            # chi^2(p_K || q_K) of a K-token block estimated from the realised ESS: ESS/N ->
+            # 1 / (1 + chi^2), per drafted token (1 + chi^2_block)^(1/K) - 1
+            "chi2_block_est": round(1.0 / ess_frac - 1.0, 4) if ess_frac > 0 else None,
+            "chi2_token_est": round((1.0 / ess_frac) ** (1.0 / wl.K) - 1.0, 4) if ess_frac > 0 else None,
         },
         "hbm": {"algorithmic_bytes_per_step": int(step_bytes),
                 "achieved_gbs": round(step_gbs, 1),
