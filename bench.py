@@ -753,9 +753,25 @@ def run_e2e(wl, args, dev, world):
     ms = max_over_ranks(t0.elapsed_time(t1), dev)
     h2d_b = sum(t.numel() * t.element_size() for t in host[0]) + prior_h.numel() * 4
     d2h = res_w.numel() * 4 + res_a.numel() * 4
+    # the PCIe bound: the same H2D copies alone, back to back on the copy stream(s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(comp)
+    for i in range(steps):
+        for cs in copies:
+            cs.wait_event(e0)
+        h2d(i)
+    for b_ in range(2):
+        for ev in h2d_done[b_]:
+            comp.wait_event(ev)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    ms_copy = max_over_ranks(e0.elapsed_time(e1), dev)
     return {"value": round(world * wl.P * steps / (ms / 1e3), 3), "unit": "steps/s",
             "h2d_bytes_per_step": int(h2d_b), "d2h_bytes_per_step": int(d2h),
             "steps": steps, "wall_s": round(wall, 4),
+            "h2d_gbs": round(h2d_b * steps / (ms / 1e3) / 1e9, 2),
+            "h2d_copy_alone_gbs": round(h2d_b * steps / (ms_copy / 1e3) / 1e9, 2),
             "note": f"inputs H2D on {n_copy} copy stream(s), double-buffered (step i+1's copy "
                     "overlaps step i)"}
 
