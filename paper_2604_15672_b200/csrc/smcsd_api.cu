@@ -108,7 +108,7 @@ smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     static int ctas[64] = {0};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
-    const size_t smem = rowstats_smem_bytes<DT>();
+    const size_t smem = rowstats_smem_bytes<DT, XP>();
     if (ctas[dev] == 0) {
         int occ = 0, sms = 0;
         if (cudaFuncSetAttribute(k_rowstats<DT, PW, XP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
@@ -577,7 +577,7 @@ smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_per_particle
     if (!logw_out || !status || !ancestors || !resampled || !workspace || !xpeer || !xlocal)
         return SMCSD_EINVAL;
     if (N > kTailMaxN || std::isnan(eta) || v_begin < 0 || v_begin + v_len > V) return SMCSD_EINVAL;
-    if (G < 1 || G > 32 || rank < 0 || rank >= G || epoch == 0 || !aligned16(xlocal)) return SMCSD_EINVAL;
+    if (G < 1 || G > kXMaxG || rank < 0 || rank >= G || epoch == 0 || !aligned16(xlocal)) return SMCSD_EINVAL;
     if (xnseg < cdiv(v_len, kSeg) || (int64_t)G * xnseg > 4096) return SMCSD_EINVAL;
     if (!(std::isfinite(alpha) && alpha > 0.0f) || !valid_temp(inv_temp_p) || !valid_temp(inv_temp_q))
         return SMCSD_EINVAL;

@@ -106,9 +106,11 @@ __host__ __device__ inline size_t x_half_elems(int rows, int G, int xnseg) {
 __device__ __forceinline__ float4 *x_parts(char *base, int rows, int G, int xnseg, uint32_t epoch) {
     return reinterpret_cast<float4 *>(base + kXFlagBytes) + (epoch & 1u) * x_half_elems(rows, G, xnseg);
 }
-__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -356,10 +358,13 @@ struct StageMeta {
     int dloc;               // S10 exchange: drafted token's column in this segment, else -1
 };
 
-template <int DT>
+constexpr int kXMaxG = 32;                                  // S10: ranks of one exchange
+
+template <int DT, bool XP = false>
 constexpr size_t rowstats_smem_bytes() {
     return (size_t)kStages * kSeg * ItemTraits<DT>::kEsz            // data ring
-         + kStages * (2 * sizeof(uint64_t) + sizeof(StageMeta) + kWarps * sizeof(float4) + 16);
+         + kStages * (2 * sizeof(uint64_t) + sizeof(StageMeta) + kWarps * sizeof(float4) + 16)
+         + (XP ? kXMaxG * sizeof(float4 *) : 0);                     // S10: per-rank destinations
 }
 
 // bf16 path: SMCSD_K1_MINB CTAs/SM (32 registers); the general-alpha and cube power sums need
@@ -369,6 +374,14 @@ constexpr int k1_min_blocks() { return DT != 1 ? 1 : (PW == -1 || PW == 3) ? SMC
 
 // XP: the S10 fused-exchange variant (smcsd_tp_step), a separate instance so that the plain
 // kernel carries none of its code.
+// S10: the drafted token of a K1 item's row (-1 when the row has none), loaded by the producer
+// one item ahead of its use.
+template <int DT>
+__device__ __forceinline__ int xp_token(const Params &prm, long long item) {
+    const ItemInfo f = item_info<DT>(prm, item);
+    return f.valid && f.tok >= 0 ? __ldg(prm.tokens + f.tok) : -1;
+}
+
 template <int DT, int PW, bool XP = false>
 __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstats(const __grid_constant__ Params prm) {
     using T = ItemTraits<DT>;
@@ -379,6 +392,8 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
     StageMeta *meta = reinterpret_cast<StageMeta *>(empty + kStages);
     float4 *red = reinterpret_cast<float4 *>(meta + kStages);       // [kStages][kWarps]
     int *done = reinterpret_cast<int *>(red + kStages * kWarps);    // [kStages]
+    float4 **xdst = reinterpret_cast<float4 **>(done + kStages);     // [kXMaxG] (XP only)
+    static_assert(kStages % 2 == 0, "xdst must stay 8-byte aligned");
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const long long total = prm.main_items + prm.bonus_items;
 
@@ -394,6 +409,8 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
         }
         fence_mbar_init();
     }
+    if (XP && tid < prm.xG)                                 // S10: this epoch's half of each buffer
+        xdst[tid] = x_parts(prm.xpeer[tid], 2 * prm.P * prm.N * prm.K, prm.xG, prm.xnseg, prm.xepoch);
     __syncthreads();
 
     if (warp == kWarps) {
@@ -409,6 +426,8 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
             // before the first global access.  Setup above overlapped its tail.
             pdl_wait();
             long long item = blockIdx.x;
+            int xtok = -1;                                  // S10: drafted token of `item`
+            if (XP && item < total) xtok = xp_token<DT>(prm, item);
             for (long long it = 0;; ++it) {
                 const int s = (int)(it % kStages);
                 mbar_wait(&empty[s], (uint32_t)(((it / kStages) & 1) ^ 1));   // slot released
@@ -426,9 +445,9 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                     m.c = f.c;
                     src = f.seg;
                     if (XP && f.valid && f.tok >= 0) {
-                        // S10: x = t_d comes from the staged segment; locate d here, off the
-                        // consumers' slot-release path
-                        const int64_t dl = (int64_t)prm.tokens[f.tok] - prm.v_begin - f.v0;
+                        // S10: x = t_d comes from the staged segment; d was loaded one
+                        // iteration ahead (xtok), so no dependent load delays the TMA issue
+                        const int64_t dl = (int64_t)xtok - prm.v_begin - f.v0;
                         m.dloc = dl >= 0 && dl < f.nv ? (int)dl : -1;
                     }
                 }
@@ -442,6 +461,7 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                 }
                 if (item >= total) break;
                 item = (long long)gridDim.x + atomicAdd(prm.work_ctr, 1u);
+                if (XP && item < total) xtok = xp_token<DT>(prm, item);   // used after the next wait
             }
         }
     } else {
@@ -503,8 +523,7 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                         out.z = z * m.c;
                     }
                     if (lane < prm.xG) {
-                        float4 *dst = x_parts(prm.xpeer[lane], 2 * prm.P * prm.N * prm.K, prm.xG, prm.xnseg, prm.xepoch);
-                        dst[(size_t)row * prm.xG * prm.xnseg + prm.xrank * prm.xnseg + sg] = out;
+                        xdst[lane][(size_t)row * prm.xG * prm.xnseg + prm.xrank * prm.xnseg + sg] = out;
                     }
                     if (lane == 0) done[s] = 0;
                 } else if (lane == 0) {
@@ -518,18 +537,29 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
     }
     if (tid == 0) SMCSD_TRACE_AT(1024 + (blockIdx.x & 1023));    // K1 CTA done
     if (XP) {
-        // every pushed partial is visible system-wide before this CTA counts as done; the last
-        // CTA then publishes the epoch in every rank's flags (release, system scope)
-        __threadfence_system();
+        // the tail may be scheduled now: its griddepcontrol.wait still waits for this whole
+        // grid (flags included), so only its launch overlaps the fences below
+        pdl_trigger();
+        // Release chain (PTX memory model): the CTA barrier orders every thread's pushes before
+        // thread 0's gpu-scope release fence + count; the CTA that completes the count
+        // acquires it and its one system-scope fence is cumulative over all of them, so the
+        // relaxed system-scope flag stores after it publish every rank's pushes (the tail
+        // reads the flags with ld.acquire.sys).  One fence per CTA at gpu scope and one at
+        // system scope per launch: a system fence in every thread cost ~10 us (measured).
         __syncthreads();
-        if (tid == 0 && atomicAdd(prm.xctr, 1u) == gridDim.x - 1) {
-            __threadfence_system();
-            for (int g = 0; g < prm.xG; ++g)
-                st_release_sys(reinterpret_cast<uint32_t *>(prm.xpeer[g]) + prm.xrank, prm.xepoch);
-            *prm.xctr = 0u;
+        if (tid == 0) {
+            fence_acq_rel_gpu();
+            if (atomicAdd(prm.xctr, 1u) == gridDim.x - 1) {
+                SMCSD_TRACE_AT(2060);                       // last K1 CTA counted
+                fence_acq_rel_sys();
+                SMCSD_TRACE_AT(2061);                       // system fence done
+                for (int g = 0; g < prm.xG; ++g)
+                    st_relaxed_sys(reinterpret_cast<uint32_t *>(prm.xpeer[g]) + prm.xrank, prm.xepoch);
+                *prm.xctr = 0u;
+            }
         }
     }
-    pdl_trigger();
+    if (!XP) pdl_trigger();
 }
 
 // S2, phase A: merged {M, S, X} of every row of prompt p into rowstat[0 .. 2NK).  Chunks of

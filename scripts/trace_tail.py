@@ -19,13 +19,28 @@ ring = [synth.lm_logits(P, N, K, V, device=dev, seed=100 + r) for r in range(6)]
 lib = ctypes.CDLL(smc.lib_path)
 buf = (ctypes.c_ulonglong * 4096)()
 flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)
+TP = os.environ.get("TP")            # fused-exchange smcsd_tp_step at G = 1 instead of smcsd_step
+B2B = int(os.environ.get("B2B", "0"))  # > 0: that many steps back to back before the traced one
+if TP:
+    from paper_2604_15672_b200.dist import TPExchange
+    ex = TPExchange.local_group(P, N, K, V, 1, device=dev)[0]
+
+
+def call(it, lp, lq, tok):
+    if TP:
+        return ex.step(lp, lq, tok, eta=math.inf, step=it, fields=())
+    return smc.smcsd_step(lp, lq, tok, V=V, eta=math.inf, step=it, fields=())
+
+
 for it in range(12):
     lp, lq, tok = ring[0 if os.environ.get("NOFLUSH") else it % 6]
     if not os.environ.get("NOFLUSH"):
         flush_sum = flush.sum()  # read-only L2 flush (no dirty lines)
     torch.cuda.synchronize()
     lib.smcsd_trace_read(buf, 4096)
-    out = smc.smcsd_step(lp, lq, tok, V=V, eta=math.inf, step=it, fields=())
+    for b in range(B2B):
+        call(100 + b, *ring[b % 6])
+    out = call(it, lp, lq, tok)
     torch.cuda.synchronize()
 lib.smcsd_trace_read(buf, 4096)
 t = list(buf)
@@ -37,9 +52,11 @@ s = sorted(us(x) for x in starts)
 e = sorted(us(x) for x in ends)
 print(f"K1 CTAs {len(starts)}: start spread {s[-1]:.2f} us; done min {e[0]:.2f} median {e[len(e)//2]:.2f} "
       f"p90 {e[int(len(e)*0.9)]:.2f} max {e[-1]:.2f} us")
-names = {2048: "tail CTA resident", 2049: "tail after pdl_wait", 2053: "chunk 0 S2+terms done", 2050: "last CTA of prompt 0", 2051: "after S3",
+names = {2060: "TP: last K1 CTA counted", 2061: "TP: system fence done", 2048: "tail CTA resident", 2049: "tail after pdl_wait", 2053: "chunk 0 S2+terms done", 2050: "last CTA of prompt 0", 2051: "after S3",
          2052: "after S4-S7"}
 for k, nm in names.items():
+    if not t[k]:
+        continue
     print(f"{nm:22s} {us(t[k]):8.2f} us")
 ck = t[2200:2207]
 if ck[0]:
