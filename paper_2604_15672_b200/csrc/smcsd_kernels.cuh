@@ -1271,18 +1271,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     if (st) atomicOr(&prm.st_ws[p], st);
     if (tid == 0 && blockIdx.x == 0) { SMCSD_TRACE_AT(2053); SMCSD_CLK_AT(2204); }      // chunk 0 S2 done
     }
-    // ---- completion: the last CTA of the prompt finishes it
-    __threadfence();
+    // ---- completion: the last CTA of the prompt finishes it.  Release chain: the barrier
+    // orders every thread's terms / flags before thread 0's gpu-scope release fence and count;
+    // the CTA completing the count acquires (fence) and its barrier passes that on to its
+    // threads, whose reads of the other CTAs' terms go to L2 (ld.cg).
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2205);
-    if (tid == 0) s_last = atomicAdd(&prm.prompt_ctr[p], 1u) == (unsigned)(per_prompt - 1);
+    if (tid == 0) {
+        fence_acq_rel_gpu();
+        s_last = atomicAdd(&prm.prompt_ctr[p], 1u) == (unsigned)(per_prompt - 1);
+        if (s_last) fence_acq_rel_gpu();
+    }
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2206);
     if (!s_last) {
         pdl_trigger();
         return;
     }
-    __threadfence();
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);
     // ---- S3: lam' = fl32(prev + sum_{j<k_n} term_j) in j order
     const double *terms = prm.ell_ws + (int64_t)p * NK;
