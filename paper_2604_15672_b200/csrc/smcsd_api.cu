@@ -153,7 +153,8 @@ smcsd_rc launch_rowstats_pw(const Params &prm, int dtype, int64_t items, cudaStr
 }
 
 // power: 0 = plain row statistics; otherwise PowerSMC's second sum, with integer alpha in
-// 1..4 taken by repeated multiplication of the first sum's ex2 (see pow_term).
+// 1..4 taken by repeated multiplication of the first sum's ex2 (see pow_acc), half-integer
+// alpha in 0.5..3.5 from one ex2 of t/2 (see half_pow), any other alpha by a second exp.
 smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream_t st,
                          bool power = false) {
     if (prm.xpeer)                                             // S10 fused exchange
@@ -165,6 +166,10 @@ smcsd_rc launch_rowstats(const Params &prm, int dtype, int64_t items, cudaStream
     if (a == 2.0f) return launch_rowstats_pw<2>(prm, dtype, items, st);
     if (a == 3.0f) return launch_rowstats_pw<3>(prm, dtype, items, st);
     if (a == 4.0f) return launch_rowstats_pw<4>(prm, dtype, items, st);
+    if (a == 0.5f) return launch_rowstats_pw<10>(prm, dtype, items, st);     // half-integer:
+    if (a == 1.5f) return launch_rowstats_pw<11>(prm, dtype, items, st);     // one ex2 per element
+    if (a == 2.5f) return launch_rowstats_pw<12>(prm, dtype, items, st);
+    if (a == 3.5f) return launch_rowstats_pw<13>(prm, dtype, items, st);
     return launch_rowstats_pw<-1>(prm, dtype, items, st);
 }
 

@@ -184,6 +184,17 @@ __device__ __forceinline__ float2 pow_acc(float2 acc, float2 e, float2 t, float 
     return ffma2(e2, e2, acc);
 }
 
+// Half-integer alpha = k + 1/2 (PW = 10 + k, k = 0..3): one ex2 per element, y = 2^(t'/2) with
+// t'/2 = fma(z, c/2, -m/2) (bit-exactly t'/2: scaling by 2^-1), then 2^t' = y^2 for s and
+// 2^(alpha t') = y (y^2)^k for s2 -- multiplies instead of a second MUFU op.
+template <int PW>
+__device__ __forceinline__ float2 half_pow(float2 y, float2 e) {
+    if (PW == 10) return y;
+    if (PW == 11) return fmul2(y, e);
+    if (PW == 12) return fmul2(fmul2(y, e), e);
+    return fmul2(fmul2(y, e), fmul2(e, e));
+}
+
 template <int DT, int PW = 0>
 __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], int nv, float c,
                                             float4 *red, float alpha = 1.0f) {
@@ -228,6 +239,7 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
     // sum of 2^(t - m): exactly one ex2 per element; t and the sums in packed fp32x2 (element
     // pairs), halving the FMA-pipe issue slots of this issue-bound loop
     const float2 cc = make_float2(c, c), mo = make_float2(-off, -off);
+    const float2 cch = make_float2(0.5f * c, 0.5f * c), moh = make_float2(-0.5f * off, -0.5f * off);
     float2 acc[T::kLoads], acc2[T::kLoads];
 #pragma unroll
     for (int i = 0; i < T::kLoads; ++i) {
@@ -237,6 +249,14 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
         for (int k = 0; k < (DT == 1 ? 4 : 2); ++k) {
             const float2 z = DT == 1 ? make_float2(bf16lo(w4[k]), bf16hi(w4[k]))
                                      : make_float2(__uint_as_float(w4[2 * k]), __uint_as_float(w4[2 * k + 1]));
+            if (PW >= 10) {
+                const float2 th = ffma2(z, cch, moh);
+                const float2 y = make_float2(ex2_approx(th.x), ex2_approx(th.y));
+                const float2 e = fmul2(y, y);
+                a = fadd2(a, e);
+                a2 = fadd2(a2, half_pow<PW>(y, e));
+                continue;
+            }
             const float2 t = ffma2(z, cc, mo);
             const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
             a = fadd2(a, e);

@@ -26,20 +26,27 @@ if TP:
     ex = TPExchange.local_group(P, N, K, V, 1, device=dev)[0]
 
 
+POWER = os.environ.get("POWER")      # alpha: smcsd_powersmc_weights on [P][N][1][V] instead
+if POWER:
+    ring = [synth.lm_logits(P, N, 1, V, device=dev, seed=100 + r, bonus=False) for r in range(2)]
+
+
 def call(it, lp, lq, tok):
+    if POWER:
+        return smc.smcsd_powersmc_weights(lp, V=V, alpha=float(POWER))
     if TP:
         return ex.step(lp, lq, tok, eta=math.inf, step=it, fields=())
     return smc.smcsd_step(lp, lq, tok, V=V, eta=math.inf, step=it, fields=())
 
 
 for it in range(12):
-    lp, lq, tok = ring[0 if os.environ.get("NOFLUSH") else it % 6]
+    lp, lq, tok = ring[0 if os.environ.get("NOFLUSH") else it % len(ring)]
     if not os.environ.get("NOFLUSH"):
         flush_sum = flush.sum()  # read-only L2 flush (no dirty lines)
     torch.cuda.synchronize()
     lib.smcsd_trace_read(buf, 4096)
     for b in range(B2B):
-        call(100 + b, *ring[b % 6])
+        call(100 + b, *ring[b % len(ring)])
     out = call(it, lp, lq, tok)
     torch.cuda.synchronize()
 lib.smcsd_trace_read(buf, 4096)

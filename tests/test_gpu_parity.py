@@ -482,7 +482,9 @@ def _power_both(smc, orc, lg, V, alpha, tau=1.0, prev=None):
     return gpu, ref
 
 
-@pytest.mark.parametrize("alpha", [0.5, 2.0, 2.5, 3.0, 4.0])
+# integer alpha (repeated products), half-integer alpha (one ex2 of t/2: 0.5 .. 3.5) and a
+# general alpha (second exp): every K1 power variant
+@pytest.mark.parametrize("alpha", [0.5, 1.5, 2.0, 2.5, 2.7, 3.0, 3.5, 4.0])
 @pytest.mark.parametrize("P,N,V,dtype", [(1, 16, 128256, torch.bfloat16), (2, 33, 20001, torch.float32),
                                          (3, 5, 8193, torch.bfloat16), (1, 1, 3, torch.float32)])
 def test_powersmc_weights_parity(smc, orc, P, N, V, dtype, alpha):
@@ -508,12 +510,14 @@ def test_powersmc_alpha_one_is_exact_zero(smc):
     assert torch.all(out.ess == 16.0)
 
 
-def test_powersmc_status_and_masked_rows(smc, orc):
-    lg, _, _ = synth.lm_logits(3, 4, 1, 9000, dtype=torch.float32, seed=21, bonus=False)
+@pytest.mark.parametrize("alpha", [2.0, 2.5, 2.7])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_powersmc_status_and_masked_rows(smc, orc, alpha, dtype):
+    lg, _, _ = synth.lm_logits(3, 4, 1, 9000, dtype=dtype, seed=21, bonus=False)
     lg[0, 2, 0, 8700] = float("nan")                   # NONFINITE, particle dead
     lg[1, :, 0, :] = -float("inf")                     # every row masked -> all dead, DEGENERATE
     lg[2, 1, 0, :8000] = -float("inf")                 # partially masked row: fine
-    gpu, ref = _power_both(smc, orc, lg, 9000, 2.0)
+    gpu, ref = _power_both(smc, orc, lg, 9000, alpha)
     assert np_(gpu.status).astype(np.uint32).tolist() == ref["status"].tolist()
     assert ref["status"].tolist() == [8, 9, 0]
     assert np.array_equal(np.isneginf(np_(gpu.logw)), np.isneginf(ref["logw"]))
