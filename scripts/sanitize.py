@@ -24,6 +24,7 @@ for (P, N, K, V, dt) in ((1, 4, 4, 1000, torch.float32), (2, 16, 8, 20001, torch
     smc.smcsd_select(w.logw, step=4)
     smc.smcsd_powersmc_weights(lp[:, :, :1].contiguous(), V=V, alpha=2.5)
     smc.smcsd_powersmc_weights(lp[:, :, :1].contiguous(), V=V, alpha=3.0)
+    smc.smcsd_powersmc_weights(lp[:, :, :1].contiguous(), V=V, alpha=0.5)      # half-integer path
     kv = synth.kv_bits((2, 2, P, N, 2, 64, 16), seed=1).to(dev)
     g = smc.kv_geometry(kv)
     dst = torch.empty_like(kv)
