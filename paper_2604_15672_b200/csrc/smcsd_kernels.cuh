@@ -1537,14 +1537,30 @@ __global__ void __launch_bounds__(kThreads) k_power_tail(const __grid_constant__
     for (int n = tid; n < N; n += kThreads) {
         const int64_t pn = (int64_t)p * N + n;
         const float4 *parts = prm.part_ws + pn * prm.nseg;     // rows [P][N] (K = 1, one model)
-        float M = -INFINITY;
-        for (int i = 0; i < prm.nseg; ++i) M = fmaxf(M, __ldcg(&parts[i]).x);
-        float S1 = 0.0f, S2 = 0.0f;
-        for (int i = 0; i < prm.nseg; ++i) {
-            const float4 q = __ldcg(&parts[i]);
-            const float d = q.x == M ? 0.0f : q.x - M;
-            S1 += q.y * (q.x == M ? 1.0f : ex2_approx(d));
-            S2 += q.w * (q.x == M ? 1.0f : ex2_approx(d * prm.alpha_f));
+        // the row's parts in chunks of 16 loaded together (one L2 round trip per chunk, not
+        // one per part); within a chunk: max, then the sums in part order.  A later chunk
+        // with a larger max rescales the running sums (V > 16 segments only).
+        float M = -INFINITY, S1 = 0.0f, S2 = 0.0f;
+        for (int i0 = 0; i0 < prm.nseg; i0 += 16) {
+            float4 q[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                q[u] = i0 + u < prm.nseg ? __ldcg(&parts[i0 + u]) : make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
+            float Mc = M;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) Mc = fmaxf(Mc, q[u].x);
+            if (Mc != M && M != -INFINITY) {
+                S1 *= ex2_approx(M - Mc);
+                S2 *= ex2_approx((M - Mc) * prm.alpha_f);
+            }
+            M = Mc;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                if (i0 + u >= prm.nseg) break;
+                const float d = q[u].x == M ? 0.0f : q[u].x - M;
+                S1 += q[u].y * (q[u].x == M ? 1.0f : ex2_approx(d));
+                S2 += q[u].w * (q[u].x == M ? 1.0f : ex2_approx(d * prm.alpha_f));
+            }
         }
         const float prev = prm.logw_prev ? prm.logw_prev[pn] : neglogN;
         bool bad = false;

@@ -486,7 +486,8 @@ def _power_both(smc, orc, lg, V, alpha, tau=1.0, prev=None):
 # general alpha (second exp): every K1 power variant
 @pytest.mark.parametrize("alpha", [0.5, 1.5, 2.0, 2.5, 2.7, 3.0, 3.5, 4.0])
 @pytest.mark.parametrize("P,N,V,dtype", [(1, 16, 128256, torch.bfloat16), (2, 33, 20001, torch.float32),
-                                         (3, 5, 8193, torch.bfloat16), (1, 1, 3, torch.float32)])
+                                         (3, 5, 8193, torch.bfloat16), (1, 1, 3, torch.float32),
+                                         (1, 8, 140001, torch.bfloat16)])   # 18 segments: 2 chunks
 def test_powersmc_weights_parity(smc, orc, P, N, V, dtype, alpha):
     lg, _, _ = synth.lm_logits(P, N, 1, V, dtype=dtype, seed=4000 + V + N, bonus=False)
     prev = synth.random_logw(P, N, seed=8, sigma=0.5)
