@@ -582,7 +582,7 @@ smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_per_particle
     if (!logw_out || !status || !ancestors || !resampled || !workspace || !xpeer || !xlocal)
         return SMCSD_EINVAL;
     if (N > kTailMaxN || std::isnan(eta) || v_begin < 0 || v_begin + v_len > V) return SMCSD_EINVAL;
-    if (G < 1 || G > kXMaxG || rank < 0 || rank >= G || epoch == 0 || !aligned16(xlocal)) return SMCSD_EINVAL;
+    if (G < 1 || G > kXMaxG || rank < 0 || rank >= G || !aligned16(xlocal)) return SMCSD_EINVAL;
     if (xnseg < cdiv(v_len, kSeg) || (int64_t)G * xnseg > 4096) return SMCSD_EINVAL;
     if (!(std::isfinite(alpha) && alpha > 0.0f) || !valid_temp(inv_temp_p) || !valid_temp(inv_temp_q))
         return SMCSD_EINVAL;
@@ -603,6 +603,7 @@ smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_per_particle
     prm.slot_src = slot_src; prm.resampled = resampled; prm.n_ties = n_ties;
     bind_workspace(prm, workspace, L);
     prm.xpeer = reinterpret_cast<char *const *>(xpeer);
+    prm.xlocal = static_cast<char *>(xlocal);                  // K1 reads the device epoch here
     prm.xrank = rank; prm.xG = G; prm.xnseg = xnseg; prm.xepoch = epoch;
     cudaStream_t st = as_stream(stream);
     rc = launch_rowstats(prm, dtype, prm.main_items, st);         // S1 + push (S10)
@@ -613,8 +614,11 @@ smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_per_particle
     t.xlocal = static_cast<char *>(xlocal);
     t.x_from_logits = 0;
     const int rows = 2 * P * N * K;
+    // explicit epoch: the host picks the parity half; device epoch (0): the tail adds
+    // (epoch & 1) * xhalf itself
+    t.xhalf = (int64_t)x_half_elems(rows, G, xnseg);
     t.parts = reinterpret_cast<const float4 *>(static_cast<char *>(xlocal) + kXFlagBytes) +
-              (epoch & 1u) * x_half_elems(rows, G, xnseg);
+              (epoch ? (epoch & 1u) * x_half_elems(rows, G, xnseg) : 0);
     t.part_row_stride = (int64_t)G * xnseg;
     t.part_seg_stride = 1;
     t.nparts = G * xnseg;

@@ -91,15 +91,25 @@ struct Params {
     char *const *xpeer;                         // [G] device array: every rank's exchange buffer
     char *xlocal;                               // this rank's exchange buffer (tail reads it)
     int xrank, xG, xnseg;                       // rank, ranks, segment slots per rank
-    uint32_t xepoch;                            // this step's epoch (>= 1)
+    uint32_t xepoch;                            // this step's epoch (>= 1), or 0: device epoch
     unsigned *xctr;                             // K1 CTA completion counter (workspace)
+    int64_t xhalf;                              // tail, device epoch: float4 elements per half
 };
 
 // Exchange buffer layout (one per rank, peer-mapped): uint32 flags[64] (flags[g] = last epoch
-// rank g finished pushing here), then two parity halves of [rows][G * xnseg] float4 partials
-// {m, s, x, 0}; row r's slot g * xnseg + s holds segment s of rank g's shard, so the rank-order
-// merge of a row's G * xnseg parts is the global column order.
+// rank g finished pushing here; word kXEpochWord = this rank's last completed epoch and word
+// kXTailCtrWord = the tail's CTA completion count, both local, device-epoch mode only), then two
+// parity halves of [rows][G * xnseg] float4 partials {m, s, x, 0}; row r's slot g * xnseg + s
+// holds segment s of rank g's shard, so the rank-order merge of a row's G * xnseg parts is the
+// global column order.
 constexpr int kXFlagBytes = 256;
+constexpr int kXEpochWord = 48, kXTailCtrWord = 49;         // flags[g] use words 0 .. 31
+// This launch's epoch: the host's, or (xepoch == 0) one past the last epoch this rank completed
+// -- device-resident, so a captured CUDA graph advances it on every replay.
+__device__ __forceinline__ uint32_t x_epoch(const Params &prm) {
+    return prm.xepoch ? prm.xepoch
+                      : __ldcg(reinterpret_cast<const uint32_t *>(prm.xlocal) + kXEpochWord) + 1u;
+}
 __host__ __device__ inline size_t x_half_elems(int rows, int G, int xnseg) {
     return (size_t)rows * G * xnseg;
 }
@@ -108,6 +118,9 @@ __device__ __forceinline__ float4 *x_parts(char *base, int rows, int G, int xnse
 }
 __device__ __forceinline__ void st_relaxed_sys(uint32_t *p, uint32_t v) {
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
@@ -384,7 +397,7 @@ template <int DT, bool XP = false>
 constexpr size_t rowstats_smem_bytes() {
     return (size_t)kStages * kSeg * ItemTraits<DT>::kEsz            // data ring
          + kStages * (2 * sizeof(uint64_t) + sizeof(StageMeta) + kWarps * sizeof(float4) + 16)
-         + (XP ? kXMaxG * sizeof(float4 *) : 0);                     // S10: per-rank destinations
+         + (XP ? kXMaxG * sizeof(float4 *) + 16 : 0);                // S10: per-rank destinations, epoch
 }
 
 // bf16 path: SMCSD_K1_MINB CTAs/SM (32 registers); the general-alpha and cube power sums need
@@ -429,9 +442,21 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
         }
         fence_mbar_init();
     }
-    if (XP && tid < prm.xG)                                 // S10: this epoch's half of each buffer
-        xdst[tid] = x_parts(prm.xpeer[tid], 2 * prm.P * prm.N * prm.K, prm.xG, prm.xnseg, prm.xepoch);
+    uint32_t *xep = reinterpret_cast<uint32_t *>(xdst + kXMaxG);     // S10: this launch's epoch
     __syncthreads();
+    if (XP && warp < kWarps) {
+        // consumers only (named barrier 1), so the producer's first TMA is not held back: the
+        // epoch word is advanced by the previous step's tail, so read it after that completes,
+        // then this epoch's half of each rank's buffer (used at the first item's merge)
+        if (tid == 0) {
+            pdl_wait();
+            *xep = x_epoch(prm);
+        }
+        named_bar_sync(1, kWarps * 32);
+        if (tid < prm.xG)
+            xdst[tid] = x_parts(prm.xpeer[tid], 2 * prm.P * prm.N * prm.K, prm.xG, prm.xnseg, *xep);
+        named_bar_sync(1, kWarps * 32);
+    }
 
     if (warp == kWarps) {
         // ------------------------------------------------------------------ producer
@@ -574,7 +599,7 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                 fence_acq_rel_sys();
                 SMCSD_TRACE_AT(2061);                       // system fence done
                 for (int g = 0; g < prm.xG; ++g)
-                    st_relaxed_sys(reinterpret_cast<uint32_t *>(prm.xpeer[g]) + prm.xrank, prm.xepoch);
+                    st_relaxed_sys(reinterpret_cast<uint32_t *>(prm.xpeer[g]) + prm.xrank, *xep);
                 *prm.xctr = 0u;
             }
         }
@@ -907,6 +932,21 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
 // the NCCL exchange for the combine path): inputs are read before griddepcontrol.wait.
 constexpr int kPairsPerCta = 32;
 
+// S10, device epoch: every tail CTA counts itself once it no longer reads the exchange buffer;
+// the last one records the epoch as this rank's completed one (the next step's K1 reads it after
+// griddepcontrol.wait, i.e. after this whole grid) and re-arms the count.
+__device__ __forceinline__ void x_tail_done(const Params &prm, uint32_t xe) {
+    if (!prm.xlocal || prm.xepoch) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t *w = reinterpret_cast<uint32_t *>(prm.xlocal);
+        if (atomicAdd(w + kXTailCtrWord, 1u) == gridDim.x - 1) {
+            w[kXTailCtrWord] = 0u;
+            w[kXEpochWord] = xe;
+        }
+    }
+}
+
 __device__ __forceinline__ float3 lane_premerge(const Params &prm, int64_t grow, int li) {
     // parts li, li+16, li+32, ... of one row, merged in index order (nparts > 16 only)
     float M = -INFINITY, S = 0.0f, X = -INFINITY;
@@ -1118,6 +1158,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     float4 *rs = cs.rs;
     double *ell_s = cs.ell_s;
     __shared__ int s_last;
+    __shared__ uint32_t s_xe;                                   // S10: this launch's epoch
     const int tid = threadIdx.x;
     const int N = prm.N, K = prm.K, NK = N * K, rows = 2 * NK;
     const int chunk_ctas = prm.P * chunks_per_prompt;
@@ -1159,26 +1200,41 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         if (resample_mode) tail_prologue(prm, p, sh);
     }
     if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2048);      // tail CTA resident
-    pdl_wait();
+    // S10 (xlocal): the epoch flags are the dependency -- every rank's flag, this rank's
+    // included, is released after all of that rank's K1 CTAs pushed their partials and left
+    // the work loop -- so the tail does not also wait for K1's grid to complete and flush.
+    if (!prm.xlocal) pdl_wait();
     if (tid == 0 && blockIdx.x == 0) {
         SMCSD_TRACE_AT(2049);                                   // predecessor complete
         SMCSD_CLK_AT(2200);
-        if (prm.work_ctr) *prm.work_ctr = 0u;                   // re-arm K1's counter
+        if (prm.work_ctr && !prm.xlocal) *prm.work_ctr = 0u;    // re-arm K1's counter
     }
     if (prm.xlocal) {
         // S10: wait until every rank has published this epoch's partials (acquire, system
         // scope; bounded: a missing peer raises ST_EXCHANGE instead of hanging the GPU)
         if (tid == 0) {
+            // (device epoch: the word was last advanced by the previous step's tail, which
+            // completed before this step's K1 passed its griddepcontrol.wait)
+            const uint32_t xe = x_epoch(prm);
+            s_xe = xe;
             const uint32_t *fl = reinterpret_cast<const uint32_t *>(prm.xlocal);
             const uint64_t t0 = globaltimer_ns();
+            bool late = false;
             for (int g = 0; g < prm.xG; ++g)
-                while ((int)(ld_acquire_sys(fl + g) - prm.xepoch) < 0) {
+                while ((int)(ld_acquire_sys(fl + g) - xe) < 0) {
                     if (globaltimer_ns() - t0 > kXTimeoutNs) {
                         atomicOr(&prm.st_ws[p], ST_EXCHANGE);
+                        late = true;
                         break;
                     }
                     __nanosleep(64);
                 }
+            // re-arm K1's counter once this rank's K1 has left its work loop: its own flag
+            // says so; after a timeout, wait for the grid instead
+            if (blockIdx.x == 0 && prm.work_ctr) {
+                if (late) pdl_wait();
+                *prm.work_ctr = 0u;
+            }
         }
         __syncthreads();
     }
@@ -1189,11 +1245,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     // (xor 2, xor 1).  x = t_d is taken from the logits (x_from_logits) or as the max of the
     // parts' x (TP combine).
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2201);
+    // S10 with the device epoch: this epoch's parity half of the exchange buffer
+    const float4 *parts = prm.xlocal && !prm.xepoch ? prm.parts + (int64_t)(s_xe & 1u) * prm.xhalf : prm.parts;
     {
         const int l4 = tid & 3, lr = tid >> 2;                  // local row: model = lr / 32
         const int qq = lr & (kPairsPerCta - 1);
         const int64_t grow = (int64_t)p * rows + (int64_t)(lr / kPairsPerCta) * NK + q0 + qq;
-        const float4 *pr = prm.parts + grow * prm.part_row_stride;
+        const float4 *pr = parts + grow * prm.part_row_stride;
         float Ml = -INFINITY, Sl = 0.0f, Xl = -INFINITY;
         if (qq < nq) {
             if (prm.nparts <= 16) {
@@ -1305,6 +1363,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2206);
     if (!s_last) {
+        x_tail_done(prm, s_xe);
         pdl_trigger();
         return;
     }
@@ -1358,6 +1417,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         else prm.status[p] = sh.st;
     }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);
+    x_tail_done(prm, s_xe);
     pdl_trigger();
 }
 

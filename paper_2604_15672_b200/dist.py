@@ -144,7 +144,8 @@ class TPExchange:
     Single process: TPExchange.local_group(...) returns G exchanges whose tables point at each
     other's buffers on one device (G simulated ranks; run each on its own stream)."""
 
-    def __init__(self, P, N, K, V, *, group=None, device=None, world=None, rank=None, _buf=None):
+    def __init__(self, P, N, K, V, *, group=None, device=None, world=None, rank=None, _buf=None,
+                 device_epoch=True):
         import paper_2604_15672_b200 as smc
         self.smc = smc
         self.device = torch.device("cuda" if device is None else device)
@@ -158,6 +159,9 @@ class TPExchange:
         self.buf = _buf if _buf is not None else torch.empty(self.nbytes, dtype=torch.uint8, device=self.device)
         smc.smcsd_tp_exchange_init(self.buf)
         self.epoch = 0
+        # device_epoch: the epoch lives in the exchange buffer and advances on the GPU, so a
+        # step captured in a CUDA graph stays correct on replay; False: host epoch per call
+        self.device_epoch = device_epoch
         self._opened: list[int] = []
         self.xpeer = None
         if world is None:                      # multi-process: share handles, open peers
@@ -172,8 +176,8 @@ class TPExchange:
         self.xpeer = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
 
     @classmethod
-    def local_group(cls, P, N, K, V, G, device=None):
-        ex = [cls(P, N, K, V, device=device, world=G, rank=g) for g in range(G)]
+    def local_group(cls, P, N, K, V, G, device=None, device_epoch=True):
+        ex = [cls(P, N, K, V, device=device, world=G, rank=g, device_epoch=device_epoch) for g in range(G)]
         ptrs = [e.buf.data_ptr() for e in ex]
         for e in ex:
             e.set_peers(ptrs)
@@ -181,11 +185,13 @@ class TPExchange:
         return ex
 
     def step(self, logits_p_shard, logits_q_shard, tokens, **kw):
-        """One smcsd_tp_step (epoch advanced here, identical on every rank)."""
+        """One smcsd_tp_step: device-resident epoch (graph-capturable), or the host epoch
+        advanced here (identical on every rank)."""
         self.epoch += 1
         return self.smc.smcsd_tp_step(logits_p_shard, logits_q_shard, tokens, V=self.V,
                                       v_begin=self.v_begin, v_len=self.v_len, rank=self.rank,
-                                      G=self.G, xnseg=self.xnseg, epoch=self.epoch,
+                                      G=self.G, xnseg=self.xnseg,
+                                      epoch=0 if self.device_epoch else self.epoch,
                                       xpeer=self.xpeer, xlocal=self.buf, **kw)
 
     def close(self):

@@ -12,7 +12,9 @@ from paper_2604_15672_b200.dist import TPExchange
 dev = torch.device("cuda")
 P, N, K, V = 1, 64, 8, 128256
 ring = [synth.lm_logits(P, N, K, V, device=dev, seed=30 + r) for r in range(3)]
-ex = TPExchange.local_group(P, N, K, V, 1, device=dev)[0]
+# TP_EXPLICIT=1: host epoch per call (for libraries without the device-resident epoch)
+ex = TPExchange.local_group(P, N, K, V, 1, device=dev,
+                            device_epoch=os.environ.get("TP_EXPLICIT") != "1")[0]
 
 
 def plain(i, out, ws, s=None):

@@ -640,6 +640,94 @@ def test_tp_step_fused_exchange(smc, orc, G, P, N, K, V, dtype):
         assert np.array_equal(np_(outs[0].logw), rr["logw"])
 
 
+def _tp_check(outs, lp, lq, tok, prev, V, step, orc):
+    for o in outs:
+        assert np.all(np_(o.status) == 0)
+        for f in ("logw_pre", "logw", "ancestors", "slot_src", "ess", "lse"):
+            assert torch.equal(getattr(o, f), getattr(outs[0], f)), f
+    ref = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, logw_prev=prev.numpy())
+    assert max_abs(np_(outs[0].logw_pre), ref["logw"]) <= TOL_LOGW
+    rr = orc.resample(np_(outs[0].logw_pre), eta=np.inf, seed=3, step=step)
+    assert np.array_equal(np_(outs[0].ancestors), rr["ancestors"])
+
+
+def test_tp_step_explicit_epoch(smc, orc):
+    # the host-epoch mode of smcsd_tp_step (epoch >= 1 per call), three steps (both halves)
+    from paper_2604_15672_b200.dist import TPExchange
+    dev = torch.device("cuda")
+    P, N, K, V, G = 1, 16, 4, 30001, 2
+    ex = TPExchange.local_group(P, N, K, V, G, device=dev, device_epoch=False)
+    streams = [torch.cuda.Stream(dev) for _ in range(G)]
+    for it in range(3):
+        lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=950 + it)
+        prev = synth.random_logw(P, N, seed=21 + it, sigma=0.5)
+        lpd, lqd, tokd, prevd = lp.to(dev), lq.to(dev), tok.to(dev), prev.to(dev)
+        shards = [(_shard(lpd, e.v_begin, e.v_begin + e.v_len, 8, dev),
+                   _shard(lqd, e.v_begin, e.v_begin + e.v_len, 8, dev)) for e in ex]
+        torch.cuda.synchronize()
+        outs = []
+        for g, e in enumerate(ex):
+            with torch.cuda.stream(streams[g]):
+                outs.append(e.step(*shards[g], tokd, logw_prev=prevd, eta=math.inf, seed=3,
+                                   step=it, workspace=smc.Workspace(dev), stream=streams[g]))
+        torch.cuda.synchronize()
+        assert ex[0].epoch == it + 1
+        _tp_check(outs, lp, lq, tok, prev, V, it, orc)
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_tp_step_graph_replay(smc, orc, G):
+    # the device-resident epoch makes smcsd_tp_step capturable: each rank's step is captured
+    # once into a CUDA graph on its own stream, then replayed for new inputs (copied into the
+    # captured buffers); every replay is the next epoch, so flags and parity halves advance
+    from paper_2604_15672_b200.dist import TPExchange
+    dev = torch.device("cuda")
+    P, N, K, V = 1, 32, 8, 128256
+    ex = TPExchange.local_group(P, N, K, V, G, device=dev)
+    streams = [torch.cuda.Stream(dev) for _ in range(G)]
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=970)
+    prev = synth.random_logw(P, N, seed=31, sigma=0.5)
+    tokd, prevd = tok.to(dev), prev.to(dev)
+    shards = [(_shard(lp.to(dev), e.v_begin, e.v_begin + e.v_len, 8, dev),
+               _shard(lq.to(dev), e.v_begin, e.v_begin + e.v_len, 8, dev)) for e in ex]
+    outs = [smc.Outputs() for _ in range(G)]
+    wss = [smc.Workspace(dev) for _ in range(G)]
+
+    def run_all(step):
+        for g, e in enumerate(ex):
+            with torch.cuda.stream(streams[g]):
+                e.step(*shards[g], tokd, logw_prev=prevd, eta=math.inf, seed=3, step=step,
+                       out=outs[g], workspace=wss[g], stream=streams[g])
+
+    for s_ in streams:
+        s_.wait_stream(torch.cuda.current_stream())
+    run_all(0)                                   # eager warm-up: outputs allocated, epoch 1
+    torch.cuda.synchronize()
+    _tp_check(outs, lp, lq, tok, prev, V, 0, orc)
+    graphs = [torch.cuda.CUDAGraph() for _ in range(G)]
+    for g, e in enumerate(ex):
+        with torch.cuda.graph(graphs[g], stream=streams[g]):
+            e.step(*shards[g], tokd, logw_prev=prevd, eta=math.inf, seed=3, step=7,
+                   out=outs[g], workspace=wss[g], stream=streams[g])
+    torch.cuda.synchronize()
+    for it in range(3):                          # epochs 2, 3, 4: both parity halves
+        lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=971 + it)
+        prev = synth.random_logw(P, N, seed=32 + it, sigma=0.5)
+        tokd.copy_(tok.to(dev))
+        prevd.copy_(prev.to(dev))
+        for g, e in enumerate(ex):
+            a, b = _shard(lp.to(dev), e.v_begin, e.v_begin + e.v_len, 8, dev), \
+                _shard(lq.to(dev), e.v_begin, e.v_begin + e.v_len, 8, dev)
+            shards[g][0].copy_(a)
+            shards[g][1].copy_(b)
+        torch.cuda.synchronize()
+        for g in range(G):
+            with torch.cuda.stream(streams[g]):
+                graphs[g].replay()
+        torch.cuda.synchronize()
+        _tp_check(outs, lp, lq, tok, prev, V, 7, orc)
+
+
 def test_extreme_and_masked_rows(smc, orc):
     # SURVEY 8(d) edge rows: +-60 extremes and -inf-masked tails (vocabulary masking), both
     # dtypes; the drafted token always keeps finite target and draft mass
