@@ -582,8 +582,8 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
     }
     if (tid == 0) SMCSD_TRACE_AT(1024 + (blockIdx.x & 1023));    // K1 CTA done
     if (XP) {
-        // the tail may be scheduled now: its griddepcontrol.wait still waits for this whole
-        // grid (flags included), so only its launch overlaps the fences below
+        // the tail may be scheduled now: in this mode its only dependency on this grid is the
+        // epoch flags published below
         pdl_trigger();
         // Release chain (PTX memory model): the CTA barrier orders every thread's pushes before
         // thread 0's gpu-scope release fence + count; the CTA that completes the count
