@@ -32,7 +32,8 @@
  *  - Ancestor indices are local to the prompt (0..N-1).  Philox counters use the GLOBAL
  *    prompt index prompt_base + p, so prompt-sharded (data-parallel) runs are bit-identical
  *    to a single-GPU run.
- *  - The library keeps no global state.  A workspace may not be shared by concurrent calls.
+ *  - The library keeps no global state beyond a per-device cache of kernel attributes and
+ *    occupancy (set on first use).  A workspace may not be shared by concurrent calls.
  */
 #ifndef SMCSD_H
 #define SMCSD_H
