@@ -96,6 +96,28 @@ smcsd_rc launch_pdl_b(void (*kernel)(KArgs...), unsigned grid, size_t smem, cuda
                ? SMCSD_OK : SMCSD_ECUDA;
 }
 
+// PDL launch with a 1-D thread-block cluster of `cluster` CTAs (grid a multiple of it).
+template <typename... KArgs, typename... Args>
+smcsd_rc launch_pdl_cluster(void (*kernel)(KArgs...), unsigned grid, unsigned cluster, cudaStream_t st,
+                            Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...) == cudaSuccess
+               ? SMCSD_OK : SMCSD_ECUDA;
+}
+
 template <typename... KArgs, typename... Args>
 smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaStream_t st,
                     Args &&...args) {
@@ -131,6 +153,9 @@ smcsd_rc ensure_tail_attrs() {
     if (!attr_set[dev]) {
         if (cudaFuncSetAttribute(k_tail_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTailStageBytes) != cudaSuccess)
             return SMCSD_ECUDA;
+        // clusters of up to 16 chunk CTAs (non-portable size; 4 SMs at 4 CTAs per SM)
+        if (cudaFuncSetAttribute(k_tail, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+            return SMCSD_ECUDA;
         attr_set[dev] = true;
     }
     return SMCSD_OK;
@@ -143,7 +168,16 @@ smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     const int bonus_ctas = prm.bonus_tok ? prm.N : 0;
     const int64_t grid = (int64_t)prm.P * chunks + (int64_t)prm.P * bonus_ctas;
     if (grid >= (1ll << 31)) return SMCSD_EINVAL;
-    return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks, bonus_ctas);
+    // one prompt's chunk CTAs as one thread-block cluster (up to 16): their completion is a
+    // cluster barrier instead of the per-prompt counter.  Bonus CTAs (after all chunk CTAs)
+    // must fill whole clusters of their own: P * N a multiple of chunks.
+#ifndef SMCSD_NO_CLUSTER_TAIL
+    const bool cl = chunks >= 2 && chunks <= 16 && (bonus_ctas == 0 || ((int64_t)prm.P * prm.N) % chunks == 0);
+#else
+    const bool cl = false;
+#endif
+    if (cl) return launch_pdl_cluster(k_tail, (unsigned)grid, (unsigned)chunks, st, prm, resample_mode, chunks, bonus_ctas, 1);
+    return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks, bonus_ctas, 0);
 }
 
 template <int PW>

@@ -1143,7 +1143,7 @@ __device__ __noinline__ uint32_t bonus_role(const Params &prm, int p, int n, Bon
 }
 
 __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Params prm, int resample_mode,
-                                                   int chunks_per_prompt, int bonus_ctas) {
+                                                   int chunks_per_prompt, int bonus_ctas, int cluster) {
     // chunk CTAs and bonus CTAs use disjoint shared state: one buffer, two views
     struct ChunkSmem {
         TailSmem sh;
@@ -1353,12 +1353,25 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     // orders every thread's terms / flags before thread 0's gpu-scope release fence and count;
     // the CTA completing the count acquires (fence) and its barrier passes that on to its
     // threads, whose reads of the other CTAs' terms go to L2 (ld.cg).
-    __syncthreads();
-    if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2205);
-    if (tid == 0) {
-        fence_acq_rel_gpu();
-        s_last = atomicAdd(&prm.prompt_ctr[p], 1u) == (unsigned)(per_prompt - 1);
-        if (s_last) fence_acq_rel_gpu();
+    if (cluster) {
+        // the prompt's chunk CTAs are one thread-block cluster: a cluster barrier (release /
+        // acquire at cluster scope, covering the global terms and flags) replaces the counter,
+        // and cluster rank 0 finishes the prompt
+        if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2205);
+        asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+        if (tid == 0) {
+            unsigned r;
+            asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+            s_last = r == 0u;
+        }
+    } else {
+        __syncthreads();
+        if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2205);
+        if (tid == 0) {
+            fence_acq_rel_gpu();
+            s_last = atomicAdd(&prm.prompt_ctr[p], 1u) == (unsigned)(per_prompt - 1);
+            if (s_last) fence_acq_rel_gpu();
+        }
     }
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2206);
