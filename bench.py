@@ -589,6 +589,10 @@ def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
                                          "all_reduce(SUM) -> combine (G = 1) -> resample"}
     # S10 fused into K1 (smcsd_tp_step): partials pushed to every rank's exchange buffer over
     # peer memory, epoch flags, tail merges in rank order -- 2 launches, no collective call
+    cpu_group = None
+    if world > 1:
+        import torch.distributed as tdist
+        cpu_group = tdist.new_group(backend="gloo")        # error agreement off the GPU
     try:
         from paper_2604_15672_b200.dist import TPExchange
         ex = TPExchange(P, N, K, V) if world > 1 else TPExchange.local_group(P, N, K, V, 1, device=dev)[0]
@@ -597,17 +601,23 @@ def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
         fnf = lambda i: ex.step(sp, sq, tok, logw_prev=logw, eta=math.inf, step=i, out=of,
                                 fields=(), workspace=wsf)
         # one checked step first: a peer mapping that does not work shows up as ST_EXCHANGE
-        # after the bounded wait (20 s), never as a hang; then the path is not timed
-        fnf(0)
-        torch.cuda.synchronize()
-        bad = float((of.status != 0).any().item())
+        # after the bounded wait (20 s), never as a hang; then the path is not timed.  The
+        # ranks agree over a CPU (gloo) group, which still works if one rank's CUDA context
+        # faulted, so every rank skips the timing together.
+        bad = 0.0
+        try:
+            fnf(0)
+            torch.cuda.synchronize()
+            bad = float((of.status != 0).any().item())
+        except Exception:
+            bad = 1.0
         if world > 1:
             import torch.distributed as tdist
-            t = torch.tensor([bad], device=dev if tdist.get_backend() == "nccl" else "cpu")
-            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            t = torch.tensor([bad])
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX, group=cpu_group)
             bad = float(t.item())
         if bad != 0:
-            raise RuntimeError(f"fused exchange check failed: status {of.status.tolist()}")
+            raise RuntimeError(f"fused exchange check failed on some rank (this rank: {bad})")
         msf = _time_steps(fnf, steps, warmup, world, dev)
         torch.cuda.synchronize()
         res["fused_exchange"] = {"ms_per_step": round(msf, 4), "steps_per_s": round(1e3 / msf, 1),

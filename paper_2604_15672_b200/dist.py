@@ -130,6 +130,29 @@ def peer_table(handles: list[bytes], rank: int, local_ptr: int, open_fn) -> list
     return [local_ptr if g == rank else int(open_fn(h)) for g, h in enumerate(handles)]
 
 
+def open_peers(handles: list[bytes], rank: int, local_ptr: int, open_fn, close_fn, group=None,
+               device="cpu") -> list[int]:
+    """peer_table with an all-rank agreement: every rank reaches the all-reduce even when
+    opening a peer fails on it, so a failure raises on every rank (and the peers it did open
+    are closed) instead of leaving the other ranks blocked in a later collective."""
+    err, ptrs = None, None
+    try:
+        ptrs = peer_table(handles, rank, local_ptr, open_fn)
+    except Exception as exc:  # depends on the machine's P2P / IPC support
+        err = exc
+    bad = torch.tensor([0.0 if err is None else 1.0],
+                       device=device if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=group)
+    if float(bad.item()) != 0.0:
+        if ptrs is not None:
+            for g, p in enumerate(ptrs):
+                if g != rank:
+                    close_fn(p, handles[g])
+        raise RuntimeError(f"opening the peers' exchange buffers failed on some rank "
+                           f"(this rank: {err!r})")
+    return ptrs
+
+
 def xnseg_for(V: int, world: int, align: int = 8) -> int:
     """Segment slots per rank: the widest shard's ceil(width / SMCSD_SEGMENT), same on all ranks."""
     seg = 8192
@@ -167,7 +190,8 @@ class TPExchange:
         if world is None:                      # multi-process: share handles, open peers
             torch.cuda.synchronize(self.device)
             handles = share_handles(smc.smcsd_ipc_export(self.buf), group)
-            ptrs = peer_table(handles, self.rank, self.buf.data_ptr(), smc.smcsd_ipc_open)
+            ptrs = open_peers(handles, self.rank, self.buf.data_ptr(), smc.smcsd_ipc_open,
+                              smc.smcsd_ipc_close, group=group, device=self.device)
             self._opened = [(p, handles[g]) for g, p in enumerate(ptrs) if g != self.rank]
             self.set_peers(ptrs)
             dist.barrier(group)                # every buffer initialised before any push

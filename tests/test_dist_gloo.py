@@ -162,6 +162,42 @@ def test_tp_exchange_handle_plumbing_gloo():
         assert opened == [1 - r]
 
 
+def _open_peers_fn(rank, world, fail_rank):
+    # open_peers: a failure to open a peer on one rank raises on EVERY rank (no rank is left in
+    # a later collective), and the peers a rank did open are closed again
+    from paper_2604_15672_b200.dist import open_peers, share_handles
+    hs = share_handles(bytes([rank]) * 8)
+    closed = []
+
+    def open_fn(b):
+        if rank == fail_rank:
+            raise OSError("no peer access")
+        return 5000 + b[0]
+
+    try:
+        tab = open_peers(hs, rank, 1000 + rank, open_fn, lambda p, h: closed.append(p))
+        return ("ok", tab, closed)
+    except RuntimeError as e:
+        return ("raised", str(e), closed)
+
+
+def _open_ok(rank, world):
+    return _open_peers_fn(rank, world, fail_rank=-1)
+
+
+def _open_fail(rank, world):
+    return _open_peers_fn(rank, world, fail_rank=1)
+
+
+def test_open_peers_agreement_gloo():
+    res = _run(_open_ok)
+    assert res[0] == ("ok", [1000, 5001], []) and res[1] == ("ok", [5000, 1001], [])
+    res = _run(_open_fail)
+    assert res[0][0] == "raised" and res[1][0] == "raised"
+    assert res[0][2] == [5001]                  # rank 0 opened rank 1's buffer, then closed it
+    assert "no peer access" in res[1][1]
+
+
 def test_xnseg_covers_every_shard():
     from paper_2604_15672_b200.dist import xnseg_for
     assert xnseg_for(128256, 8) == 2 and xnseg_for(128256, 1) == 16 and xnseg_for(128256, 4) == 4
