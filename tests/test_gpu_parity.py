@@ -50,6 +50,9 @@ CASES = [
     (2, 33, 2, 50000, torch.float32, 0.5),        # N not a multiple of 32
     (2, 3, 33, 1000, torch.float32, 0.5),         # K > 32: chunks split particles (S3 in last CTA)
     (1, 7, 7, 3000, torch.bfloat16, 0.5),         # K = 7: 28-pair chunks of whole particles
+    (2, 40, 8, 20001, torch.bfloat16, 0.5),       # 10 chunk CTAs per prompt: a 10-CTA cluster
+    (1, 64, 8, 30000, torch.bfloat16, 0.5),       # 16 chunk CTAs: the largest (non-portable) cluster
+    (1, 65, 8, 9000, torch.float32, 0.5),         # 17 chunks: the per-prompt counter path
 ]
 
 
