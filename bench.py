@@ -1,12 +1,12 @@
 #!/usr/bin/env python
 """bench.py -- SMC-SD verify + resample hot path on B200 (driver contract).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2|cfg1|cfg3|cfg4|cfg5]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--no-secondary] [--no-cpu-baseline]
 
 A step is one pass of the whole hot path over one batch of
 synthetic input.  Default workload (configs[1] of BASELINE.json, one prompt per GPU):
-  verify + resample  V=128256, N=16, K=8, bf16 logits   (smcsd_step: S1-S7, one launch)
+  verify + resample  V=128256, N=16, K=8, bf16 logits   (smcsd_step: S1-S7, K1 + K2)
   + KV reindex of Llama-3.1-70B-shaped per-particle KV caches (80 L x 2 x 8 KV heads x
     seq 2048 x d 128 bf16 = 640 MiB per particle) with the in-place slot plan (S8)
   + token-history reindex (S9).
@@ -14,7 +14,9 @@ eta = +inf forces a resample every step (worst case).  Logits come from a ring o
 sets (394 MB > 126 MB L2); the KV caches (10.7 GB) exceed L2.  Timing: W untimed steps, then K
 steps bracketed by barrier + synchronize, CUDA events on the launching stream, max over ranks.
 For N > 1 (torchrun) each rank runs its own prompt (global prompt index = rank): weak scaling,
-no data-path collective (cfg5 is the tensor-parallel variant with the NCCL exchange).
+no data-path collective.  The line's `secondary` object adds cfg4 (64 prompts), cfg5 (vocab-
+sharded TP: the fused peer-memory exchange, with the NCCL all-gather / all-reduce forms as
+baselines), cfg3 (70B KV reindex, dense and paged), the cfg2 verify path alone and PowerSMC.
 """
 from __future__ import annotations
 
