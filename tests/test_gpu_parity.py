@@ -731,6 +731,46 @@ def test_tp_step_graph_replay(smc, orc, G):
         _tp_check(outs, lp, lq, tok, prev, V, 7, orc)
 
 
+def test_tp_step_many_epochs(smc, orc):
+    # 600 graph replays of a G = 2 fused step (both ranks concurrently on their own streams):
+    # epochs and parity halves advance on the device every replay; no rank ever times out and
+    # the ranks stay bit-identical and equal to the oracle
+    from paper_2604_15672_b200.dist import TPExchange
+    dev = torch.device("cuda")
+    P, N, K, V, G = 1, 16, 4, 30001, 2
+    ex = TPExchange.local_group(P, N, K, V, G, device=dev)
+    streams = [torch.cuda.Stream(dev) for _ in range(G)]
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=990)
+    prev = synth.random_logw(P, N, seed=41, sigma=0.5)
+    tokd, prevd = tok.to(dev), prev.to(dev)
+    shards = [(_shard(lp.to(dev), e.v_begin, e.v_begin + e.v_len, 8, dev),
+               _shard(lq.to(dev), e.v_begin, e.v_begin + e.v_len, 8, dev)) for e in ex]
+    outs = [smc.Outputs() for _ in range(G)]
+    wss = [smc.Workspace(dev) for _ in range(G)]
+    for s_ in streams:
+        s_.wait_stream(torch.cuda.current_stream())
+    for g, e in enumerate(ex):                   # eager first step: outputs allocated
+        with torch.cuda.stream(streams[g]):
+            e.step(*shards[g], tokd, logw_prev=prevd, eta=math.inf, seed=3, step=5,
+                   out=outs[g], workspace=wss[g], stream=streams[g])
+    torch.cuda.synchronize()
+    graphs = [torch.cuda.CUDAGraph() for _ in range(G)]
+    for g, e in enumerate(ex):
+        with torch.cuda.graph(graphs[g], stream=streams[g]):
+            for _ in range(10):
+                e.step(*shards[g], tokd, logw_prev=prevd, eta=math.inf, seed=3, step=5,
+                       out=outs[g], workspace=wss[g], stream=streams[g])
+    torch.cuda.synchronize()
+    for _ in range(60):
+        for g in range(G):
+            with torch.cuda.stream(streams[g]):
+                graphs[g].replay()
+    torch.cuda.synchronize()
+    word = [int(e.buf[48 * 4:49 * 4].view(torch.int32).item()) for e in ex]
+    assert word == [601, 601]                    # device epoch: 1 eager + 600 replayed steps
+    _tp_check(outs, lp, lq, tok, prev, V, 5, orc)
+
+
 def test_extreme_and_masked_rows(smc, orc):
     # SURVEY 8(d) edge rows: +-60 extremes and -inf-masked tails (vocabulary masking), both
     # dtypes; the drafted token always keeps finite target and draft mass
