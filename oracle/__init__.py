@@ -59,8 +59,8 @@ def lib():
         L.orc_select.argtypes = [vp, i32, i32, i64, u64, u64, vp, vp, vp, vp]
         L.orc_powersmc_weights.argtypes = [vp, i64, i32, i32, vp, i32, i32, i64, dbl, dbl, vp, vp,
                                            vp, vp, vp, vp, vp]
-        L.orc_bonus.argtypes = [vp, i64, i32, i32, vp, i32, i32, i32, i64, dbl, u64, u64, i64, vp, vp,
-                                vp, vp]
+        L.orc_bonus.argtypes = [vp, i64, i32, i32, vp, i32, i32, i32, i64, dbl, u64, u64, i64, i64,
+                                vp, vp, vp, vp, vp, vp]
         L.orc_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32]
         L.orc_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
         _lib = L
@@ -176,19 +176,23 @@ def powersmc_weights(logits, *, V=None, logw_prev=None, alpha=1.0, tau=1.0):
     return out
 
 
-def bonus(logits_p, *, K, V=None, n_drafted=None, tau=1.0, seed=0x5EED5EED, step=0, prompt_base=0):
+def bonus(logits_p, *, K, V=None, n_drafted=None, tau=1.0, seed=0x5EED5EED, step=0, prompt_base=0,
+          seg=8192):
     """Bonus-token oracle (NEXT #2; reading G22): one exact draw from
-    softmax(tau z) of target row k_n per particle.  Returns bonus, seg_margin, key_margin, status."""
+    softmax(tau z) of target row k_n per particle, with segment width `seg` (a parameter of the
+    reading).  Returns bonus, seg_margin, key_margin, second (runner-up column of the chosen
+    segment), alt (the draw of the segment across the nearest CDF boundary) and status."""
     lg = np.ascontiguousarray(logits_p)
     P, N, rpp, ld = lg.shape
     V = ld if V is None else V
     nd = None if n_drafted is None else np.ascontiguousarray(n_drafted, dtype=np.int32)
     out = dict(bonus=np.zeros((P, N), np.int32), seg_margin=np.zeros((P, N)),
-               key_margin=np.zeros((P, N)), status=np.zeros(P, np.uint32))
+               key_margin=np.zeros((P, N)), second=np.zeros((P, N), np.int32),
+               alt=np.zeros((P, N), np.int32), status=np.zeros(P, np.uint32))
     lib().orc_bonus(_ptr(lg), ld, rpp, _dtype_code(lg), _ptr(nd), P, N, K, V, float(tau),
-                    int(seed) & (2**64 - 1), int(step) & (2**64 - 1), int(prompt_base),
+                    int(seed) & (2**64 - 1), int(step) & (2**64 - 1), int(prompt_base), int(seg),
                     _ptr(out["bonus"]), _ptr(out["seg_margin"]), _ptr(out["key_margin"]),
-                    _ptr(out["status"]))
+                    _ptr(out["second"]), _ptr(out["alt"]), _ptr(out["status"]))
     return out
 
 

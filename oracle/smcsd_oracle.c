@@ -523,29 +523,63 @@ void orc_select(const float *logw, int P, int N, int64_t prompt_base, uint64_t s
 /* Bonus token (NEXT #2; Alg. 1 line "sample bonus token x+ ~ p(. | x, y)";   */
 /* PAPER.md:330 appends it; weight-neutral).  Reading G22: an    */
 /* exact draw from softmax(tau z) of the target row j = k_n (k_n = n_drafted or K) by a      */
-/* two-level sampler with counter-based uniforms:                                             */
+/* two-level sampler with counter-based uniforms.  The segment width `seg` is a parameter   */
+/* of the reading (any width gives an exact draw; the product path uses 8192 and the tests  */
+/* pin this oracle at 8192 and 4096):                                                       */
 /*   1. segment masses w_i = sum_{v in seg i} exp(tau z_v - M), M = max_v tau z_v, segments  */
-/*      of 8192 columns [8192 i, min(V, 8192 (i+1))); W = sum_i w_i (left to right);          */
+/*      of `seg` columns [seg i, min(V, seg (i+1))); W = sum_i w_i (left to right);           */
 /*   2. U = word0(Philox(key = seed, ctr = (step_lo, step_hi, prompt, 2^31 + 2^20 n))) 2^-32; */
 /*      a = #{i : C_i / W <= U}, C_i = w_0 + ... + w_i  (inverse CDF, as in S6);              */
-/*   3. Gumbel-max inside segment a: for column v = 8192 a + 4 q + k, word k of               */
+/*   3. Gumbel-max inside segment a: for column v = seg a + 4 q + k, word k of                */
 /*      Philox(ctr = (step_lo, step_hi, prompt, 2^31 + 2^20 n + 1 + q)) gives                  */
 /*      u_v = (word + 1/2) 2^-32, E_v = -ln u_v (= -log1p(-(1 - u_v)) for u_v >= 1/2),        */
 /*      g_v = -ln E_v; x+ = argmax_v (tau z_v + g_v), smallest v on equal keys.               */
 /* P(x+ = v) = (w_a / W) (exp(tau z_v - M) / w_a) = softmax(tau z)_v, exactly.                */
-/* margins (optional, test tolerance for rounding-order near-ties, reading G7):               */
-/*   seg_margin[pn] = min_i |C_i / W - U|,  key_margin[pn] = key(x+) - second-best key.       */
+/* Near-tie diagnostics (optional, the test tolerance for rounding-order near-ties, G7):      */
+/*   seg_margin[pn] = min_i |C_i / W - U| (boundary i* attains it),                           */
+/*   key_margin[pn] = key(x+) - second-best key in segment a, second[pn] = that column,      */
+/*   alt[pn] = the Gumbel-max column of the segment on the other side of boundary i*         */
+/*             (i* if C_i* / W <= U, else i* + 1; -1 when that segment does not exist).       */
 /* Invalid k_n: -1 and BAD_TOKEN; NaN / +inf logit or an all -inf row: -1 and NONFINITE.      */
 /* ------------------------------------------------------------------------------------ */
-#define ORC_BONUS_SEG 8192
+static int64_t gumbel_max_segment(const char *row, int dtype, int64_t V, double tau, int64_t seg,
+                                  int64_t a, const uint32_t key[2], const uint32_t ctr_hi[3],
+                                  uint32_t stream, double *best_out, double *second_out,
+                                  int64_t *second_col)
+{
+    const double two_m32 = 1.0 / 4294967296.0;
+    int64_t v0 = a * seg;
+    int64_t nv = V - v0 < seg ? V - v0 : seg;
+    double best = -INFINITY, second = -INFINITY;
+    int64_t arg = -1, arg2 = -1;
+    uint32_t ctr[4] = {ctr_hi[0], ctr_hi[1], ctr_hi[2], 0u}, r[4] = {0, 0, 0, 0};
+    for (int64_t i = 0; i < nv; ++i) {
+        if (i % 4 == 0) {
+            ctr[3] = stream + 1u + (uint32_t)(i / 4);
+            orc_philox4x32_10(ctr, key, r);
+        }
+        uint32_t w = r[i % 4];
+        double E;
+        if (w < 0x80000000u) E = -log(((double)w + 0.5) * two_m32);
+        else E = -log1p(-(((double)(0xFFFFFFFFu - w) + 0.5) * two_m32));
+        double k = tau * decode_logit(row, dtype, v0 + i) - log(E);
+        if (k > best) { second = best; arg2 = arg; best = k; arg = v0 + i; }
+        else if (k > second) { second = k; arg2 = v0 + i; }
+    }
+    *best_out = best;
+    *second_out = second;
+    *second_col = arg2;
+    return arg;
+}
+
 void orc_bonus(const void *logits_p, int64_t ld, int rpp, int dtype, const int32_t *n_drafted,
                int P, int N, int K, int64_t V, double tau, uint64_t seed, uint64_t step,
-               int64_t prompt_base, int32_t *bonus, double *seg_margin, double *key_margin,
-               uint32_t *status)
+               int64_t prompt_base, int64_t seg, int32_t *bonus, double *seg_margin,
+               double *key_margin, int32_t *second, int32_t *alt, uint32_t *status)
 {
     const double two_m32 = 1.0 / 4294967296.0;
     size_t esz = dtype == 1 ? 2 : 4;
-    int64_t nseg = (V + ORC_BONUS_SEG - 1) / ORC_BONUS_SEG;
+    int64_t nseg = (V + seg - 1) / seg;
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     for (int p = 0; p < P; ++p) {
         uint32_t st = 0;
@@ -555,6 +589,8 @@ void orc_bonus(const void *logits_p, int64_t ld, int rpp, int dtype, const int32
             bonus[pn] = -1;
             if (seg_margin) seg_margin[pn] = INFINITY;
             if (key_margin) key_margin[pn] = INFINITY;
+            if (second) second[pn] = -1;
+            if (alt) alt[pn] = -1;
             int kn = n_drafted ? n_drafted[pn] : K;
             if (kn < 0 || kn > K) { st |= ORC_ST_BAD_TOKEN; continue; }
             const char *row = (const char *)logits_p + (pn * rpp + kn) * ld * (int64_t)esz;
@@ -567,51 +603,45 @@ void orc_bonus(const void *logits_p, int64_t ld, int rpp, int dtype, const int32
                 else if (y > M) M = y;
             }
             if (bad || M == -INFINITY) { st |= ORC_ST_NONFINITE; continue; }
-            double W = 0.0, C[4096];
-            if (nseg > 4096) { st |= ORC_ST_NONFINITE; continue; }
+            double W = 0.0, C[8192];
+            if (nseg > 8192) { st |= ORC_ST_NONFINITE; continue; }
             for (int64_t i = 0; i < nseg; ++i) {
                 double w = 0.0;
-                int64_t e = (i + 1) * ORC_BONUS_SEG < V ? (i + 1) * ORC_BONUS_SEG : V;
-                for (int64_t v = i * ORC_BONUS_SEG; v < e; ++v)
+                int64_t e = (i + 1) * seg < V ? (i + 1) * seg : V;
+                for (int64_t v = i * seg; v < e; ++v)
                     w = w + exp(tau * decode_logit(row, dtype, v) - M);
                 W = W + w;
                 C[i] = W;
             }
             /* step 2: segment by inverse CDF */
-            uint32_t ctr[4] = {(uint32_t)step, (uint32_t)(step >> 32), prompt,
-                               0x80000000u + ((uint32_t)n << 20)};
+            uint32_t stream = 0x80000000u + ((uint32_t)n << 20);
+            uint32_t ctr[4] = {(uint32_t)step, (uint32_t)(step >> 32), prompt, stream};
             uint32_t r[4];
             orc_philox4x32_10(ctr, key, r);
             double U = (double)r[0] * two_m32;
-            int64_t a = 0;
+            int64_t a = 0, inear = 0;
             double mg = INFINITY;
             for (int64_t i = 0; i < nseg; ++i) {
                 double c = C[i] / W;
                 if (c <= U) a++;
-                if (fabs(c - U) < mg) mg = fabs(c - U);
+                if (fabs(c - U) < mg) { mg = fabs(c - U); inear = i; }
             }
             if (a >= nseg) a = nseg - 1;     /* U < 1 = C_last / W: unreachable up to rounding */
             /* step 3: Gumbel-max inside segment a */
-            int64_t v0 = a * ORC_BONUS_SEG;
-            int64_t nv = V - v0 < ORC_BONUS_SEG ? V - v0 : ORC_BONUS_SEG;
-            double best = -INFINITY, second = -INFINITY;
-            int64_t arg = -1;
-            for (int64_t i = 0; i < nv; ++i) {
-                if (i % 4 == 0) {
-                    ctr[3] = 0x80000000u + ((uint32_t)n << 20) + 1u + (uint32_t)(i / 4);
-                    orc_philox4x32_10(ctr, key, r);
-                }
-                uint32_t w = r[i % 4];
-                double E;
-                if (w < 0x80000000u) E = -log(((double)w + 0.5) * two_m32);
-                else E = -log1p(-(((double)(0xFFFFFFFFu - w) + 0.5) * two_m32));
-                double k = tau * decode_logit(row, dtype, v0 + i) - log(E);
-                if (k > best) { second = best; best = k; arg = v0 + i; }
-                else if (k > second) second = k;
-            }
+            double best, sec, b2, s2;
+            int64_t col2, col2b;
+            int64_t arg = gumbel_max_segment(row, dtype, V, tau, seg, a, key, ctr, stream,
+                                             &best, &sec, &col2);
             bonus[pn] = (int32_t)arg;
             if (seg_margin) seg_margin[pn] = mg;
-            if (key_margin) key_margin[pn] = best - second;
+            if (key_margin) key_margin[pn] = best - sec;
+            if (second) second[pn] = (int32_t)col2;
+            if (alt) {
+                int64_t b = C[inear] / W <= U ? inear : inear + 1;
+                if (b >= 0 && b < nseg)
+                    alt[pn] = (int32_t)gumbel_max_segment(row, dtype, V, tau, seg, b, key, ctr,
+                                                          stream, &b2, &s2, &col2b);
+            }
         }
         if (status) status[p] = st;
     }

@@ -196,6 +196,78 @@ def test_resample_worked_examples(smc, orc):
         assert np_(gpu.offspring)[0].tolist() == [int(v) for v in off.split(",")]
 
 
+def _tie_flagged(u, C, delta=2.0 ** -40):
+    """Particles n whose u_n lies within the tie radius of some C_m (reading G7)."""
+    return np.array([np.any(np.abs(un - C) <= delta) for un in u])
+
+
+def _assert_ties_equal(gpu_a, ref, u):
+    """n_ties equal and > 0; ancestors equal except at flagged particles (reading G7)."""
+    assert np.array_equal(np_(gpu_a.n_ties), ref["n_ties"])
+    for p in range(ref["n_ties"].shape[0]):
+        flag = _tie_flagged(u[p], ref["cdf"][p])
+        assert int(flag.sum()) > 0 and int(ref["n_ties"][p]) > 0
+        ga, ra = np_(gpu_a.ancestors)[p], ref["ancestors"][p]
+        assert np.array_equal(ga[~flag], ra[~flag])
+        # at a flagged particle the ancestor may move only across the boundaries within the tie
+        # radius: #{m : C_m < u_n - delta} <= a_n <= #{m : C_m <= u_n + delta}
+        C = ref["cdf"][p]
+        for n in np.nonzero(flag)[0]:
+            lo = int(np.sum(C < u[p][n] - 2.0 ** -40))
+            hi = int(np.sum(C <= u[p][n] + 2.0 ** -40))
+            assert lo <= int(ga[n]) <= hi, (p, n, int(ga[n]), lo, hi)
+
+
+def test_forced_ties_resample_and_step(smc, orc):
+    """Forced scan-boundary ties (tests/golden/systematic_ties.txt, derived by hand): the GPU
+    reports the same n_ties > 0 as the oracle through smcsd_resample and through the fused
+    smcsd_step (p == q bitwise gives Delta = 0 exactly, so lam' = lam_prev and C is exact)."""
+    from conftest import read_golden
+    dev = torch.device("cuda")
+    rows = []
+    for line in read_golden("systematic_ties.txt"):
+        w, x, anc, off, ties = [s.strip() for s in line.split(";")]
+        wts = np.array([float(v) for v in w.split(",")])
+        if int(ties) == 0:
+            continue
+        with np.errstate(divide="ignore"):
+            rows.append((np.log(wts).astype(np.float32), int(x), [int(v) for v in anc.split(",")],
+                         int(ties)))
+    for lw1, x, anc, ties in rows:
+        N = lw1.size
+        lw = lw1[None, :]
+        un = np.array([x], np.uint32)
+        gpu, ref = _resample_both(smc, orc, lw, uniforms=un)
+        u = ((np.arange(N) + x / 2 ** 32) / N)[None, :]
+        assert int(ref["n_ties"][0]) == ties
+        _assert_ties_equal(gpu, ref, u)
+        assert np_(gpu.ancestors)[0].tolist() == anc            # C is exact here: no slack used
+        # fused step: p == q (bitwise), logw_prev = the same log-weights -> lam' == lam_prev
+        V, K = 1000, 2
+        lp, _, tok = synth.lm_logits(1, N, K, V, dtype=torch.float32, seed=5 + N)
+        lq = lp[:, :, :K].contiguous()
+        out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V,
+                             logw_prev=torch.from_numpy(lw).to(dev), eta=math.inf,
+                             uniforms=torch.from_numpy(un.view(np.int32)).to(dev))
+        torch.cuda.synchronize()
+        assert np_(out.logw_pre).tobytes() == lw.tobytes()
+        ref_s = orc.resample(np_(out.logw_pre), eta=math.inf, uniforms=un)
+        _assert_ties_equal(out, ref_s, u)
+        assert np_(out.ancestors)[0].tolist() == anc
+    # N = 1024 at the radius boundary (test_oracle_resample.py::test_tie_threshold_boundary)
+    lw = np.zeros((2, 1024), np.float32)
+    un = np.array([4, 5], np.uint32)
+    gpu = smc.smcsd_resample(torch.from_numpy(lw).to(dev), eta=math.inf,
+                             uniforms=torch.from_numpy(un.view(np.int32)).to(dev))
+    torch.cuda.synchronize()
+    assert np_(gpu.n_ties).tolist() == [1023, 0]
+    # multinomial: same rule over i.i.d. u_n
+    words = np.array([[0, 1 << 30, 1 << 31, 3 << 30]], np.uint32)
+    gpu, ref = _resample_both(smc, orc, np.zeros((1, 4), np.float32), uniforms=words, scheme=1)
+    assert int(np_(gpu.n_ties)[0]) == int(ref["n_ties"][0]) == 3
+    assert np_(gpu.ancestors)[0].tolist() == ref["ancestors"][0].tolist() == [0, 1, 2, 3]
+
+
 def test_reset_value_table(smc):
     # fl32(-ln N), N = 1..1024, bitwise equal to the oracle's and Python's (PAPER.md:331)
     dev = torch.device("cuda")
@@ -531,12 +603,28 @@ def test_powersmc_status_and_masked_rows(smc, orc, alpha, dtype):
 # ------------------------------------------------------------- bonus token (NEXT #2)
 SEG_MARGIN_TOL = 1e-5      # |C_i/W - U| below this: segment choice is a rounding-order near-tie
 KEY_MARGIN_TOL = 1e-4      # top-2 Gumbel keys (natural units) closer than this: near-tie
+BONUS_SEG = 8192           # reading G22's segment width as the product path uses it
 
 
 def _bonus_check(gpu_b, ref):
-    ok = (ref["seg_margin"] > SEG_MARGIN_TOL) & (ref["key_margin"] > KEY_MARGIN_TOL)
+    """Draw-for-draw parity except at rounding-order near-ties, and there the GPU's draw must be
+    one of the near-tied candidates the oracle names: at a segment near-tie the draw of the
+    segment across the nearest CDF boundary (ref['alt']), at a key near-tie the runner-up column
+    of the chosen segment (ref['second'])."""
+    seg_tie = ref["seg_margin"] <= SEG_MARGIN_TOL
+    key_tie = ref["key_margin"] <= KEY_MARGIN_TOL
+    ok = ~seg_tie & ~key_tie
     assert ok.mean() > 0.9
     assert np.array_equal(gpu_b[ok], ref["bonus"][ok])
+    for idx in zip(*np.nonzero(~ok)):
+        g = gpu_b[idx]
+        allowed = {int(ref["bonus"][idx])}
+        if seg_tie[idx]:
+            allowed.add(int(ref["alt"][idx]))
+        if key_tie[idx]:
+            allowed.add(int(ref["second"][idx]))
+        allowed.discard(-1)
+        assert int(g) in allowed, (idx, int(g), allowed)
     return ok
 
 
@@ -551,7 +639,8 @@ def test_bonus_token_parity(smc, orc, P, N, K, V, dtype):
     out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), bonus=True, **kw)
     plain = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), **kw)
     torch.cuda.synchronize()
-    ref = orc.bonus(to_host(lp), K=K, V=V, tau=1.0 / 0.7, seed=77, step=5, prompt_base=3)
+    ref = orc.bonus(to_host(lp), K=K, V=V, tau=1.0 / 0.7, seed=77, step=5, prompt_base=3,
+                    seg=BONUS_SEG)
     _bonus_check(np_(out.bonus), ref)
     assert np.all(np_(out.status) == 0) and np.all(ref["status"] == 0)
     # the bonus row never enters the weights or the resampling
@@ -568,7 +657,7 @@ def test_bonus_token_n_drafted_and_flags(smc, orc):
     out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, n_drafted=nd.to(dev),
                          eta=math.inf, step=2, bonus=True)
     torch.cuda.synchronize()
-    ref = orc.bonus(to_host(lp), K=K, V=V, n_drafted=nd.numpy(), step=2)
+    ref = orc.bonus(to_host(lp), K=K, V=V, n_drafted=nd.numpy(), step=2, seg=BONUS_SEG)
     _bonus_check(np_(out.bonus), ref)
     assert np_(out.bonus)[1, 2] == -1 and np_(out.bonus)[1, 4] == -1
     assert int(np_(out.status)[1]) & 8
@@ -843,7 +932,7 @@ def test_bonus_at_max_vocab(smc, orc):
     out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, step=1, bonus=True)
     torch.cuda.synchronize()
     assert int(out.status.abs().sum()) == 0
-    ref = orc.bonus(to_host(lp), K=K, V=V, step=1)
+    ref = orc.bonus(to_host(lp), K=K, V=V, step=1, seg=BONUS_SEG)
     _bonus_check(np_(out.bonus), ref)
     w = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V)
     assert max_abs(np_(out.logw_pre), w["logw"]) <= TOL_LOGW

@@ -29,6 +29,54 @@ def test_worked_examples(orc):
         assert out["n_ties"][0] == 0
 
 
+def test_tie_counts(orc):
+    """Positive pins for the scan-boundary tie count (reading G7; Alg. 1 resample step,
+    PAPER.md:326-331).  Hand derivations for tests/golden/systematic_ties.txt (U = x 2^-32):
+
+    * N equal weights, x = 0: e_n = exp(0) = 1 exactly, P_m = m+1, C_m = fl((m+1)/N) and
+      u_n = fl(n/N) -- the same correctly rounded quotient -- so u_n == C_{n-1} for n = 1..N-1:
+      N-1 ties (N = 4: 3, N = 8: 7, N = 3: 2).  a_n = #{m : C_m <= u_n} = n (identity).
+    * (.5, 0, 0, .5), x = 0: e = (1, 0, 0, 1), C = (.5, .5, .5, 1), u = (0, .25, .5, .75).
+      u_2 = .5 meets the zero-weight plateau C_0 = C_1 = C_2: 3 ties (each pair counts once).
+      a = (0, 0, 3, 3): the zero-weight particles 1, 2 are skipped.
+    * (0, 0, 1, 1), x = 0: C = (0, 0, .5, 1); u_0 = 0 meets C_0 = C_1 (2 ties), u_2 = .5 meets
+      C_2 (1 tie): 3.  a = (2, 2, 3, 3): the plateau at zero is never chosen even at u = 0.
+    * N = 4 equal, x = 1: u_n - C_{n-1} = 2^-32/4 = 2^-34 > 2^-40: no tie.
+    """
+    for line in read_golden("systematic_ties.txt"):
+        w, x, anc, off, ties = [s.strip() for s in line.split(";")]
+        out = orc.resample(_logw([float(v) for v in w.split(",")]), eta=np.inf,
+                           uniforms=np.array([int(x)], np.uint32))
+        assert out["ancestors"][0].tolist() == [int(v) for v in anc.split(",")], line
+        assert out["offspring"][0].tolist() == [int(v) for v in off.split(",")], line
+        assert int(out["n_ties"][0]) == int(ties), line
+
+
+def test_tie_threshold_boundary(orc):
+    """The tie radius is 2^-40 inclusive (reading G7).  N = 1024 equal weights: C_{n-1} = n/1024
+    and u_n = (n + x 2^-32)/1024 are exact in fp64, so u_n - C_{n-1} = x 2^-42.  x = 4 gives
+    exactly 2^-40 (a tie at each of the 1023 interior boundaries); x = 5 gives 1.25 2^-40 (none).
+    A strict '<', a wrong radius (2^-41 or 2^-39) or a one-sided count fails one of these."""
+    lw = np.zeros((1, 1024), np.float32)
+    for x, want in ((4, 1023), (5, 0), (0, 1023), (3, 1023)):
+        out = orc.resample(lw, eta=np.inf, uniforms=np.array([x], np.uint32))
+        assert int(out["n_ties"][0]) == want, x
+        assert out["ancestors"][0].tolist() == list(range(1024))
+    # radius 2^-39 would make x = 8 a tie; 2^-40 must not
+    out = orc.resample(lw, eta=np.inf, uniforms=np.array([8], np.uint32))
+    assert int(out["n_ties"][0]) == 0
+
+
+def test_tie_count_multinomial(orc):
+    """Multinomial uses the same tie rule over its i.i.d. u_n.  Equal weights (N = 4,
+    C = (.25, .5, .75, 1)) with raw words 0, 2^30, 2^31, 3 2^30 (u = 0, .25, .5, .75) tie at
+    u = .25, .5, .75: 3 ties; a_n = #{C_m <= u_n} = (0, 1, 2, 3)."""
+    words = np.array([[0, 1 << 30, 1 << 31, 3 << 30]], np.uint32)
+    out = orc.resample(np.zeros((1, 4), np.float32), eta=np.inf, scheme=1, uniforms=words)
+    assert int(out["n_ties"][0]) == 3
+    assert out["ancestors"][0].tolist() == [0, 1, 2, 3]
+
+
 def _closed_form_offspring(C, U, N):
     o = np.zeros(N, np.int64)
     prev = 0.0

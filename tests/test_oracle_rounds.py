@@ -15,7 +15,7 @@ def _oracle_backend(orc, P, N, K, seed):
     def backend(r, lp, lq, tok, eta):
         w = orc.weights(lp, lq, tok, V=sr.V, logw_prev=np.full((P, N), orc.neg_log_n(N), np.float32))
         rs = orc.resample(w["logw"], eta=eta, seed=seed, step=r)
-        b = orc.bonus(lp, K=K, V=sr.V, seed=seed, step=r)
+        b = orc.bonus(lp, K=K, V=sr.V, seed=seed, step=r, seg=8192)
         assert (w["status"] == 0).all() and (b["status"] == 0).all()
         return w["lse"], b["bonus"], rs["slot_src"], w["logw"]
 
