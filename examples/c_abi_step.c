@@ -80,8 +80,10 @@ static int run_case(int perturb, void *ws, size_t wsb) {
     CK(cudaMemcpy(dkv, hkv, sizeof hkv, cudaMemcpyHostToDevice));
     const int64_t e = 4;
     RC(smcsd_kv_reindex(dkv, dkv, L * 2, P * N * blk * e, N * blk * e, blk * e, H, S * D * e, S * D * e,
-                        dslot, P, N, NULL));
+                        dslot, P, N, dst, NULL));
     CK(cudaMemcpy(out, dkv, sizeof out, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&st, dst, 4, cudaMemcpyDeviceToHost));
+    EXPECT(st == 0);                               /* slot plan is valid: no SMCSD_ST_BAD_INDEX */
     for (int o = 0; o < L * 2; ++o)
         for (int n = 0; n < N; ++n)
             EXPECT(memcmp(out + (o * N + n) * blk, hkv + (o * N + slot[n]) * blk, blk * sizeof(float)) == 0);

@@ -72,6 +72,9 @@ typedef enum { SMCSD_SYSTEMATIC = 0, SMCSD_MULTINOMIAL = 1 } smcsd_scheme;
 #define SMCSD_ST_NONFINITE   8u  /* NaN/+inf logit or log-weight, or a row whose max is -inf        */
 #define SMCSD_ST_BAD_PAGE   16u  /* paged reindex: page id or ancestor out of range (entry skipped) */
 #define SMCSD_ST_EXCHANGE   32u  /* smcsd_tp_step: a peer's partials did not arrive within 20 s     */
+#define SMCSD_ST_BAD_INDEX  64u  /* kv reindex: src_index entry outside [0,N) (entry skipped), or an
+                                    in-place index that is both a source and a destination (the
+                                    prompt's in-place copies skipped)                              */
 
 /* Segment length (elements) of the fixed in-row split used by every logit row (G17). */
 #define SMCSD_SEGMENT 8192
@@ -209,11 +212,15 @@ SMCSD_API smcsd_rc smcsd_partials_rescale(const float *partials, const float *ma
  *                             and a destination, which slot_src guarantees).
  * Copies are bitwise (16-byte integer vectors; NaN payloads survive) and source-major: each
  * source chunk is read once and written to all of its destinations.  seg_bytes, all strides
- * and both base pointers must be multiples of 16; N <= 1024. */
+ * and both base pointers must be multiples of 16; N <= 1024.
+ *  status [P] (optional, device): SMCSD_ST_BAD_INDEX when prompt p's src_index holds an entry
+ *  outside [0, N) (that destination is left untouched) or, in place, an index that is both a
+ *  source and a destination (the prompt's in-place copies are skipped); 0 otherwise.  The index
+ *  values live on the device, so this cannot be a synchronous error. */
 SMCSD_API smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_stride,
                           int64_t prompt_stride, int64_t particle_stride, int64_t seg_count,
                           int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index,
-                          int P, int N, void *stream);
+                          int P, int N, uint32_t *status, void *stream);
 
 /* S8/S9 over several state tensors in ONE launch, with one src_index: e.g. per-layer K and V
  * tensors of a serving engine (dst[], src[], n_tensors) plus the token history.
@@ -228,7 +235,8 @@ typedef struct {
     int64_t seg_count, seg_bytes, seg_stride;                        /* bytes */
 } smcsd_kv_tensor;
 SMCSD_API smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
-                                          const int32_t *src_index, int P, int N, void *stream);
+                                          const int32_t *src_index, int P, int N, uint32_t *status,
+                                          void *stream);
 
 /* Terminal selection: "one complete sequence is sampled from the terminal
  * normalized weights".  selected[p] = #{m : C_m <= u} with u = word0(Philox(key = seed,
@@ -303,7 +311,7 @@ SMCSD_API smcsd_rc smcsd_ipc_open(const void *handle, void **dev_ptr_out);
 SMCSD_API smcsd_rc smcsd_ipc_close(void *dev_ptr, const void *handle);
 /* S1 + S10 + S2-S7 on this rank's shard.  Arguments as smcsd_step, plus
  *  v_begin/v_len: this rank's columns (logits rows hold only them; tokens are global ids);
- *  rank, G, xnseg, epoch: see above;  xpeer: DEVICE array [G] of every rank's exchange buffer
+ *  rank, G (1..32), xnseg, epoch: see above;  xpeer: DEVICE array [G] of every rank's exchange buffer
  *  as mapped in this process (xpeer[rank] == xlocal);  xlocal: this rank's buffer.
  *  Workspace: smcsd_workspace_bytes(P, N, K, v_len).  N <= 1024, G <= 32. */
 SMCSD_API smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,

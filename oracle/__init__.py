@@ -27,6 +27,7 @@ ST_NOT_ABSCONT = 2
 ST_BAD_TOKEN = 4
 ST_NONFINITE = 8
 ST_BAD_PAGE = 16
+ST_BAD_INDEX = 64
 
 
 def build(force: bool = False) -> str:
@@ -61,7 +62,7 @@ def lib():
                                            vp, vp, vp, vp, vp]
         L.orc_bonus.argtypes = [vp, i64, i32, i32, vp, i32, i32, i32, i64, dbl, u64, u64, i64, i64,
                                 vp, vp, vp, vp, vp, vp]
-        L.orc_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32]
+        L.orc_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
         L.orc_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
         _lib = L
     return _lib
@@ -211,11 +212,14 @@ def select(logw, *, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None):
 
 def kv_reindex(dst: np.ndarray, src: np.ndarray, src_index: np.ndarray, *, n_outer, outer_stride,
                prompt_stride, particle_stride, seg_count, seg_bytes, seg_stride):
-    """S8/S9 oracle: byte copies (strides in bytes).  dst is src for in-place."""
+    """S8/S9 oracle: byte copies (strides in bytes).  dst is src for in-place.  Returns the
+    per-prompt status (ST_BAD_INDEX for an out-of-range or, in place, hazardous index)."""
     idx = np.ascontiguousarray(src_index, dtype=np.int32)
     P, N = idx.shape
+    st = np.zeros(P, np.uint32)
     lib().orc_kv_reindex(_ptr(dst), _ptr(src), n_outer, outer_stride, prompt_stride,
-                         particle_stride, seg_count, seg_bytes, seg_stride, _ptr(idx), P, N)
+                         particle_stride, seg_count, seg_bytes, seg_stride, _ptr(idx), P, N, _ptr(st))
+    return st
 
 
 def kv_reindex_paged(table, n_pages, refcount, src_index, *, num_pages=None):

@@ -720,16 +720,32 @@ void orc_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages_src, 
 /* Out-of-place (dst != src): dst block n <- src block src_index[n] for every n.         */
 /* In-place (dst == src): for every n with src_index[n] != n, block n <- block           */
 /* src_index[n] (the slot plan guarantees sources are never destinations).              */
+/* Invalid index policy (reading G23): an entry outside [0, N) is skipped     */
+/* (destination untouched) and flags ORC_ST_BAD_INDEX in status[p]; in place, an entry   */
+/* whose source is itself a destination (src_index[s] != s) makes the plan not           */
+/* hazard-free: the prompt is flagged and none of its blocks is copied.                  */
 /* ------------------------------------------------------------------------------------ */
+#define ORC_ST_BAD_INDEX 64u
 void orc_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_stride,
                     int64_t prompt_stride, int64_t particle_stride, int64_t seg_count,
-                    int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index, int P, int N)
+                    int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index, int P, int N,
+                    uint32_t *status)
 {
     int in_place = (dst == src);
-    for (int64_t o = 0; o < n_outer; ++o)
-        for (int p = 0; p < P; ++p)
+    for (int p = 0; p < P; ++p) {
+        const int32_t *idx = src_index + (int64_t)p * N;
+        int oob = 0, hazard = 0;
+        for (int n = 0; n < N; ++n) {
+            int s = idx[n];
+            if (s < 0 || s >= N) oob = 1;
+            else if (s != n && idx[s] != s) hazard = 1;
+        }
+        if (status) status[p] = (oob || (in_place && hazard)) ? ORC_ST_BAD_INDEX : 0u;
+        if (in_place && hazard) continue;
+        for (int64_t o = 0; o < n_outer; ++o)
             for (int n = 0; n < N; ++n) {
-                int s = src_index[(int64_t)p * N + n];
+                int s = idx[n];
+                if (s < 0 || s >= N) continue;
                 if (in_place && s == n) continue;
                 for (int64_t g = 0; g < seg_count; ++g) {
                     char *d = (char *)dst + o * outer_stride + p * prompt_stride + n * particle_stride + g * seg_stride;
@@ -737,4 +753,5 @@ void orc_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_s
                     memcpy(d, sp, (size_t)seg_bytes);
                 }
             }
+    }
 }

@@ -25,14 +25,14 @@ __all__ = [
     "smcsd_version", "kv_geometry", "smcsd_select", "smcsd_kv_reindex_paged", "ST_BAD_PAGE",
     "smcsd_powersmc_weights", "smcsd_tp_exchange_bytes", "smcsd_tp_exchange_init",
     "smcsd_ipc_handle_bytes", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close", "smcsd_tp_step",
-    "ST_EXCHANGE",
+    "ST_EXCHANGE", "ST_BAD_INDEX",
 ]
 
 SMCSD_F32, SMCSD_BF16 = 0, 1
 SMCSD_SYSTEMATIC, SMCSD_MULTINOMIAL = 0, 1
 SEGMENT = 8192
 ST_DEGENERATE, ST_NOT_ABSCONT, ST_BAD_TOKEN, ST_NONFINITE, ST_BAD_PAGE = 1, 2, 4, 8, 16
-ST_EXCHANGE = 32
+ST_EXCHANGE, ST_BAD_INDEX = 32, 64
 _RC = {0: "ok", 1: "invalid argument", 2: "CUDA launch or runtime error", 3: "not implemented"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -74,8 +74,8 @@ def _load():
                                         i64, i64, f32, f32, vp, vp, sz, vp]
     L.smcsd_weights_combine.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i64, f32, vp, vp, vp,
                                         vp, vp, vp, vp, vp, sz, vp]
-    L.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
-    L.smcsd_kv_reindex_multi.argtypes = [ctypes.POINTER(_KvTensor), i32, vp, i32, i32, vp]
+    L.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp, vp]
+    L.smcsd_kv_reindex_multi.argtypes = [ctypes.POINTER(_KvTensor), i32, vp, i32, i32, vp, vp]
     L.smcsd_partials_rescale.argtypes = [vp, vp, vp, i64, vp]
     L.smcsd_select.argtypes = [vp, i32, i32, i64, u64, u64, vp, vp, vp, vp, sz, vp]
     L.smcsd_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
@@ -145,6 +145,43 @@ def _logits_geom(t, name):
     return t.shape[3], t.shape[2]
 
 
+def _chk(t, name, dtypes, shape, device, *, optional=True):
+    """Argument validation (marshalling only): dtype, shape, device and contiguity of a tensor
+    whose data_ptr() goes to the C ABI.  Raises ValueError; None passes when optional."""
+    if t is None:
+        if optional:
+            return
+        raise ValueError(f"{name} is required")
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.dtype not in dtypes:
+        raise ValueError(f"{name} must be {' or '.join(str(d) for d in dtypes)}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_cuda or t.device != device:
+        raise ValueError(f"{name} must be on {device} (no CPU fallback), got {t.device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+_I32 = (torch.int32,)
+_U32 = (torch.int32, torch.uint32) if hasattr(torch, "uint32") else (torch.int32,)
+_F32 = (torch.float32,)
+
+
+def _check_inputs(dev, P, N, K, *, tokens=None, n_drafted=None, logw_prev=None, uniforms=None,
+                  scheme=SMCSD_SYSTEMATIC):
+    _chk(tokens, "tokens", _I32, (P, N, K), dev, optional=False)
+    _chk(n_drafted, "n_drafted", _I32, (P, N), dev)
+    _chk(logw_prev, "logw_prev", _F32, (P, N), dev)
+    _chk(uniforms, "uniforms", _U32, (P,) if scheme == SMCSD_SYSTEMATIC else (P, N), dev)
+
+
+def _resolve_eta(eta, N):
+    """eta = None selects the reference threshold ESS < N/2 (reading G2)."""
+    return N / 2.0 if eta is None else eta
+
+
 def _empty(shape, dtype, device):
     return torch.empty(shape, dtype=dtype, device=device)
 
@@ -186,7 +223,9 @@ _default_ws = {}
 
 def _ws(ws, device, P, N, K, v_len, stream):
     if ws is None:
-        key = (device.type, device.index)
+        # one default workspace per (device, stream): concurrent calls on different streams
+        # must not share one (include/smcsd.h), calls on one stream are ordered by it
+        key = (device.type, device.index, _stream(stream))
         ws = _default_ws.setdefault(key, Workspace(device))
     if isinstance(ws, Workspace):
         return ws.get(P, N, K, v_len, stream)
@@ -221,9 +260,11 @@ def _alloc(out: Outputs, dev, P, N, K, fields):
                   slot_src=((P, N), torch.int32), resampled=((P,), torch.uint8),
                   n_ties=((P,), torch.int32), bonus=((P, N), torch.int32))
     for f in fields:
+        shp, dt = shapes[f]
         if getattr(out, f) is None:
-            shp, dt = shapes[f]
             setattr(out, f, _empty(shp, dt, dev))
+        else:
+            _chk(getattr(out, f), f"out.{f}", (dt,), shp, dev)
     return out
 
 
@@ -242,6 +283,9 @@ def smcsd_weights(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_pr
     P, N, K = tokens.shape
     V = ld_p if V is None else V
     dev = logits_p.device
+    _check_inputs(dev, P, N, K, tokens=tokens, n_drafted=n_drafted, logw_prev=logw_prev)
+    if logits_q.device != dev:
+        raise ValueError("logits_p and logits_q must be on one device")
     out = _alloc(out or Outputs(), dev, P, N, K, ("logw", "status") + tuple(fields))
     ws = _ws(workspace, dev, P, N, K, V, stream)
     rc = _lib.smcsd_weights(_p(logits_p), ld_p, rpp_p, _p(logits_q), ld_q, rpp_q,
@@ -254,7 +298,7 @@ def smcsd_weights(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_pr
 
 
 def _step_args(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=None,
-               alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, eta=math.inf,
+               alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, eta=None,
                scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
                out: Outputs | None = None, fields=_ALL_S, workspace=None, stream=None, bonus=False):
     """Validated smcsd_step argument list (in ABI order) and the Outputs it writes."""
@@ -265,6 +309,11 @@ def _step_args(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=
     P, N, K = tokens.shape
     V = ld_p if V is None else V
     dev = logits_p.device
+    _check_inputs(dev, P, N, K, tokens=tokens, n_drafted=n_drafted, logw_prev=logw_prev,
+                  uniforms=uniforms, scheme=scheme)
+    if logits_q.device != dev:
+        raise ValueError("logits_p and logits_q must be on one device")
+    eta = _resolve_eta(eta, N)
     out = _alloc(out or Outputs(), dev, P, N, K,
                  ("logw", "status", "ancestors", "resampled") + tuple(fields)
                  + (("bonus",) if bonus else ()))
@@ -278,17 +327,18 @@ def _step_args(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=
             _p(out.ancestors), _p(out.offspring), _p(out.slot_src),
             _p(out.resampled), _p(out.n_ties), _p(out.bonus) if bonus else None,
             _p(ws), ws.numel(), _stream(stream)]
-    return args, out
+    return args, out, ws
 
 
 def smcsd_step(logits_p, logits_q, tokens, *, V=None, n_drafted=None, logw_prev=None,
-               alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, eta=math.inf,
+               alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0, eta=None,
                scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
                out: Outputs | None = None, fields=_ALL_S, workspace=None,
                stream=None, bonus=False) -> Outputs:
     """Fused S1-S7 (one launch).  bonus=True also draws the bonus token x+ of every particle
-    from target row k_n (NEXT #2; logits_p needs K+1 rows) into out.bonus [P][N]."""
-    args, out = _step_args(logits_p, logits_q, tokens, V=V, n_drafted=n_drafted,
+    from target row k_n (NEXT #2; logits_p needs K+1 rows) into out.bonus [P][N].
+    eta: resample iff ESS < eta; None = N/2 (reading G2), math.inf forces a resample."""
+    args, out, _ = _step_args(logits_p, logits_q, tokens, V=V, n_drafted=n_drafted,
                            logw_prev=logw_prev, alpha=alpha, inv_temp_p=inv_temp_p,
                            inv_temp_q=inv_temp_q, eta=eta, scheme=scheme, seed=seed, step=step,
                            prompt_base=prompt_base, uniforms=uniforms, out=out, fields=fields,
@@ -307,7 +357,15 @@ class StepPlan:
     _I_LP, _I_LQ, _I_TOK, _I_STEP = 0, 3, 7, 20
 
     def __init__(self, logits_p, logits_q, tokens, **kw):
-        self._args, self.out = _step_args(logits_p, logits_q, tokens, **kw)
+        # The plan keeps a private workspace (a raw tensor passed as workspace= is used as is
+        # and must be exclusive to the plan): run() skips Workspace's shape bookkeeping, so a
+        # shared Workspace could be regrown (freeing the buffer the plan writes) or re-zeroed /
+        # overwritten by another shape's call between runs.
+        ws = kw.get("workspace")
+        if ws is None or isinstance(ws, Workspace):
+            kw["workspace"] = Workspace(logits_p.device)
+        self._args, self.out, self._ws = _step_args(logits_p, logits_q, tokens, **kw)
+        self._ws_owner = kw["workspace"]           # keeps the buffer alive as long as the plan
         self._sig = (tuple(logits_p.shape), tuple(logits_q.shape), tuple(tokens.shape),
                      logits_p.dtype, logits_p.device)
         ctypes_types = _lib.smcsd_step.argtypes
@@ -332,12 +390,17 @@ class StepPlan:
         return self.out
 
 
-def smcsd_resample(logw, *, eta=math.inf, scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0,
+def smcsd_resample(logw, *, eta=None, scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0,
                    prompt_base=0, uniforms=None, out: Outputs | None = None,
                    fields=("offspring", "slot_src", "ess", "lse", "wnorm", "n_ties"),
                    stream=None) -> Outputs:
-    """S4-S7 from fp32 log-weights [P][N]."""
+    """S4-S7 from fp32 log-weights [P][N].  eta: None = N/2 (reading G2), math.inf forces."""
+    if logw.dim() != 2:
+        raise ValueError("logw must be [P][N]")
     P, N = logw.shape
+    _chk(logw, "logw", _F32, (P, N), logw.device, optional=False)
+    _chk(uniforms, "uniforms", _U32, (P,) if scheme == SMCSD_SYSTEMATIC else (P, N), logw.device)
+    eta = _resolve_eta(eta, N)
     out = _alloc(out or Outputs(), logw.device, P, N, 1,
                  ("ancestors", "logw", "resampled", "status") + tuple(fields))
     rc = _lib.smcsd_resample(_p(logw), P, N, prompt_base, eta, scheme, seed & (2 ** 64 - 1),
@@ -359,6 +422,7 @@ def smcsd_weights_partial(logits_p, logits_q, tokens, *, v_begin, v_len=None, n_
     P, N, K = tokens.shape
     v_len = ld_p if v_len is None else v_len
     dev = logits_p.device
+    _check_inputs(dev, P, N, K, tokens=tokens, n_drafted=n_drafted)
     if partials is None:
         partials = _empty((P, 2, N, K, 4), torch.float32, dev)
     ws = _ws(workspace, dev, P, N, K, v_len, stream)
@@ -377,6 +441,8 @@ def smcsd_weights_combine(gathered, tokens, *, V, n_drafted=None, logw_prev=None
     G = gathered.shape[0]
     P, N, K = tokens.shape
     dev = gathered.device
+    _check_inputs(dev, P, N, K, tokens=tokens, n_drafted=n_drafted, logw_prev=logw_prev)
+    _chk(gathered, "gathered", _F32, (G, P, 2, N, K, 4), dev, optional=False)
     out = _alloc(out or Outputs(), dev, P, N, K, ("logw", "status") + tuple(fields))
     ws = _ws(workspace, dev, P, N, K, 1, stream)
     rc = _lib.smcsd_weights_combine(_p(gathered), G, _p(tokens), _p(n_drafted), _p(logw_prev),
@@ -392,6 +458,8 @@ def smcsd_select(logw, *, seed=0x5EED5EED, step=0, prompt_base=0, uniforms=None,
     """Terminal selection: one particle index per prompt (-1 if degenerate)."""
     P, N = logw.shape
     dev = logw.device
+    _chk(logw, "logw", _F32, (P, N), dev, optional=False)
+    _chk(uniforms, "uniforms", _U32, (P,), dev)
     selected = _empty((P,), torch.int32, dev) if selected is None else selected
     status = _empty((P,), torch.int32, dev) if status is None else status
     ws = _ws(workspace, dev, P, N, 1, 1, stream)
@@ -409,6 +477,7 @@ def smcsd_powersmc_weights(logits, *, V=None, logw_prev=None, alpha=1.0, inv_tem
     P, N = logits.shape[0], logits.shape[1]
     V = ld if V is None else V
     dev = logits.device
+    _chk(logw_prev, "logw_prev", _F32, (P, N), dev)
     out = out or Outputs()
     if out.logp_tok is None:
         out.logp_tok = _empty((P, N), torch.float32, dev)
@@ -453,7 +522,7 @@ def smcsd_ipc_close(ptr: int, handle: bytes):
 
 def smcsd_tp_step(logits_p, logits_q, tokens, *, V, v_begin, rank, G, xnseg, epoch, xpeer, xlocal,
                   v_len=None, n_drafted=None, logw_prev=None, alpha=1.0, inv_temp_p=1.0, inv_temp_q=1.0,
-                  eta=math.inf, scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0,
+                  eta=None, scheme=SMCSD_SYSTEMATIC, seed=0x5EED5EED, step=0, prompt_base=0,
                   uniforms=None, out: Outputs | None = None, fields=_ALL_S, workspace=None,
                   stream=None) -> Outputs:
     """S1 + fused peer-memory exchange (S10) + S2-S7 on this rank's vocabulary shard.
@@ -468,6 +537,11 @@ def smcsd_tp_step(logits_p, logits_q, tokens, *, V, v_begin, rank, G, xnseg, epo
     P, N, K = tokens.shape
     v_len = min(ld_p, V - v_begin) if v_len is None else v_len
     dev = logits_p.device
+    _check_inputs(dev, P, N, K, tokens=tokens, n_drafted=n_drafted, logw_prev=logw_prev,
+                  uniforms=uniforms, scheme=scheme)
+    if logits_q.device != dev or xlocal.device != dev or xpeer.device != dev:
+        raise ValueError("logits, xlocal and xpeer must be on one device")
+    eta = _resolve_eta(eta, N)
     out = _alloc(out or Outputs(), dev, P, N, K,
                  ("logw", "status", "ancestors", "resampled") + tuple(fields))
     ws = _ws(workspace, dev, P, N, K, v_len, stream)
@@ -489,6 +563,11 @@ def smcsd_kv_reindex_paged(table_src, n_pages_src, refcount, src_index, *, table
     """Paged (pointer) reindex: block-table rows + refcounts, no KV bytes."""
     P, N, MP = table_src.shape
     dev = table_src.device
+    _chk(table_src, "table_src", _I32, (P, N, MP), dev, optional=False)
+    _chk(n_pages_src, "n_pages_src", _I32, (P, N), dev, optional=False)
+    _chk(src_index, "src_index", _I32, (P, N), dev, optional=False)
+    if refcount.dtype != torch.int32 or refcount.device != dev or not refcount.is_contiguous():
+        raise ValueError("refcount must be a contiguous int32 tensor on the tables' device")
     table_dst = torch.empty_like(table_src) if table_dst is None else table_dst
     n_pages_dst = torch.empty_like(n_pages_src) if n_pages_dst is None else n_pages_dst
     status = _empty((P,), torch.int32, dev) if status is None else status
@@ -530,23 +609,36 @@ def kv_tensor(dst, src, *, n_outer, outer_stride, prompt_stride, particle_stride
                            seg_stride=seg_stride))
 
 
-def smcsd_kv_reindex_multi(tensors, src_index, *, stream=None):
+def smcsd_kv_reindex_multi(tensors, src_index, *, status=None, stream=None):
     """S8/S9 over several state tensors in one launch (per-layer K/V tensors, token history):
-    tensors is a list of kv_tensor(...) entries sharing src_index [P][N]."""
+    tensors is a list of kv_tensor(...) entries sharing src_index [P][N].  status (optional,
+    int32 [P]) receives ST_BAD_INDEX for a prompt with an out-of-range or hazardous index."""
     P, N = src_index.shape
+    _chk(src_index, "src_index", _I32, (P, N), src_index.device, optional=False)
+    _chk(status, "status", _I32, (P,), src_index.device)
     arr = (_KvTensor * len(tensors))()
     for k, (dst, src, g) in enumerate(tensors):
+        if dst.device != src_index.device or src.device != src_index.device:
+            raise ValueError("state tensors and src_index must be on one device")
         arr[k] = _KvTensor(_p(dst), _p(src), g["n_outer"], g["outer_stride"], g["prompt_stride"],
                            g["particle_stride"], g["seg_count"], g["seg_bytes"], g["seg_stride"])
-    rc = _lib.smcsd_kv_reindex_multi(arr, len(tensors), _p(src_index), P, N, _stream(stream))
+    rc = _lib.smcsd_kv_reindex_multi(arr, len(tensors), _p(src_index), P, N, _p(status),
+                                     _stream(stream))
     _check("smcsd_kv_reindex_multi", rc)
+    return status
 
 
 def smcsd_kv_reindex(dst, src, src_index, *, n_outer, outer_stride, prompt_stride,
-                     particle_stride, seg_count, seg_bytes, seg_stride, stream=None):
-    """S8/S9 block gather; pass dst is src for the in-place slot plan."""
+                     particle_stride, seg_count, seg_bytes, seg_stride, status=None, stream=None):
+    """S8/S9 block gather; pass dst is src for the in-place slot plan.  status: see
+    smcsd_kv_reindex_multi."""
     P, N = src_index.shape
+    _chk(src_index, "src_index", _I32, (P, N), src_index.device, optional=False)
+    _chk(status, "status", _I32, (P,), src_index.device)
+    if dst.device != src_index.device or src.device != src_index.device:
+        raise ValueError("dst, src and src_index must be on one device")
     rc = _lib.smcsd_kv_reindex(_p(dst), _p(src), n_outer, outer_stride, prompt_stride,
                                particle_stride, seg_count, seg_bytes, seg_stride, _p(src_index),
-                               P, N, _stream(stream))
+                               P, N, _p(status), _stream(stream))
     _check("smcsd_kv_reindex", rc)
+    return status

@@ -423,12 +423,13 @@ smcsd_rc smcsd_partials_rescale(const float *partials, const float *max_partials
 }
 
 smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
-                                const int32_t *src_index, int P, int N, void *stream) {
+                                const int32_t *src_index, int P, int N, uint32_t *status,
+                                void *stream) {
     if (!tensors || !src_index || n_tensors < 1 || n_tensors > kMaxKvTensors) return SMCSD_EINVAL;
     if (P < 1 || N < 1 || N > kTailMaxN) return SMCSD_EINVAL;
     KvParams prm;
     std::memset(&prm, 0, sizeof prm);
-    prm.idx = src_index; prm.P = P; prm.N = N; prm.n_tensors = n_tensors;
+    prm.idx = src_index; prm.P = P; prm.N = N; prm.n_tensors = n_tensors; prm.status = status;
     int64_t items = 0;
     for (int k = 0; k < n_tensors; ++k) {
         const smcsd_kv_tensor &a = tensors[k];
@@ -448,6 +449,7 @@ smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
         t.particle_stride = a.particle_stride; t.seg_stride = a.seg_stride;
         t.vps = (uint32_t)vps;
         t.in_place = a.dst == a.src;
+        prm.any_in_place |= t.in_place;
         t.vecs = (uint64_t)a.seg_count * vps;
         t.nchunks = (int64_t)cdiv((int64_t)t.vecs, kKvChunkVec);
         items += a.n_outer * P * t.nchunks;
@@ -460,10 +462,10 @@ smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
 smcsd_rc smcsd_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_stride,
                           int64_t prompt_stride, int64_t particle_stride, int64_t seg_count,
                           int64_t seg_bytes, int64_t seg_stride, const int32_t *src_index,
-                          int P, int N, void *stream) {
+                          int P, int N, uint32_t *status, void *stream) {
     const smcsd_kv_tensor t = {dst, src, n_outer, outer_stride, prompt_stride, particle_stride,
                                seg_count, seg_bytes, seg_stride};
-    return smcsd_kv_reindex_multi(&t, 1, src_index, P, N, stream);
+    return smcsd_kv_reindex_multi(&t, 1, src_index, P, N, status, stream);
 }
 
 smcsd_rc smcsd_select(const float *logw, int P, int N, int64_t prompt_base, uint64_t seed,
@@ -538,7 +540,7 @@ smcsd_rc smcsd_powersmc_weights(const void *logits, int64_t ld, int rows_per_par
 }
 
 size_t smcsd_tp_exchange_bytes(int P, int N, int K, int G, int xnseg) {
-    if (P < 1 || N < 1 || K < 1 || G < 1 || G > kXFlagBytes / 4 || xnseg < 1) return 0;
+    if (P < 1 || N < 1 || K < 1 || G < 1 || G > kXMaxG || xnseg < 1) return 0;
     return kXFlagBytes + 2 * x_half_elems(2 * P * N * K, G, xnseg) * sizeof(float4);
 }
 

@@ -31,6 +31,7 @@ namespace smcsd {
 constexpr uint32_t ST_DEGENERATE = 1u, ST_NOT_ABSCONT = 2u, ST_BAD_TOKEN = 4u, ST_NONFINITE = 8u;
 constexpr uint32_t ST_BAD_PAGE = 16u;
 constexpr uint32_t ST_EXCHANGE = 32u;                         // S10 peer flag wait timed out
+constexpr uint32_t ST_BAD_INDEX = 64u;                        // reindex: src_index out of range / hazard
 constexpr uint64_t kXTimeoutNs = 20000000000ull;              // 20 s
 #ifndef SMCSD_PHASE
 #define SMCSD_PHASE(i) do { } while (0)
@@ -392,6 +393,7 @@ struct StageMeta {
 };
 
 constexpr int kXMaxG = 32;                                  // S10: ranks of one exchange
+static_assert(kXMaxG <= kXEpochWord, "flag words of the ranks must not reach the epoch words");
 
 template <int DT, bool XP = false>
 constexpr size_t rowstats_smem_bytes() {
@@ -1825,7 +1827,9 @@ constexpr int kMaxKvTensors = 256;        // 256 x 72 B of __grid_constant__ par
 
 struct KvParams {
     const int32_t *idx;           // [P][N] src_index (ancestors, or the slot plan in place)
+    uint32_t *status;             // [P] or null: ST_BAD_INDEX per prompt (written by chunk 0)
     int P, N, n_tensors;
+    int any_in_place;             // some tensor is reindexed in place
     KvTensor t[kMaxKvTensors];
 };
 
@@ -1853,14 +1857,29 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex(const __grid_constant__
     const int32_t *idx = prm.idx + (int64_t)p * N;
     pdl_wait();                                                // src_index from the tail kernel
 
-    // ---- copy plan for prompt p: destinations grouped by source (counting sort)
-    for (int n = tid; n < N; n += kThreads) cnt[n] = 0;
-    __syncthreads();
+    // ---- copy plan for prompt p: destinations grouped by source (counting sort).  Entries
+    // outside [0, N) are skipped; an in-place plan in which some index is both a source and a
+    // destination (not hazard-free) is skipped whole.  Both raise ST_BAD_INDEX.
+    __shared__ int s_bad;
+    if (tid == 0) s_bad = 0;
     for (int n = tid; n < N; n += kThreads) {
-        const int s = idx[n];
-        if ((unsigned)s < (unsigned)N && (!in_place || s != n)) atomicAdd(&cnt[s], 1);
+        cnt[n] = 0;
+        srcs[n] = idx[n];                                      // staged copy (srcs is rebuilt below)
     }
     __syncthreads();
+    int bad = 0;
+    for (int n = tid; n < N; n += kThreads) {
+        const int s = srcs[n];
+        if ((unsigned)s >= (unsigned)N) bad |= 1;
+        else if (s != n && srcs[s] != s) bad |= 2;             // source s is itself overwritten
+        if ((unsigned)s < (unsigned)N && (!in_place || s != n)) atomicAdd(&cnt[s], 1);
+    }
+    if (bad) atomicOr(&s_bad, bad);
+    __syncthreads();
+    const int pbad = s_bad;
+    if (prm.status && lo == 0 && o == 0 && chunk == 0 && tid == 0)
+        prm.status[p] = ((pbad & 1) || ((pbad & 2) && prm.any_in_place)) ? ST_BAD_INDEX : 0u;
+    if (in_place && (pbad & 2)) return;                        // uniform across the CTA
     for (int n = tid; n < N; n += kThreads) {
         start[n] = cnt[n];
         fill[n] = cnt[n] > 0;

@@ -187,6 +187,9 @@ class TPExchange:
         self.device_epoch = device_epoch
         self._opened: list[int] = []
         self.xpeer = None
+        # this rank's own workspace: simulated ranks run concurrently on separate streams and
+        # must not share counters / partials (include/smcsd.h: no sharing by concurrent calls)
+        self.ws = smc.Workspace(self.device)
         if world is None:                      # multi-process: share handles, open peers
             torch.cuda.synchronize(self.device)
             handles = share_handles(smc.smcsd_ipc_export(self.buf), group)
@@ -212,6 +215,7 @@ class TPExchange:
         """One smcsd_tp_step: device-resident epoch (graph-capturable), or the host epoch
         advanced here (identical on every rank)."""
         self.epoch += 1
+        kw.setdefault("workspace", self.ws)
         return self.smc.smcsd_tp_step(logits_p_shard, logits_q_shard, tokens, V=self.V,
                                       v_begin=self.v_begin, v_len=self.v_len, rank=self.rank,
                                       G=self.G, xnseg=self.xnseg,

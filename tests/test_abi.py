@@ -98,7 +98,7 @@ def test_resample_and_kv_einval(lib):
     assert lib.smcsd_resample(*args(16, float("nan"), 0)) == 1   # NaN eta
     assert lib.smcsd_resample(*args(1025, 1.0, 1)) == 1          # multinomial, N > 1024
     assert lib.smcsd_resample(*args(16, 1.0, 7)) == 1            # unknown scheme
-    lib.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
+    lib.smcsd_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp, vp]
     lib.smcsd_kv_reindex.restype = i32
     ok = dict(dst=0x10000, src=0x20000, n_outer=4, outer=4096, prompt=2048, particle=512,
               segc=2, segb=256, segs=256)
@@ -106,7 +106,7 @@ def test_resample_and_kv_einval(lib):
         a = {**ok, **kw}
         return lib.smcsd_kv_reindex(a["dst"], a["src"], a["n_outer"], a["outer"], a["prompt"],
                                     a["particle"], a["segc"], a["segb"], a["segs"], 0x30000, 1, 4,
-                                    None)
+                                    None, None)
     assert kv(segb=100) == 1            # not a multiple of 16
     assert kv(dst=0x10008) == 1         # misaligned
     assert kv(particle=520) == 1
@@ -121,16 +121,17 @@ def test_kv_reindex_multi_rejects_bad_arguments(lib):
         _fields_ = [("dst", c.c_void_p), ("src", c.c_void_p)] + [
             (n, c.c_int64) for n in ("n_outer", "outer_stride", "prompt_stride", "particle_stride",
                                      "seg_count", "seg_bytes", "seg_stride")]
-    lib.smcsd_kv_reindex_multi.argtypes = [c.POINTER(T), c.c_int, c.c_void_p, c.c_int, c.c_int, c.c_void_p]
+    lib.smcsd_kv_reindex_multi.argtypes = [c.POINTER(T), c.c_int, c.c_void_p, c.c_int, c.c_int, c.c_void_p,
+                                           c.c_void_p]
     lib.smcsd_kv_reindex_multi.restype = c.c_int
     good = T(0x10000, 0x20000, 4, 4096, 2048, 512, 2, 256, 256)
     arr = (T * 2)(good, good)
-    assert lib.smcsd_kv_reindex_multi(arr, 0, 0x30000, 1, 4, None) == 1      # no tensors
-    assert lib.smcsd_kv_reindex_multi(arr, 257, 0x30000, 1, 4, None) == 1    # > 256 tensors
-    assert lib.smcsd_kv_reindex_multi(None, 1, 0x30000, 1, 4, None) == 1     # null list
-    assert lib.smcsd_kv_reindex_multi(arr, 2, None, 1, 4, None) == 1         # null src_index
+    assert lib.smcsd_kv_reindex_multi(arr, 0, 0x30000, 1, 4, None, None) == 1      # no tensors
+    assert lib.smcsd_kv_reindex_multi(arr, 257, 0x30000, 1, 4, None, None) == 1    # > 256 tensors
+    assert lib.smcsd_kv_reindex_multi(None, 1, 0x30000, 1, 4, None, None) == 1     # null list
+    assert lib.smcsd_kv_reindex_multi(arr, 2, None, 1, 4, None, None) == 1         # null src_index
     arr[1] = T(0x10000, 0x20008, 4, 4096, 2048, 512, 2, 256, 256)            # misaligned 2nd
-    assert lib.smcsd_kv_reindex_multi(arr, 2, 0x30000, 1, 4, None) == 1
+    assert lib.smcsd_kv_reindex_multi(arr, 2, 0x30000, 1, 4, None, None) == 1
     arr[1] = T(0x10000, 0x20000, 4, 4096, 2048, 512, 2, 100, 256)            # seg_bytes % 16
-    assert lib.smcsd_kv_reindex_multi(arr, 2, 0x30000, 1, 4, None) == 1
+    assert lib.smcsd_kv_reindex_multi(arr, 2, 0x30000, 1, 4, None, None) == 1
 

@@ -268,6 +268,33 @@ def test_forced_ties_resample_and_step(smc, orc):
     assert np_(gpu.ancestors)[0].tolist() == ref["ancestors"][0].tolist() == [0, 1, 2, 3]
 
 
+def test_default_eta_is_half_n_and_inputs_validated(smc, orc):
+    """The binding's default threshold is ESS < N/2 (reading G2), and wrongly
+    typed / shaped / placed inputs raise instead of being read as raw bytes (int64 tokens,
+    non-contiguous views, CPU tensors)."""
+    dev = torch.device("cuda")
+    P, N = 8, 16
+    lw = synth.random_logw(P, N, seed=4, sigma=1.5).numpy()
+    lw[0] = 0.0                                              # ESS = N: kept under N/2
+    lw[1] = -np.inf; lw[1, 3] = 0.0                          # ESS = 1: resampled
+    gpu = smc.smcsd_resample(torch.from_numpy(lw).to(dev))
+    torch.cuda.synchronize()
+    ref = orc.resample(lw, eta=N / 2)
+    assert np.array_equal(np_(gpu.resampled), ref["resampled"])
+    assert np_(gpu.resampled)[0] == 0 and np_(gpu.resampled)[1] == 1
+    assert np.array_equal(np_(gpu.ancestors), ref["ancestors"])
+    lp, lq, tok = synth.lm_logits(1, 4, 2, 1000, dtype=torch.float32, seed=8)
+    lpd, lqd = lp.to(dev), lq.to(dev)
+    with pytest.raises(ValueError):
+        smc.smcsd_step(lpd, lqd, tok.to(dev).long(), V=1000)         # int64 tokens
+    with pytest.raises(ValueError):
+        smc.smcsd_step(lpd, lqd, tok.to(dev), V=1000, logw_prev=torch.zeros(4, 1, device=dev).t())
+    with pytest.raises(ValueError):
+        smc.smcsd_step(lpd, lqd, tok, V=1000)                        # tokens on the host
+    with pytest.raises(ValueError):
+        smc.smcsd_resample(torch.zeros(2, 4, dtype=torch.float64, device=dev))
+
+
 def test_reset_value_table(smc):
     # fl32(-ln N), N = 1..1024, bitwise equal to the oracle's and Python's (PAPER.md:331)
     dev = torch.device("cuda")
@@ -434,6 +461,27 @@ def test_token_history_reindex(smc, orc):
     dst = torch.zeros_like(src)
     smc.smcsd_kv_reindex(dst, src, torch.from_numpy(r["ancestors"]).to(dev), **geom)
     want = np.stack([tok.numpy()[p][r["ancestors"][p]] for p in range(P)])
+    assert np.array_equal(dst.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("in_place", [False, True])
+def test_kv_reindex_invalid_index_status(smc, orc, in_place):
+    """ST_BAD_INDEX (reading G23) against the oracle, bytes included: out-of-range entries are
+    skipped; an in-place plan that overwrites one of its sources is skipped whole."""
+    dev = torch.device("cuda")
+    kv = synth.kv_bits((2, 2, 4, 6, 2, 16, 16), seed=3)
+    a = np.array([[1, 6, 2, -1, 4, 5], [0, 0, 1, 1, 4, 5], [5, 1, 2, 3, 4, 5],
+                  [0, 1, 2, 3, 4, 5]], np.int32)
+    geom = smc.kv_geometry(kv)
+    src = kv.to(dev)
+    dst = src if in_place else torch.zeros_like(src)
+    want = kv.numpy().copy() if in_place else np.zeros_like(kv.numpy())
+    st_ref = orc.kv_reindex(want, want if in_place else kv.numpy().copy(), a, **geom)
+    st = torch.full((4,), -1, dtype=torch.int32, device=dev)
+    smc.smcsd_kv_reindex(dst, src, torch.from_numpy(a).to(dev), status=st, **geom)
+    torch.cuda.synchronize()
+    assert np_(st).astype(np.uint32).tolist() == st_ref.tolist()
+    assert st_ref.tolist() == ([64, 64, 0, 0] if in_place else [64, 0, 0, 0])
     assert np.array_equal(dst.cpu().numpy(), want)
 
 
@@ -911,7 +959,7 @@ def test_step_at_abi_limits(smc, orc, P, N, K, V, dtype):
     g = torch.Generator().manual_seed(3)
     ndr = torch.randint(0, K + 1, (P, N), generator=g, dtype=torch.int32)
     out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, n_drafted=ndr.to(dev),
-                         logw_prev=prev.to(dev), step=4, seed=synth.PHILOX_SEED)
+                         logw_prev=prev.to(dev), eta=math.inf, step=4, seed=synth.PHILOX_SEED)
     torch.cuda.synchronize()
     ref = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, n_drafted=ndr.numpy(),
                       logw_prev=prev.numpy())

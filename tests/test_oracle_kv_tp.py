@@ -64,6 +64,28 @@ def test_kv_in_place_slot_plan(orc):
         assert key(out) == key(kv)
 
 
+def test_kv_invalid_index_policy(orc):
+    """Reading G23: an out-of-range entry is skipped (its destination untouched) and flags
+    ST_BAD_INDEX; an in-place plan whose source is itself a destination is not hazard-free
+    (SPEC.md:466-474 copies are defined only for a valid ancestor vector) -- the prompt is
+    flagged and left untouched.  Valid prompts of the same call are unaffected."""
+    src = _kv(1, 3, 4, 1, 4, 16, seed=5)
+    dst = np.zeros_like(src)
+    a = np.array([[1, 4, 2, -1], [0, 0, 1, 1], [3, 3, 3, 3]], np.int32)
+    st = orc.kv_reindex(dst, src, a, **_geom(src))
+    assert st.tolist() == [orc.ST_BAD_INDEX, 0, 0]
+    assert np.array_equal(dst[:, :, 0, 0], src[:, :, 0, 1]) and np.array_equal(dst[:, :, 0, 2], src[:, :, 0, 2])
+    assert np.all(dst[:, :, 0, 1] == 0) and np.all(dst[:, :, 0, 3] == 0)       # skipped entries
+    assert np.array_equal(dst[:, :, 1], src[:, :, 1][:, :, [0, 0, 1, 1]])
+    # out-of-place, [0,0,1,1] is a fine ancestor vector; in place it overwrites source 1
+    kv = _kv(1, 2, 4, 1, 4, 16, seed=6)
+    before = kv.copy()
+    st = orc.kv_reindex(kv, kv, np.array([[0, 0, 1, 1], [0, 0, 2, 3]], np.int32), **_geom(kv))
+    assert st.tolist() == [orc.ST_BAD_INDEX, 0]
+    assert np.array_equal(kv[:, :, 0], before[:, :, 0])                          # untouched
+    assert np.array_equal(kv[:, :, 1], before[:, :, 1][:, :, [0, 0, 2, 3]])
+
+
 def test_tp_partials_merge_to_unsharded(orc):
     rng = np.random.default_rng(4)
     V = 1000
