@@ -288,7 +288,7 @@ def test_default_eta_is_half_n_and_inputs_validated(smc, orc):
     with pytest.raises(ValueError):
         smc.smcsd_step(lpd, lqd, tok.to(dev).long(), V=1000)         # int64 tokens
     with pytest.raises(ValueError):
-        smc.smcsd_step(lpd, lqd, tok.to(dev), V=1000, logw_prev=torch.zeros(4, 1, device=dev).t())
+        smc.smcsd_step(lpd, lqd, tok.to(dev), V=1000, logw_prev=torch.zeros(1, 8, device=dev)[:, ::2])
     with pytest.raises(ValueError):
         smc.smcsd_step(lpd, lqd, tok, V=1000)                        # tokens on the host
     with pytest.raises(ValueError):
