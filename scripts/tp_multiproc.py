@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Two (or more) processes, ONE GPU, CUDA IPC: the fused TP step (smcsd_tp_step) with a real
-cross-process exchange (IPC-mapped buffers, time-sliced contexts).  Checks every rank gets
+"""Two (or more) processes, one GPU each (or all on cuda:0 of a 1-GPU box), CUDA IPC: the fused
+TP step (smcsd_tp_step) with a real cross-process exchange (IPC-mapped peer buffers).  Checks every rank gets
 bit-identical results and that they match the single-process smcsd_step within 1e-4.
 Launch: torchrun --nproc-per-node 2 scripts/tp_multiproc.py   (gloo for the plumbing)."""
 import math
@@ -19,7 +19,10 @@ from paper_2604_15672_b200.dist import TPExchange
 def main():
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
-    dev = torch.device("cuda:0")
+    # one device per rank when the box has them (real NVLink P2P between ranks); on a 1-GPU box
+    # every rank shares cuda:0 (time-sliced contexts, the IPC path still crosses processes)
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dev = torch.device("cuda", local % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     P, N, K, V = 1, 16, 4, 50000
     pad = torch.empty(12345 + 777 * rank, dtype=torch.uint8, device=dev)  # buffer at an offset

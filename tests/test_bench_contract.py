@@ -12,9 +12,10 @@ BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_ste
              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
 
 
-def _run(args, timeout):
+def _run(args, timeout, env=None):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT,
-                       capture_output=True, text=True, timeout=timeout)
+                       capture_output=True, text=True, timeout=timeout,
+                       env={**os.environ, **(env or {})})
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1, r.stdout
@@ -43,3 +44,32 @@ def test_our_arm_line():
     assert d["e2e"]["h2d_bytes_per_step"] > 60e6 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["config"]["workload"].startswith("cfg2")
+
+
+def test_gpus_n_self_launches_ranks():
+    """`bench.py --gpus 2` with no torchrun wrapper launches 2 ranks itself (the reference arm:
+    CPU only, gloo plumbing); rank 0 prints the one line with n_gpus = 2."""
+    d = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3"], 600)
+    assert d["n_gpus"] == 2 and d["impl"] == "reference" and d["value"] > 0
+
+
+def test_world_size_mismatch_is_an_error():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--gpus", "4", "--steps", "1"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=120, env={**os.environ, "WORLD_SIZE": "2", "RANK": "0"})
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr
+
+
+@pytest.mark.gpu
+def test_our_arm_two_ranks_self_launched():
+    """Our arm at --gpus 2 without a wrapper; on a 1-GPU box the ranks share cuda:0 over gloo
+    (SMCSD_BENCH_BACKEND=gloo: a functional check, not a bench value)."""
+    env = {} if torch_gpus() >= 2 else {"SMCSD_BENCH_BACKEND": "gloo"}
+    d = _run(["--gpus", "2", "--steps", "3", "--warmup", "3", "--no-secondary", "--no-cpu-baseline"],
+             900, env=env)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "dp2 (prompts)"
+
+
+def torch_gpus():
+    import torch
+    return torch.cuda.device_count()
