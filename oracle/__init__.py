@@ -20,7 +20,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "smcsd_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
-_lib = None
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")     # timing-only build (-fopenmp)
+_libs = {}
+_threads = 1
 
 ST_DEGENERATE = 1
 ST_NOT_ABSCONT = 2
@@ -31,20 +33,31 @@ ST_BAD_INDEX = 64
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (no fast-math, no FMA contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-               "-shared", "-o", _LIB + ".tmp", _SRC, "-lm"]
-        subprocess.run(cmd, check=True)
-        os.replace(_LIB + ".tmp", _LIB)
+    """Compile the oracle with gcc (no fast-math, no FMA contraction): liboracle.so (plain,
+    single-threaded) and liboracle_omp.so (the same source with -fopenmp, timing only)."""
+    for out, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+            cmd = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+                   *extra, "-shared", "-o", out + ".tmp", _SRC, "-lm"]
+            subprocess.run(cmd, check=True)
+            os.replace(out + ".tmp", out)
     return _LIB
 
 
+def set_threads(n: int) -> int:
+    """Select the plain build (n = 1) or the OpenMP timing build with n threads (n > 1) for
+    the following calls.  Returns the threads the selected build will use."""
+    global _threads
+    _threads = max(1, int(n))
+    L = lib()
+    return int(L.orc_set_threads(_threads)) if _threads > 1 else 1
+
+
 def lib():
-    global _lib
-    if _lib is None:
+    key = "omp" if _threads > 1 else "plain"
+    if key not in _libs:
         build()
-        L = ctypes.CDLL(_LIB)
+        L = ctypes.CDLL(_LIB_OMP if key == "omp" else _LIB)
         vp, i64, i32, dbl, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_uint64
         L.orc_philox4x32_10.argtypes = [vp, vp, vp]
         L.orc_row_logprob.argtypes = [vp, i32, i64, dbl, i64, vp]
@@ -64,8 +77,10 @@ def lib():
                                 vp, vp, vp, vp, vp, vp]
         L.orc_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
         L.orc_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
-        _lib = L
-    return _lib
+        L.orc_set_threads.argtypes = [i32]
+        L.orc_set_threads.restype = i32
+        _libs[key] = L
+    return _libs[key]
 
 
 def _ptr(a):

@@ -14,6 +14,9 @@
  *
  * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -shared -fPIC -lm
  * (-ffp-contract=off: no fused multiply-add, so every fp64 op is one IEEE rounding.)
+ * A second, timing-only build adds -fopenmp (liboracle_omp.so): the row pass of S1+S2 and the
+ * KV copy planes run on several threads; every row / block is computed exactly as above, so
+ * its outputs are bit-identical (tests/test_oracle_weights.py checks it).
  *
  * Pinned by tests/test_oracle_*.py (see DESIGN.md section 4 for the pin table).
  * Parity unpinned: nothing here.  Multi-round composition (R rounds of weights, resample, bonus,
@@ -21,7 +24,24 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Timing-only build (liboracle_omp.so, -fopenmp): threads for the row-parallel S1+S2 pass
+ * and the KV copy planes.  The plain build (liboracle.so) is single-threaded. */
+int orc_set_threads(int n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
 
 /* Status bits (the ABI contract, retyped here from DESIGN.md section 2; no shared header). */
 #define ORC_ST_DEGENERATE  1u  /* every log-weight of the prompt is -inf           */
@@ -198,6 +218,47 @@ static int s4_normalise(const float *lam, int N, double *e, double *Pcum,
 /* logp_tok/logq_tok (optional, [P][N][K] fp64): ell per row; 0 for rows j >= k_n, NaN   */
 /* for invalid rows.  wnorm (optional [P][N] fp64): e_n / S.                              */
 /* ------------------------------------------------------------------------------------ */
+/* Pass 1 of orc_weights: S1+S2 of every scored row (p, n, j < k_n).  Rows are independent,
+ * so the timing-only build (liboracle_omp.so, -fopenmp) runs them on several threads; the
+ * plain build ignores the pragma.  Each row's arithmetic is the same either way.
+ * code[row]: -1 unread (j >= k_n or invalid k_n), 0 ok, 1 bad token, 2 non-finite row,
+ * 3 q(d) = 0. */
+static void s12_rows(const void *logits_p, int64_t ld_p, int rpp_p, const void *logits_q,
+                     int64_t ld_q, int rpp_q, int dtype, const int32_t *tokens,
+                     const int32_t *n_drafted, int P, int N, int K, int64_t V, double tau_p,
+                     double tau_q, double *lp_out, double *lq_out, int *code)
+{
+    size_t esz = dtype == 1 ? 2 : 4;
+    int64_t rows = (int64_t)P * N * K;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t r = 0; r < rows; ++r) {
+        int64_t pn = r / K;
+        int j = (int)(r - pn * K);
+        int k_n = n_drafted ? n_drafted[pn] : K;
+        if (k_n < 0 || k_n > K) k_n = 0;
+        double lp = 0.0, lq = 0.0;
+        int c = -1;
+        if (j < k_n) {
+            int64_t d = tokens[pn * K + j];
+            if (d < 0 || d >= V) {
+                c = 1;
+                lp = NAN;
+                lq = NAN;
+            } else {
+                const char *rp = (const char *)logits_p + ((pn * rpp_p + j) * ld_p) * (int64_t)esz;
+                const char *rq = (const char *)logits_q + ((pn * rpp_q + j) * ld_q) * (int64_t)esz;
+                uint32_t fp, fq;
+                lp = orc_row_logprob(rp, dtype, V, tau_p, d, &fp);
+                lq = orc_row_logprob(rq, dtype, V, tau_q, d, &fq);
+                c = (fp | fq) ? 2 : (lq == -INFINITY ? 3 : 0);
+            }
+        }
+        lp_out[r] = lp;
+        lq_out[r] = lq;
+        code[r] = c;
+    }
+}
+
 void orc_weights(const void *logits_p, int64_t ld_p, int rpp_p,
                  const void *logits_q, int64_t ld_q, int rpp_q, int dtype,
                  const int32_t *tokens, const int32_t *n_drafted, const float *logw_prev,
@@ -206,7 +267,12 @@ void orc_weights(const void *logits_p, int64_t ld_p, int rpp_p,
                  double *lse_out, double *ess_out, double *wnorm, uint32_t *status,
                  double *scratch /* 2*N doubles */)
 {
-    size_t esz = dtype == 1 ? 2 : 4;
+    int64_t rows = (int64_t)P * N * K;
+    double *lp_all = logp_tok ? logp_tok : (double *)malloc((size_t)rows * sizeof(double));
+    double *lq_all = logq_tok ? logq_tok : (double *)malloc((size_t)rows * sizeof(double));
+    int *code = (int *)malloc((size_t)(rows > 0 ? rows : 1) * sizeof(int));
+    s12_rows(logits_p, ld_p, rpp_p, logits_q, ld_q, rpp_q, dtype, tokens, n_drafted, P, N, K, V,
+             tau_p, tau_q, lp_all, lq_all, code);
     for (int p = 0; p < P; ++p) {
         uint32_t st = 0;
         for (int n = 0; n < N; ++n) {
@@ -219,34 +285,20 @@ void orc_weights(const void *logits_p, int64_t ld_p, int rpp_p,
                 k_n = 0;
             }
             double delta = 0.0;
-            for (int j = 0; j < K; ++j) {
-                double lp = 0.0, lq = 0.0;
-                if (j < k_n) {
-                    int64_t d = tokens[pn * K + j];
-                    if (d < 0 || d >= V) {
-                        st |= ORC_ST_BAD_TOKEN;
-                        bad = 1;
-                        lp = NAN;
-                        lq = NAN;
-                    } else {
-                        const char *rp = (const char *)logits_p + ((pn * rpp_p + j) * ld_p) * (int64_t)esz;
-                        const char *rq = (const char *)logits_q + ((pn * rpp_q + j) * ld_q) * (int64_t)esz;
-                        uint32_t fp, fq;
-                        lp = orc_row_logprob(rp, dtype, V, tau_p, d, &fp);
-                        lq = orc_row_logprob(rq, dtype, V, tau_q, d, &fq);
-                        if (fp | fq) {
-                            st |= ORC_ST_NONFINITE;
-                            bad = 1;
-                        } else if (lq == -INFINITY) {
-                            st |= ORC_ST_NOT_ABSCONT;
-                            bad = 1;
-                        } else {
-                            delta = delta + (alpha * lp - lq);
-                        }
-                    }
+            for (int j = 0; j < k_n; ++j) {
+                int64_t r = pn * K + j;
+                if (code[r] == 1) {
+                    st |= ORC_ST_BAD_TOKEN;
+                    bad = 1;
+                } else if (code[r] == 2) {
+                    st |= ORC_ST_NONFINITE;
+                    bad = 1;
+                } else if (code[r] == 3) {
+                    st |= ORC_ST_NOT_ABSCONT;
+                    bad = 1;
+                } else {
+                    delta = delta + (alpha * lp_all[r] - lq_all[r]);
                 }
-                if (logp_tok) logp_tok[pn * K + j] = lp;
-                if (logq_tok) logq_tok[pn * K + j] = lq;
             }
             float prev = logw_prev ? logw_prev[pn] : (float)(-log((double)N));
             if (isnan(prev) || prev == INFINITY) {
@@ -270,6 +322,9 @@ void orc_weights(const void *logits_p, int64_t ld_p, int rpp_p,
         }
         if (status) status[p] = st;
     }
+    free(code);
+    if (!logq_tok) free(lq_all);
+    if (!logp_tok) free(lp_all);
 }
 
 /* ------------------------------------------------------------------------------------ */
@@ -742,6 +797,7 @@ void orc_kv_reindex(void *dst, const void *src, int64_t n_outer, int64_t outer_s
         }
         if (status) status[p] = (oob || (in_place && hazard)) ? ORC_ST_BAD_INDEX : 0u;
         if (in_place && hazard) continue;
+#pragma omp parallel for schedule(static)
         for (int64_t o = 0; o < n_outer; ++o)
             for (int n = 0; n < N; ++n) {
                 int s = idx[n];

@@ -245,3 +245,21 @@ def test_powersmc_matches_scipy(orc):
         for n in range(3):
             lp = log_softmax(tau * lg[0, n, 0].astype(np.float64))
             assert out["inc"][0, n] == pytest.approx(logsumexp(a * lp), abs=1e-10)
+
+
+def test_openmp_timing_build_is_bit_identical(orc):
+    """liboracle_omp.so (the timing-only -fopenmp build used by bench.py's cpu_baseline) gives
+    the same bits as the plain build: the rows of S1+S2 are independent and S3/S4 stay serial."""
+    import torch
+    import synth
+    lp, lq, tok = synth.lm_logits(3, 9, 5, 20001, dtype=torch.bfloat16, seed=12)
+    u16 = lambda t: t.view(torch.int16).numpy().view(np.uint16)
+    nd = np.array([[5, 0, 3, 5, 5, 9, 5, 1, 5]] * 3, np.int32)
+    a = orc.weights(u16(lp), u16(lq), tok.numpy(), n_drafted=nd, alpha=1.5)
+    try:
+        assert orc.set_threads(4) >= 1
+        b = orc.weights(u16(lp), u16(lq), tok.numpy(), n_drafted=nd, alpha=1.5)
+    finally:
+        orc.set_threads(1)
+    for k in a:
+        assert np.array_equal(a[k], b[k], equal_nan=True), k
