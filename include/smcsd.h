@@ -264,6 +264,46 @@ SMCSD_API smcsd_rc smcsd_kv_reindex_paged(const int32_t *table_src, const int32_
                                           const int32_t *src_index, int P, int N, int max_pages,
                                           int num_pages, uint32_t *status, void *stream);
 
+/* Paged append with copy-on-write (NEXT #1; Sec. 3.3 Obs. 2: resampling
+ * shares the ancestor's pages, so the first write after a resample must not land in a page
+ * another particle sees; SPEC.md:466-470 append_tokens; reading G24).  Defined sequentially in
+ * (p, n) order; particle n appends n_new[p][n] tokens (e.g. its K + 1 new tokens):
+ *   f = seq_len mod page_size (filled tokens of a partial tail page, 0 = none);
+ *   if n_new > 0, f > 0 and refcount[tail] > 1 (shared, e.g. after smcsd_kv_reindex_paged):
+ *     copy-on-write -- a fresh page c receives the tail's f filled tokens (only those: full
+ *     pages are immutable and never copied), refcount[tail] -= 1, refcount[c] = 1, and c
+ *     replaces the tail in the particle's table;  otherwise the tail is filled in place;
+ *   fresh pages (refcount 1) take the remaining tokens; every fresh page is the LOWEST-id page
+ *   whose refcount is 0 (the free pool is the set of refcount-0 pages: smcsd_kv_reindex_paged
+ *   releases pages by bringing their refcount to 0);
+ *   slot_mapping[p][n][j] = page * page_size + offset where new token j's KV goes (-1 for
+ *   j >= n_new, up to max_new); seq_len += n_new; n_pages updated.
+ * table [P][N][max_pages], n_pages / seq_len / n_new [P][N], refcount [num_pages] (device,
+ * int32, updated in place).  cow_src / cow_dst / cow_tokens [P][N]: the copy-on-write list
+ * (-1 / -1 / 0 where none).  pools: HOST array of n_pools (0..64) KV pool descriptors whose
+ * copy-on-write content is copied on the device (bytes: plane o of page g starts at
+ * base + o * plane_stride + g * page_stride, token t at + t * token_bytes; all multiples of 16).
+ * All-or-nothing: if any particle's state is invalid (page id outside [0, num_pages) or with
+ * refcount < 1, n_pages != ceil(seq_len / page_size), n_new outside [0, max_new], more than
+ * max_pages pages) its prompt gets SMCSD_ST_BAD_PAGE; if fewer pages are free than the call
+ * needs every prompt gets SMCSD_ST_OUT_OF_PAGES; then *result (device int32) = 1 and nothing
+ * is modified (slot_mapping and the copy list are not written).  *result = 0 on success.
+ * workspace: smcsd_kv_append_workspace_bytes(P, N, num_pages, max_pages) bytes, zeroed once
+ * (smcsd_workspace_init) -- the call leaves it zeroed.  num_pages * page_size < 2^31. */
+typedef struct {
+    void *base;
+    int64_t n_planes, plane_stride, page_stride, token_bytes;
+} smcsd_kv_pool;
+#define SMCSD_ST_OUT_OF_PAGES 128u
+SMCSD_API size_t smcsd_kv_append_workspace_bytes(int P, int N, int num_pages, int max_pages);
+SMCSD_API smcsd_rc smcsd_kv_append_paged(int32_t *table, int32_t *n_pages, int32_t *seq_len,
+                                         int32_t *refcount, const int32_t *n_new, int P, int N,
+                                         int max_pages, int num_pages, int page_size, int max_new,
+                                         int32_t *slot_mapping, int32_t *cow_src, int32_t *cow_dst,
+                                         int32_t *cow_tokens, uint32_t *status, int32_t *result,
+                                         const smcsd_kv_pool *pools, int n_pools, void *workspace,
+                                         size_t workspace_bytes, void *stream);
+
 /* PowerSMC weights (App. F): K = 1, no bonus token, draft = target.  Row 0
  * of each particle (rows_per_particle >= 1) gives p = softmax(inv_temp * z) and the weight
  * increment log w = ln sum_v p_v^alpha; lam' = fl32(lam_prev + log w), then

@@ -30,6 +30,7 @@ ST_BAD_TOKEN = 4
 ST_NONFINITE = 8
 ST_BAD_PAGE = 16
 ST_BAD_INDEX = 64
+ST_OUT_OF_PAGES = 128
 
 
 def build(force: bool = False) -> str:
@@ -77,6 +78,9 @@ def lib():
                                 vp, vp, vp, vp, vp, vp]
         L.orc_kv_reindex.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp, i32, i32, vp]
         L.orc_kv_reindex_paged.argtypes = [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
+        L.orc_kv_append_paged.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp, vp,
+                                          vp, vp, vp, vp]
+        L.orc_paged_cow_copy.argtypes = [vp, i64, i64, i64, i64, vp, vp, vp, i64]
         L.orc_set_threads.argtypes = [i32]
         L.orc_set_threads.restype = i32
         _libs[key] = L
@@ -251,6 +255,39 @@ def kv_reindex_paged(table, n_pages, refcount, src_index, *, num_pages=None):
     lib().orc_kv_reindex_paged(_ptr(t), _ptr(npg), _ptr(out["table"]), _ptr(out["n_pages"]),
                                _ptr(rc), _ptr(out["freed"]), _ptr(idx), P, N, MP, num_pages,
                                _ptr(out["status"]))
+    return out
+
+
+def kv_append_paged(table, n_pages, seq_len, refcount, n_new, *, page_size, max_new=None,
+                    pools=()):
+    """Paged append with copy-on-write oracle (NEXT #1; PAPER.md:488-490, SPEC.md:466-470,
+    reading G24).  Arrays are copied, never modified in place: returns a dict with the new
+    table / n_pages / seq_len / refcount, slot_mapping [P][N][max_new], cow_src / cow_dst /
+    cow_tokens [P][N], status [P] and result (0 ok, 1 nothing changed).  pools: iterable of
+    (uint8 array, n_planes, plane_stride, page_stride, token_bytes) KV pools whose copy-on-write
+    content is copied in place."""
+    t = np.ascontiguousarray(table, dtype=np.int32).copy()
+    P, N, MP = t.shape
+    npg = np.ascontiguousarray(n_pages, dtype=np.int32).copy()
+    sl = np.ascontiguousarray(seq_len, dtype=np.int32).copy()
+    rc = np.ascontiguousarray(refcount, dtype=np.int32).copy()
+    nn = np.ascontiguousarray(n_new, dtype=np.int32)
+    max_new = int(nn.max()) if max_new is None else int(max_new)
+    max_new = max(max_new, 1)
+    out = dict(table=t, n_pages=npg, seq_len=sl, refcount=rc,
+               slot_mapping=np.zeros((P, N, max_new), np.int32), cow_src=np.zeros((P, N), np.int32),
+               cow_dst=np.zeros((P, N), np.int32), cow_tokens=np.zeros((P, N), np.int32),
+               status=np.zeros(P, np.uint32), result=np.zeros(1, np.int32))
+    lib().orc_kv_append_paged(_ptr(t), _ptr(npg), _ptr(sl), _ptr(rc), _ptr(nn), P, N, MP, rc.size,
+                              int(page_size), max_new, _ptr(out["slot_mapping"]), _ptr(out["cow_src"]),
+                              _ptr(out["cow_dst"]), _ptr(out["cow_tokens"]), _ptr(out["status"]),
+                              _ptr(out["result"]))
+    out["result"] = int(out["result"][0])
+    if out["result"] == 0:
+        for pool, n_planes, plane_stride, page_stride, token_bytes in pools:
+            lib().orc_paged_cow_copy(_ptr(pool), n_planes, plane_stride, page_stride, token_bytes,
+                                     _ptr(out["cow_src"]), _ptr(out["cow_dst"]),
+                                     _ptr(out["cow_tokens"]), P * N)
     return out
 
 

@@ -769,6 +769,144 @@ void orc_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages_src, 
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* Paged append with copy-on-write (NEXT #1, the other half of the paper's mechanism:       */
+/* PAPER.md:488-490, Sec. 3.3 Obs. 2 -- duplicated particles share their ancestor's pages;   */
+/* SPEC.md:466-470 append_tokens: "fills the particle's last page if it has exclusive        */
+/* ownership (refcount 1); otherwise performs copy-on-write of the partial tail page ...,    */
+/* then allocates fresh pages"; full pages are immutable and never copied).  Reading G24.    */
+/* Particles are processed one at a time in (p, n) order; particle n appends n_new tokens:  */
+/*   f = seq_len mod page_size (tokens in a partial tail page; 0 = no partial page);        */
+/*   if n_new > 0, f > 0 and refcount[tail] > 1: copy-on-write -- a fresh page c takes the   */
+/*     tail's f filled tokens (cow_src/dst/tokens record it), refcount[tail] -= 1,           */
+/*     refcount[c] = 1, the table's last entry becomes c;                                    */
+/*   the tail's free slots take the first new tokens, then fresh pages (refcount 1) are      */
+/*   appended for the rest; every fresh page is the LOWEST-id page with refcount 0;         */
+/*   slot_mapping[p][n][j] = page * page_size + offset of new token j (-1 for j >= n_new);   */
+/*   seq_len += n_new, n_pages updated.                                                      */
+/* The call is all-or-nothing: if any particle's state is invalid (page id out of range or   */
+/* with refcount < 1, n_pages != ceil(seq_len / page_size), n_new < 0 or > max_new, or the   */
+/* list would exceed max_pages) its prompt gets ORC_ST_BAD_PAGE; if the pool has fewer free  */
+/* pages than the call needs every prompt gets ORC_ST_OUT_OF_PAGES; then *result = 1 and     */
+/* nothing changes.  No page is freed here (copy-on-write only leaves shared pages).         */
+/* ------------------------------------------------------------------------------------ */
+#define ORC_ST_OUT_OF_PAGES 128u
+static int lowest_free(const int32_t *refcount, int num_pages, int from)
+{
+    for (int pg = from; pg < num_pages; ++pg)
+        if (refcount[pg] == 0) return pg;
+    return -1;
+}
+
+void orc_kv_append_paged(int32_t *table, int32_t *n_pages, int32_t *seq_len, int32_t *refcount,
+                         const int32_t *n_new, int P, int N, int max_pages, int num_pages,
+                         int page_size, int max_new, int32_t *slot_mapping, int32_t *cow_src,
+                         int32_t *cow_dst, int32_t *cow_tokens, uint32_t *status, int32_t *result)
+{
+    int ok = 1;
+    int64_t need_total = 0;
+    /* simulated refcounts of the tails for the copy-on-write decisions (sequential order) */
+    for (int p = 0; p < P; ++p) {
+        status[p] = 0;
+        for (int n = 0; n < N; ++n) {
+            int64_t pn = (int64_t)p * N + n;
+            int len = seq_len[pn], np_ = n_pages[pn], add = n_new[pn];
+            int bad = len < 0 || np_ < 0 || np_ > max_pages || add < 0 || add > max_new ||
+                      np_ != (len + page_size - 1) / page_size;
+            for (int i = 0; !bad && i < np_; ++i) {
+                int pg = table[pn * max_pages + i];
+                if (pg < 0 || pg >= num_pages || refcount[pg] < 1) bad = 1;
+            }
+            if (!bad) {
+                int f = len % page_size;
+                int room = f ? page_size - f : 0;
+                int fresh = add > room ? (add - room + page_size - 1) / page_size : 0;
+                if (np_ + fresh > max_pages) bad = 1;
+            }
+            if (bad) { status[p] |= ORC_ST_BAD_PAGE; ok = 0; }
+        }
+    }
+    if (ok) {
+        /* pages the call needs, in the sequential semantics */
+        int32_t *rc = (int32_t *)malloc((size_t)num_pages * sizeof(int32_t));
+        memcpy(rc, refcount, (size_t)num_pages * sizeof(int32_t));
+        for (int64_t pn = 0; pn < (int64_t)P * N; ++pn) {
+            int len = seq_len[pn], add = n_new[pn];
+            if (add == 0) continue;
+            int f = len % page_size;
+            int room = f ? page_size - f : 0;
+            if (f && rc[table[pn * max_pages + n_pages[pn] - 1]] > 1) {
+                rc[table[pn * max_pages + n_pages[pn] - 1]] -= 1;
+                need_total += 1;
+            }
+            need_total += add > room ? (add - room + page_size - 1) / page_size : 0;
+        }
+        free(rc);
+        int64_t free_pages = 0;
+        for (int pg = 0; pg < num_pages; ++pg) free_pages += refcount[pg] == 0;
+        if (need_total > free_pages) {
+            for (int p = 0; p < P; ++p) status[p] |= ORC_ST_OUT_OF_PAGES;
+            ok = 0;
+        }
+    }
+    *result = ok ? 0 : 1;
+    if (!ok) return;
+    int cursor = 0;                    /* pages below it are all in use (lowest-id allocation) */
+    for (int p = 0; p < P; ++p)
+        for (int n = 0; n < N; ++n) {
+            int64_t pn = (int64_t)p * N + n;
+            int32_t *row = table + pn * max_pages;
+            int len = seq_len[pn], add = n_new[pn];
+            int f = len % page_size;
+            cow_src[pn] = -1;
+            cow_dst[pn] = -1;
+            cow_tokens[pn] = 0;
+            for (int j = 0; j < max_new; ++j) slot_mapping[pn * max_new + j] = -1;
+            if (add == 0) continue;
+            if (f && refcount[row[n_pages[pn] - 1]] > 1) {           /* copy-on-write */
+                int t = row[n_pages[pn] - 1];
+                int c = lowest_free(refcount, num_pages, cursor);
+                cursor = c + 1;
+                refcount[t] -= 1;
+                refcount[c] = 1;
+                row[n_pages[pn] - 1] = c;
+                cow_src[pn] = t;
+                cow_dst[pn] = c;
+                cow_tokens[pn] = f;
+            }
+            for (int j = 0; j < add; ++j) {
+                int pos = len + j;                                   /* token position */
+                int pi = pos / page_size, off = pos % page_size;
+                if (pi >= n_pages[pn]) {                             /* a fresh page */
+                    int c = lowest_free(refcount, num_pages, cursor);
+                    cursor = c + 1;
+                    refcount[c] = 1;
+                    row[pi] = c;
+                    n_pages[pn] = pi + 1;
+                }
+                slot_mapping[pn * max_new + j] = row[pi] * page_size + off;
+            }
+            seq_len[pn] = len + add;
+        }
+}
+
+/* The content copies of orc_kv_append_paged's copy-on-write list for one KV pool: for every  */
+/* particle with cow_dst >= 0 and every plane o (e.g. L x {K, V}), the first cow_tokens       */
+/* tokens of page cow_src are copied to page cow_dst:                                          */
+/*   base + o*plane_stride + page*page_stride + [0, tokens * token_bytes)   (bytes).          */
+void orc_paged_cow_copy(void *pool, int64_t n_planes, int64_t plane_stride, int64_t page_stride,
+                        int64_t token_bytes, const int32_t *cow_src, const int32_t *cow_dst,
+                        const int32_t *cow_tokens, int64_t count)
+{
+    for (int64_t i = 0; i < count; ++i) {
+        if (cow_dst[i] < 0) continue;
+        for (int64_t o = 0; o < n_planes; ++o)
+            memcpy((char *)pool + o * plane_stride + (int64_t)cow_dst[i] * page_stride,
+                   (const char *)pool + o * plane_stride + (int64_t)cow_src[i] * page_stride,
+                   (size_t)(cow_tokens[i] * token_bytes));
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* S8/S9: reindex per-particle state to the ancestor's (Alg. 1: x^(n) <- x^(a_n) d^(a_n) */
 /* x+_(a_n)).  Block (o, p, n) = seg_count segments of seg_bytes bytes at  */
 /* base + o*outer_stride + p*prompt_stride + n*particle_stride + s*seg_stride.           */

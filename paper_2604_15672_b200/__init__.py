@@ -25,14 +25,15 @@ __all__ = [
     "smcsd_version", "kv_geometry", "smcsd_select", "smcsd_kv_reindex_paged", "ST_BAD_PAGE",
     "smcsd_powersmc_weights", "smcsd_tp_exchange_bytes", "smcsd_tp_exchange_init",
     "smcsd_ipc_handle_bytes", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close", "smcsd_tp_step",
-    "ST_EXCHANGE", "ST_BAD_INDEX",
+    "ST_EXCHANGE", "ST_BAD_INDEX", "ST_OUT_OF_PAGES", "smcsd_kv_append_paged", "kv_pool",
+    "paged_pool_geometry", "AppendOutputs", "smcsd_kv_append_workspace_bytes",
 ]
 
 SMCSD_F32, SMCSD_BF16 = 0, 1
 SMCSD_SYSTEMATIC, SMCSD_MULTINOMIAL = 0, 1
 SEGMENT = 8192
 ST_DEGENERATE, ST_NOT_ABSCONT, ST_BAD_TOKEN, ST_NONFINITE, ST_BAD_PAGE = 1, 2, 4, 8, 16
-ST_EXCHANGE, ST_BAD_INDEX = 32, 64
+ST_EXCHANGE, ST_BAD_INDEX, ST_OUT_OF_PAGES = 32, 64, 128
 _RC = {0: "ok", 1: "invalid argument", 2: "CUDA launch or runtime error", 3: "not implemented"}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -51,6 +52,12 @@ class _KvTensor(ctypes.Structure):
                 ("outer_stride", ctypes.c_int64), ("prompt_stride", ctypes.c_int64),
                 ("particle_stride", ctypes.c_int64), ("seg_count", ctypes.c_int64),
                 ("seg_bytes", ctypes.c_int64), ("seg_stride", ctypes.c_int64)]
+
+
+class _KvPool(ctypes.Structure):
+    """include/smcsd.h smcsd_kv_pool (byte geometry of one paged KV pool)."""
+    _fields_ = [("base", ctypes.c_void_p), ("n_planes", ctypes.c_int64), ("plane_stride", ctypes.c_int64),
+                ("page_stride", ctypes.c_int64), ("token_bytes", ctypes.c_int64)]
 
 
 def _load():
@@ -94,7 +101,11 @@ def _load():
                                 i64, i64, f32, f32, f32, f32, i32, u64, u64, i64, vp,
                                 i32, i32, i32, u32, vp, vp,
                                 vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
-    for name in ("smcsd_workspace_init", "smcsd_weights", "smcsd_resample", "smcsd_step",
+    L.smcsd_kv_append_workspace_bytes.argtypes = [i32, i32, i32, i32]
+    L.smcsd_kv_append_workspace_bytes.restype = sz
+    L.smcsd_kv_append_paged.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp,
+                                        vp, vp, vp, ctypes.POINTER(_KvPool), i32, vp, sz, vp]
+    for name in ("smcsd_kv_append_paged", "smcsd_workspace_init", "smcsd_weights", "smcsd_resample", "smcsd_step",
                  "smcsd_weights_partial", "smcsd_weights_combine", "smcsd_kv_reindex",
                  "smcsd_kv_reindex_multi", "smcsd_partials_rescale", "smcsd_select", "smcsd_kv_reindex_paged", "smcsd_powersmc_weights",
                  "smcsd_tp_exchange_init", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close",
@@ -642,3 +653,96 @@ def smcsd_kv_reindex(dst, src, src_index, *, n_outer, outer_stride, prompt_strid
                                P, N, _p(status), _stream(stream))
     _check("smcsd_kv_reindex", rc)
     return status
+
+
+# ------------------------------------------------------------------------------------------
+# Paged append with copy-on-write (NEXT #1; include/smcsd.h)
+# ------------------------------------------------------------------------------------------
+def kv_pool(pool: torch.Tensor, *, n_planes, plane_stride, page_stride, token_bytes):
+    """One KV pool descriptor: (device tensor, byte geometry) -- see paged_pool_geometry."""
+    return (pool, dict(n_planes=n_planes, plane_stride=plane_stride, page_stride=page_stride,
+                       token_bytes=token_bytes))
+
+
+def paged_pool_geometry(pool: torch.Tensor) -> dict:
+    """Byte geometry of a contiguous paged KV pool laid out [planes][num_pages][page_size][H][d]
+    (planes = L x {K, V}; the per-layer [2][num_blocks][block][H][d] tensors of a serving
+    engine are one pool each with 2 planes)."""
+    if pool.dim() != 5 or not pool.is_contiguous():
+        raise ValueError("pool must be a contiguous [planes][num_pages][page_size][H][d] tensor")
+    Lp, G, S, H, d = pool.shape
+    e = pool.element_size()
+    return dict(n_planes=Lp, plane_stride=G * S * H * d * e, page_stride=S * H * d * e,
+                token_bytes=H * d * e)
+
+
+@dataclass
+class AppendOutputs:
+    slot_mapping: torch.Tensor = None
+    cow_src: torch.Tensor = None
+    cow_dst: torch.Tensor = None
+    cow_tokens: torch.Tensor = None
+    status: torch.Tensor = None
+    result: torch.Tensor = None
+
+
+_append_ws = {}
+
+
+def smcsd_kv_append_workspace_bytes(P: int, N: int, num_pages: int, max_pages: int) -> int:
+    return int(_lib.smcsd_kv_append_workspace_bytes(P, N, num_pages, max_pages))
+
+
+def _append_workspace(dev, stream, P, N, num_pages, max_pages):
+    need = smcsd_kv_append_workspace_bytes(P, N, num_pages, max_pages)
+    key = (dev.type, dev.index, _stream(stream))
+    ent = _append_ws.get(key)
+    shape = (P, N, num_pages, max_pages)
+    if ent is None or ent[0].numel() < need or ent[1] != shape:
+        buf = ent[0] if ent is not None and ent[0].numel() >= need else \
+            torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        smcsd_workspace_init(buf, stream)           # zero once per layout; the call keeps it zero
+        ent = (buf, shape)
+        _append_ws[key] = ent
+    return ent[0]
+
+
+def smcsd_kv_append_paged(table, n_pages, seq_len, refcount, n_new, *, page_size, max_new=None,
+                          pools=(), out: AppendOutputs | None = None, stream=None) -> AppendOutputs:
+    """Append n_new[p][n] tokens to every particle's page list, copying a shared partial tail
+    page first (copy-on-write).  table / n_pages / seq_len / refcount are updated in place;
+    pools: kv_pool(...) entries whose copy-on-write content the call copies.  out.result[0] = 1
+    means the call changed nothing (see out.status)."""
+    if table.dim() != 3:
+        raise ValueError("table must be [P][N][max_pages]")
+    P, N, MP = table.shape
+    dev = table.device
+    _chk(table, "table", _I32, (P, N, MP), dev, optional=False)
+    for name, t in (("n_pages", n_pages), ("seq_len", seq_len), ("n_new", n_new)):
+        _chk(t, name, _I32, (P, N), dev, optional=False)
+    if refcount.dim() != 1:
+        raise ValueError("refcount must be [num_pages]")
+    _chk(refcount, "refcount", _I32, (refcount.numel(),), dev, optional=False)
+    if max_new is None:
+        max_new = max(1, int(n_new.max().item()))
+    out = out or AppendOutputs()
+    shapes = dict(slot_mapping=(P, N, max_new), cow_src=(P, N), cow_dst=(P, N), cow_tokens=(P, N),
+                  status=(P,), result=(1,))
+    for f, shp in shapes.items():
+        if getattr(out, f) is None:
+            setattr(out, f, torch.empty(shp, dtype=torch.int32, device=dev))
+        else:
+            _chk(getattr(out, f), f"out.{f}", _I32, shp, dev)
+    arr = (_KvPool * max(1, len(pools)))()
+    for k, (t, g) in enumerate(pools):
+        if t.device != dev:
+            raise ValueError("pools must be on the tables' device")
+        arr[k] = _KvPool(_p(t), g["n_planes"], g["plane_stride"], g["page_stride"], g["token_bytes"])
+    ws = _append_workspace(dev, stream, P, N, refcount.numel(), MP)
+    rc = _lib.smcsd_kv_append_paged(_p(table), _p(n_pages), _p(seq_len), _p(refcount), _p(n_new),
+                                    P, N, MP, refcount.numel(), page_size, max_new,
+                                    _p(out.slot_mapping), _p(out.cow_src), _p(out.cow_dst),
+                                    _p(out.cow_tokens), _p(out.status), _p(out.result), arr,
+                                    len(pools), _p(ws), ws.numel(), _stream(stream))
+    _check("smcsd_kv_append_paged", rc)
+    return out

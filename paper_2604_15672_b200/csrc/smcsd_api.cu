@@ -10,6 +10,7 @@
 
 #include "smcsd.h"
 #include "smcsd_kernels.cuh"
+#include "smcsd_paged.cuh"
 
 using namespace smcsd;
 
@@ -509,6 +510,72 @@ smcsd_rc smcsd_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages
     smcsd_rc rc = launch_pdl(k_paged_gather, (unsigned)P, 0, st, q);
     if (rc != SMCSD_OK || !freed) return rc;
     return launch_pdl(k_paged_freed, (unsigned)P, 0, st, q);
+}
+
+size_t smcsd_kv_append_workspace_bytes(int P, int N, int num_pages, int max_pages) {
+    if (P < 1 || N < 1 || num_pages < 1 || max_pages < 1) return 0;
+    const size_t chunks = (size_t)cdiv(num_pages, kFreeChunk);
+    return align256(2 * (size_t)num_pages * 4) + align256(chunks * 4) + align256((size_t)P * N * 4) +
+           align256((size_t)P * N * (size_t)(max_pages + 1) * 4);
+}
+
+smcsd_rc smcsd_kv_append_paged(int32_t *table, int32_t *n_pages, int32_t *seq_len, int32_t *refcount,
+                               const int32_t *n_new, int P, int N, int max_pages, int num_pages,
+                               int page_size, int max_new, int32_t *slot_mapping, int32_t *cow_src,
+                               int32_t *cow_dst, int32_t *cow_tokens, uint32_t *status,
+                               int32_t *result, const smcsd_kv_pool *pools, int n_pools,
+                               void *workspace, size_t workspace_bytes, void *stream) {
+    if (!table || !n_pages || !seq_len || !refcount || !n_new || !slot_mapping || !cow_src ||
+        !cow_dst || !cow_tokens || !status || !result || !workspace)
+        return SMCSD_EINVAL;
+    if (P < 1 || N < 1 || max_pages < 1 || num_pages < 1 || page_size < 1 || max_new < 1)
+        return SMCSD_EINVAL;
+    if ((int64_t)num_pages * page_size >= (1ll << 31) || (int64_t)P * N >= (1 << 24)) return SMCSD_EINVAL;
+    if (n_pools < 0 || n_pools > kMaxPools || (n_pools > 0 && !pools)) return SMCSD_EINVAL;
+    if (workspace_bytes < smcsd_kv_append_workspace_bytes(P, N, num_pages, max_pages) || !aligned16(workspace))
+        return SMCSD_EINVAL;
+    AppendParams q;
+    std::memset(&q, 0, sizeof q);
+    q.table = table; q.n_pages = n_pages; q.seq_len = seq_len; q.refcount = refcount; q.n_new = n_new;
+    q.P = P; q.N = N; q.max_pages = max_pages; q.num_pages = num_pages; q.page_size = page_size;
+    q.max_new = max_new; q.slot_mapping = slot_mapping; q.cow_src = cow_src; q.cow_dst = cow_dst;
+    q.cow_tokens = cow_tokens; q.status = status; q.result = result;
+    q.nchunks = (int)cdiv(num_pages, kFreeChunk);
+    char *b = static_cast<char *>(workspace);
+    q.cnt = reinterpret_cast<int32_t *>(b);
+    q.last = q.cnt + num_pages;
+    b += align256(2 * (size_t)num_pages * 4);
+    q.chunk_free = reinterpret_cast<int32_t *>(b);  b += align256((size_t)q.nchunks * 4);
+    q.need = reinterpret_cast<int32_t *>(b);        b += align256((size_t)P * N * 4);
+    q.alloc = reinterpret_cast<int32_t *>(b);
+    q.max_alloc = (int64_t)P * N * (max_pages + 1);
+    q.n_pools = n_pools;
+    int64_t planes = 0;
+    for (int k = 0; k < n_pools; ++k) {
+        const smcsd_kv_pool &a = pools[k];
+        if (!a.base || !aligned16(a.base) || a.n_planes < 1 || a.token_bytes < 16) return SMCSD_EINVAL;
+        if ((a.plane_stride | a.page_stride | a.token_bytes) & 15) return SMCSD_EINVAL;
+        if (a.plane_stride < 0 || a.page_stride < (int64_t)page_size * a.token_bytes) return SMCSD_EINVAL;
+        planes += a.n_planes;
+        q.pool[k] = KvPool{static_cast<char *>(a.base), a.plane_stride, a.page_stride, a.token_bytes, planes};
+    }
+    q.total_planes = planes;
+    cudaStream_t st = as_stream(stream);
+    smcsd_rc rc = launch_pdl(k_append_count, (unsigned)q.nchunks, 0, st, q);
+    if (rc != SMCSD_OK) return rc;
+    rc = launch_pdl(k_append_plan, 1u, 0, st, q);
+    if (rc != SMCSD_OK || planes == 0) return rc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(P * N), (unsigned)cdiv(planes, kCowPlanesPerCta));
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cdiv(planes, kCowPlanesPerCta) > 65535) return SMCSD_EINVAL;
+    return cudaLaunchKernelEx(&cfg, k_append_cow, q) == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
 }
 
 smcsd_rc smcsd_powersmc_weights(const void *logits, int64_t ld, int rows_per_particle, int dtype,

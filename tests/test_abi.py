@@ -33,7 +33,7 @@ def lib():
 
 def test_every_declared_symbol_is_exported(lib):
     names = _declared()
-    assert len(names) == 22, names
+    assert len(names) == 24, names
     for n in names:
         assert hasattr(lib, n), n
 
@@ -135,3 +135,39 @@ def test_kv_reindex_multi_rejects_bad_arguments(lib):
     arr[1] = T(0x10000, 0x20000, 4, 4096, 2048, 512, 2, 100, 256)            # seg_bytes % 16
     assert lib.smcsd_kv_reindex_multi(arr, 2, 0x30000, 1, 4, None, None) == 1
 
+
+
+def test_kv_append_paged_rejects_bad_arguments(lib):
+    """smcsd_kv_append_paged validates synchronously (EINVAL, nothing enqueued)."""
+    import ctypes as c
+
+    class Pool(c.Structure):
+        _fields_ = [("base", c.c_void_p)] + [(n, c.c_int64) for n in
+                                              ("n_planes", "plane_stride", "page_stride", "token_bytes")]
+    vp, i32, sz = c.c_void_p, c.c_int, c.c_size_t
+    lib.smcsd_kv_append_workspace_bytes.argtypes = [i32, i32, i32, i32]
+    lib.smcsd_kv_append_workspace_bytes.restype = sz
+    wsb = lib.smcsd_kv_append_workspace_bytes(2, 4, 100, 8)
+    assert wsb > 0 and lib.smcsd_kv_append_workspace_bytes(0, 4, 100, 8) == 0
+    lib.smcsd_kv_append_paged.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp,
+                                          vp, vp, vp, c.POINTER(Pool), i32, vp, sz, vp]
+    lib.smcsd_kv_append_paged.restype = i32
+    good = Pool(0x100000, 2, 1 << 20, 16 * 256, 256)
+    arr = (Pool * 1)(good)
+    A = [0x1000, 0x2000, 0x3000, 0x4000, 0x5000]
+    O = [0x6000, 0x7000, 0x8000, 0x9000, 0xa000, 0xb000]
+
+    def call(P=2, N=4, MP=8, NP=100, page=16, mx=9, pools=arr, npool=1, ws=0x200000, wb=wsb):
+        return lib.smcsd_kv_append_paged(*A, P, N, MP, NP, page, mx, *O, pools, npool, ws, wb, None)
+    assert call(page=0) == 1
+    assert call(NP=1 << 28, page=16) == 1                   # num_pages * page_size >= 2^31
+    assert call(wb=wsb - 1) == 1                            # short workspace
+    assert call(npool=65) == 1
+    arr[0] = Pool(0x100008, 2, 1 << 20, 16 * 256, 256)      # misaligned pool
+    assert call() == 1
+    arr[0] = Pool(0x100000, 2, 1 << 20, 16 * 256, 100)      # token bytes not a multiple of 16
+    assert call() == 1
+    arr[0] = Pool(0x100000, 2, 1 << 20, 256, 256)           # page stride < page_size x token
+    assert call() == 1
+    assert lib.smcsd_kv_append_paged(None, *A[1:], 2, 4, 8, 100, 16, 9, *O, arr, 0, 0x200000, wsb,
+                                     None) == 1
