@@ -759,9 +759,80 @@ def measure_cfg3(dev, hbm_peak, steps=5, warmup=2):
                     "table_bytes": int(2 * N * PG * 4 + num_pages * 5),
                     "vs_dense_in_place": round(res["in_place"]["ms_per_step"] / msp, 1),
                     "note": "resample + block-table/refcount reindex (K5); pages of 16 tokens"}
+    res["paged_round"] = measure_paged_round(dev, hbm_peak)
     res["workload"] = ("cfg3: 70B KV, N=32, pinned pattern (16 sources x 2 offspring, 16 dead slots); "
                        "step = smcsd_resample + smcsd_kv_reindex (dense) or smcsd_kv_reindex_paged")
     return res
+
+
+def measure_paged_round(dev, hbm_peak, rounds=12, warmup=3):
+    """One engine round on the paper's pointer mechanism at the 70B KV shape:
+    resample (N=32, pinned pattern: 16 sources x 2) -> paged reindex (block tables + refcounts)
+    -> paged append of K+1 = 9 tokens per particle with copy-on-write of the shared partial tail
+    pages (smcsd_kv_append_paged).  The pool holds every page of the 80 layers x {K, V} (8 KV
+    heads x d 128 bf16, 16-token pages): the copy-on-write moves only the filled tokens of the
+    copied tails.  Each round starts from the same state (tables restored by a device copy)."""
+    import torch
+    import paper_2604_15672_b200 as smc
+    N, page, K1 = 32, 16, 9
+    L, H, S, d = KV70B["L"], KV70B["H"], KV70B["S"], KV70B["d"]
+    seq0 = S - K1 - 3                                 # 2036 tokens: a 4-token partial tail page
+    PG = (S + page - 1) // page + 1
+    own = (seq0 + page - 1) // page
+    num_pages = N * own + N * 2 + 64
+    pool = torch.empty((L * 2, num_pages, page, H, d), dtype=torch.bfloat16, device=dev)
+    pool.view(torch.int16).random_(-32768, 32767)
+    geom = smc.paged_pool_geometry(pool)
+    tab0 = torch.full((1, N, PG), -1, dtype=torch.int32, device=dev)
+    tab0[0, :, :own] = torch.arange(N * own, dtype=torch.int32, device=dev).view(N, own)
+    npg0 = torch.full((1, N), own, dtype=torch.int32, device=dev)
+    sl0 = torch.full((1, N), seq0, dtype=torch.int32, device=dev)
+    rc0 = torch.zeros(num_pages, dtype=torch.int32, device=dev)
+    rc0[:N * own] = 1
+    lw = torch.zeros((1, N), device=dev)
+    lw[0, 1::2] = -float("inf")
+    tab, npg, sl, rc = tab0.clone(), npg0.clone(), sl0.clone(), rc0.clone()
+    tab2, npg2 = torch.empty_like(tab), torch.empty_like(npg)
+    nn = torch.full((1, N), K1, dtype=torch.int32, device=dev)
+    o = smc.Outputs()
+    ao = smc.AppendOutputs()
+    pools = (smc.kv_pool(pool, **geom),)
+
+    def reset():
+        tab.copy_(tab0); npg.copy_(npg0); sl.copy_(sl0); rc.copy_(rc0)
+
+    def round_(i):
+        r = smc.smcsd_resample(lw, eta=math.inf, step=i, out=o)
+        smc.smcsd_kv_reindex_paged(tab, npg, rc, r.ancestors, table_dst=tab2, n_pages_dst=npg2)
+        sl.copy_(torch.gather(sl, 1, r.ancestors.long()))
+        smc.smcsd_kv_append_paged(tab2, npg2, sl, rc, nn, page_size=page, max_new=K1, pools=pools, out=ao)
+
+    for i in range(warmup):
+        reset(); round_(i)
+    torch.cuda.synchronize()
+    copies = int((ao.cow_dst >= 0).sum().item())
+    tokens = int(ao.cow_tokens.sum().item())
+    ok = int(ao.result.item()) == 0
+    ts = []
+    for i in range(rounds):
+        reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        round_(warmup + i)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = statistics.median(ts)
+    cow_bytes = tokens * H * d * 2 * L * 2
+    del pool
+    torch.cuda.empty_cache()
+    return {"us_per_round": round(ms * 1e3, 2), "ok": ok, "cow_pages": copies,
+            "cow_content_bytes": int(cow_bytes), "resample_content_bytes": 0,
+            "dense_equivalent_bytes_in_place": int(2 * 16 * L * 2 * H * S * d * 2),
+            "note": "resample + smcsd_kv_reindex_paged + smcsd_kv_append_paged (K+1 = 9 tokens, "
+                    "copy-on-write of shared 4-token tails) over a 70B-shaped paged pool; "
+                    "median of rounds from the same start state (the state reset is outside the "
+                    "timed region)"}
 
 
 def run_e2e(wl, args, dev, world):
