@@ -669,14 +669,19 @@ def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
             raise RuntimeError(f"fused exchange check failed on some rank (this rank: {bad})")
         msf = _time_steps(fnf, steps, warmup, world, dev)
         torch.cuda.synchronize()
+        # the shard's K1 (+ row merge) alone, timed the same way (no host sync between steps)
+        fnp_ = lambda i: smc.smcsd_weights_partial(sp, sq, tok, v_begin=b, v_len=w, partials=part,
+                                                   workspace=ws_p)
+        ms_k1 = _time_steps(fnp_, steps, warmup, world, dev)
         res["fused_exchange"] = {"ms_per_step": round(msf, 4), "steps_per_s": round(1e3 / msf, 1),
                                  "status_ok": bool((of.status == 0).all().item()),
                                  # the two launches of one call cannot be split by events: the
                                  # shard's K1 (+ merge) timed alone as smcsd_weights_partial, the
                                  # rest is the push / flag exchange + S2-S7 tail
-                                 "breakdown": {"k1_shard_ms": round(part_ms, 4),
-                                               "exchange_plus_tail_ms": round(msf - part_ms, 4),
-                                               "note": "k1_shard_ms from the all-gather phase timing"},
+                                 "breakdown": {"k1_shard_ms": round(ms_k1, 4),
+                                               "exchange_plus_tail_ms": round(msf - ms_k1, 4),
+                                               "note": "k1_shard_ms: smcsd_weights_partial on the "
+                                                       "same shard timed alone (K1 + row merge)"},
                                  "path": "smcsd_tp_step: K1 pushes partials to peers (P2P "
                                          "stores + release flags), tail waits (acquire) + S2-S7"}
         # the product path is the line's cfg5 figure

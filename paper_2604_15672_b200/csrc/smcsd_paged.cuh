@@ -90,15 +90,26 @@ __global__ void __launch_bounds__(kThreads) k_append_plan(const __grid_constant_
     if (tid == 0) { s_bad = 0; s_free = 0; }
     for (int p = tid; p < q.P; p += kThreads) q.status[p] = 0u;
     __syncthreads();
-    // ---- 1. validation; appenders of a partial tail count themselves on the tail page
+    // ---- 1. validation; appenders of a partial tail count themselves on the tail page.  The
+    // page ids of every list are checked over (particle, slot) pairs, so the loads of a long
+    // list are independent (not one dependent chain per particle).
+    for (int64_t e = tid; e < (int64_t)PN * MP; e += kThreads) {
+        const int pn = (int)(e / MP), i = (int)(e - (int64_t)pn * MP);
+        const int np = q.n_pages[pn];
+        if (i < np && np <= MP) {
+            const int pg = q.table[e];
+            if (pg < 0 || pg >= q.num_pages || __ldcg(&q.refcount[pg]) < 1) {
+                atomicOr(&q.status[pn / q.N], ST_BAD_PAGE);
+                s_bad = 1;
+            }
+        }
+    }
+    __syncthreads();
     for (int pn = tid; pn < PN; pn += kThreads) {
         const int len = q.seq_len[pn], np = q.n_pages[pn], add = q.n_new[pn];
         bool bad = len < 0 || np < 0 || np > MP || add < 0 || add > q.max_new ||
-                   np != (int)(((long long)len + page - 1) / page);
-        for (int i = 0; !bad && i < np; ++i) {
-            const int pg = q.table[(int64_t)pn * MP + i];
-            bad = pg < 0 || pg >= q.num_pages || __ldcg(&q.refcount[pg]) < 1;
-        }
+                   np != (int)(((long long)len + page - 1) / page) ||
+                   (__ldcg(&q.status[pn / q.N]) & ST_BAD_PAGE) != 0;
         if (!bad && np + append_fresh(len, add, page) > MP) bad = true;
         if (bad) {
             atomicOr(&q.status[pn / q.N], ST_BAD_PAGE);
@@ -228,16 +239,45 @@ __global__ void __launch_bounds__(kThreads) k_append_cow(const __grid_constant__
     if (cd < 0) return;
     const int cs = q.cow_src[pn], ct = q.cow_tokens[pn];
     const int64_t pl0 = (int64_t)blockIdx.y * kCowPlanesPerCta;
-    for (int64_t pl = pl0; pl < pl0 + kCowPlanesPerCta && pl < q.total_planes; ++pl) {
-        int k = 0;
-        while (q.pool[k].plane_end <= pl) ++k;
-        const KvPool &P_ = q.pool[k];
-        const int64_t o = pl - (k ? q.pool[k - 1].plane_end : 0);
-        const int64_t nvec = (int64_t)ct * P_.token_bytes / 16;
-        const char *src = P_.base + o * P_.plane_stride + (int64_t)cs * P_.page_stride;
-        char *dst = P_.base + o * P_.plane_stride + (int64_t)cd * P_.page_stride;
-        for (int64_t v = threadIdx.x; v < nvec; v += kThreads)
-            st_stream(dst + v * 16, ld_stream(src + v * 16));
+    const int npl = (int)min((int64_t)kCowPlanesPerCta, q.total_planes - pl0);
+    // every plane of this CTA copies the same token range: (plane, vector) pairs flattened so a
+    // thread keeps 4 independent 16-byte loads in flight
+    const char *srcp[kCowPlanesPerCta];
+    char *dstp[kCowPlanesPerCta];
+    int64_t nv[kCowPlanesPerCta];
+    int64_t tot = 0;
+#pragma unroll
+    for (int u = 0; u < kCowPlanesPerCta; ++u) {
+        nv[u] = 0; srcp[u] = nullptr; dstp[u] = nullptr;
+        if (u < npl) {
+            const int64_t pl = pl0 + u;
+            int k = 0;
+            while (q.pool[k].plane_end <= pl) ++k;
+            const KvPool &P_ = q.pool[k];
+            const int64_t o = pl - (k ? q.pool[k - 1].plane_end : 0);
+            nv[u] = (int64_t)ct * P_.token_bytes / 16;
+            srcp[u] = P_.base + o * P_.plane_stride + (int64_t)cs * P_.page_stride;
+            dstp[u] = P_.base + o * P_.plane_stride + (int64_t)cd * P_.page_stride;
+            tot += nv[u];
+        }
+    }
+    for (int64_t b = threadIdx.x; b < tot; b += 4 * kThreads) {
+        uint4 r[4];
+        char *dp[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            int64_t v = b + (int64_t)w * kThreads;
+            dp[w] = nullptr;
+            if (v < tot) {
+                int u = 0;
+                while (v >= nv[u]) { v -= nv[u]; ++u; }
+                r[w] = ld_stream(srcp[u] + v * 16);
+                dp[w] = dstp[u] + v * 16;
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+            if (dp[w]) st_stream(dp[w], r[w]);
     }
 }
 
