@@ -130,6 +130,17 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Store into cluster rank `rank`'s copy of a shared-memory object (distributed shared memory).
+__device__ __forceinline__ void st_cluster_f32(float *local, unsigned rank, float v) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(local), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(r), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t *local, unsigned rank, uint32_t v) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(local), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1161,6 +1172,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     double *ell_s = cs.ell_s;
     __shared__ int s_last;
     __shared__ uint32_t s_xe;                                   // S10: this launch's epoch
+    // cluster tail with whole particles per chunk (K divides 32): S3 runs in the chunk CTAs and
+    // each pushes its particles' lam' and its status bits into cluster rank 0's shared memory
+    // (DSMEM stores, ordered by the cluster barrier), so rank 0 goes straight to S4-S7
+    __shared__ double term_s[kPairsPerCta];
+    __shared__ uint32_t s_cst;                                  // this chunk's status bits
+    __shared__ uint32_t s_flags[16];                            // rank 0: every chunk's bits
     const int tid = threadIdx.x;
     const int N = prm.N, K = prm.K, NK = N * K, rows = 2 * NK;
     const int chunk_ctas = prm.P * chunks_per_prompt;
@@ -1180,6 +1197,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     const int p = blockIdx.x / per_prompt, c = blockIdx.x - p * per_prompt;
     const int q0 = c * kPairsPerCta, nq = min(kPairsPerCta, NK - q0);
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+    const bool s3_local = cluster && (kPairsPerCta % K) == 0;   // uniform
     {
 
     // ---- inputs (not produced by the predecessor): before the wait
@@ -1199,6 +1217,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     }
     if (tid == 0) {
         sh.st = 0;
+        s_cst = 0;
         if (resample_mode) tail_prologue(prm, p, sh);
     }
     if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2048);      // tail CTA resident
@@ -1346,9 +1365,46 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
                 term = __dsub_rn(__dmul_rn(prm.alpha, lp), lq);
             }
         }
-        __stcg(&prm.ell_ws[(int64_t)p * NK + qq], term);
+        if (s3_local) term_s[tid] = term;
+        else __stcg(&prm.ell_ws[(int64_t)p * NK + qq], term);
     }
-    if (st) atomicOr(&prm.st_ws[p], st);
+    if (s3_local) {
+        if (st) atomicOr(&s_cst, st);
+        __syncthreads();
+        // S3 for this chunk's whole particles, exactly as the rank-0 loop below does it
+        const int np_chunk = nq / K;
+        unsigned crank;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+        if (tid < np_chunk) {
+            const int n = q0 / K + tid;
+            const int64_t pn = (int64_t)p * N + n;
+            int kn = drafted_len(prm, pn);
+            uint32_t st3 = 0;
+            bool bad = false;
+            if (kn < 0 || kn > K) {
+                st3 |= ST_BAD_TOKEN;
+                bad = true;
+                kn = 0;
+            }
+            double delta = 0.0;
+            for (int j = 0; j < kn; ++j) delta = __dadd_rn(delta, term_s[tid * K + j]);
+            if (isnan(delta)) bad = true;
+            const float prev = prm.logw_prev ? prm.logw_prev[pn] : (float)(-log((double)N));
+            if (isnan(prev) || prev == INFINITY) {
+                st3 |= ST_NONFINITE;
+                bad = true;
+            }
+            const float lam = bad ? -INFINITY : (float)__dadd_rn((double)prev, delta);
+            st_cluster_f32(&sh.lam[n], 0u, lam);
+            if (prm.logw_pre) prm.logw_pre[pn] = lam;
+            if (!resample_mode) prm.logw_out[pn] = lam;
+            if (st3) atomicOr(&s_cst, st3);
+        }
+        __syncthreads();
+        if (tid == 0) st_cluster_u32(&s_flags[crank], 0u, s_cst);
+    } else if (st) {
+        atomicOr(&prm.st_ws[p], st);
+    }
     if (tid == 0 && blockIdx.x == 0) { SMCSD_TRACE_AT(2053); SMCSD_CLK_AT(2204); }      // chunk 0 S2 done
     }
     // ---- completion: the last CTA of the prompt finishes it.  Release chain: the barrier
@@ -1383,6 +1439,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         return;
     }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);
+    if (s3_local) {
+        // S3 ran in the chunk CTAs: lam' is in sh.lam, the chunks' status bits in s_flags
+        if (tid == 0) {
+            uint32_t f = 0;
+            for (int r = 0; r < per_prompt; ++r) f |= s_flags[r];
+            sh.st |= f;
+            prm.prompt_ctr[p] = 0u;
+        }
+        __syncthreads();
+    } else {
     // ---- S3: lam' = fl32(prev + sum_{j<k_n} term_j) in j order
     const double *terms = prm.ell_ws + (int64_t)p * NK;
     uint32_t st3 = 0;
@@ -1423,8 +1489,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         prm.st_ws[p] = 0u;
         prm.prompt_ctr[p] = 0u;                                  // graph-replay safe
     }
-    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2051);
     __syncthreads();
+    }
+    if (tid == 0 && p == 0) SMCSD_TRACE_AT(2051);
     normalise_resample(prm, p, resample_mode != 0, sh);
     __syncthreads();
     if (tid == 0) {
