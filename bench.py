@@ -324,6 +324,7 @@ def run_ours(args, rank, world, local):
             secondary["cfg3"] = settled(measure_cfg3, dev, hbm_peak)
             secondary["cfg2_verify"] = settled(measure_cfg2_verify, dev, hbm_peak)
             secondary["powersmc"] = settled(measure_power, dev, hbm_peak)
+            secondary["paper_sweep"] = settled(measure_paper_sweep, dev, hbm_peak)
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "steps/s", "n_gpus": world,
@@ -530,6 +531,56 @@ def measure_cfg2_verify(dev, hbm_peak, steps=120, warmup=6):
     del ring
     torch.cuda.empty_cache()
     return res
+
+
+PAPER_NK = [(12, 8), (8, 16), (6, 12), (12, 16), (4, 32), (8, 32), (4, 64), (16, 12), (8, 48), (8, 8),
+            (4, 16), (8, 26)]
+
+
+def measure_paper_sweep(dev, hbm_peak, replays=8):
+    """The paper's batch-1..16 operating points: (N, K) from PAPER.md:537-674, P from
+    PAPER.md:729, V = 128256 bf16, smcsd_step S1-S7 (eta = inf).  Each point: a 2-set ring of
+    steps captured in one CUDA graph, median of `replays` replays (no host in the loop); the
+    fraction is of the measured copy peak for the algorithmic logit bytes 2 N K V 2 P."""
+    import torch
+    import paper_2604_15672_b200 as smc
+    import synth
+    V = 128256
+    rows = []
+    for P in (1, 4, 8, 16):
+        for N, K in PAPER_NK:
+            ring = [synth.lm_logits(P, N, K, V, device=dev, seed=31 + r) for r in range(2)]
+            ws, out = smc.Workspace(dev), smc.Outputs()
+            gs = torch.cuda.Stream(dev)
+            gs.wait_stream(torch.cuda.current_stream(dev))
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(gs):
+                for i in range(2):
+                    smc.smcsd_step(*ring[i], V=V, eta=math.inf, step=i, out=out, fields=(),
+                                   workspace=ws, stream=gs)
+                torch.cuda.synchronize(dev)
+                with torch.cuda.graph(graph, stream=gs):
+                    for i in range(2):
+                        smc.smcsd_step(*ring[i], V=V, eta=math.inf, step=i, out=out, fields=(),
+                                       workspace=ws, stream=gs)
+            graph.replay()
+            torch.cuda.synchronize(dev)
+            reps = []
+            for _ in range(replays):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                graph.replay()
+                e1.record()
+                torch.cuda.synchronize(dev)
+                reps.append(e0.elapsed_time(e1) / 2)
+            ms = statistics.median(reps)
+            byts = 2 * N * K * V * 2 * P
+            rows.append([N, K, P, round(ms * 1e3, 2), round(byts / (ms / 1e3) / 1e9 / hbm_peak, 3)])
+            del graph, ring
+    torch.cuda.empty_cache()
+    return {"workload": "paper operating points (PAPER.md:537-674, 729): smcsd_step S1-S7, V=128256 bf16, "
+                        "CUDA-graph replay of a 2-set ring, median of 8",
+            "columns": ["N", "K", "P", "us_per_step", "frac_of_measured"], "rows": rows}
 
 
 def measure_power(dev, hbm_peak, steps=20, warmup=3):
