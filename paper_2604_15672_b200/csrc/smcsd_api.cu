@@ -120,6 +120,21 @@ smcsd_rc launch_pdl_cluster(void (*kernel)(KArgs...), unsigned grid, unsigned cl
 }
 
 template <typename... KArgs, typename... Args>
+smcsd_rc launch_pdl_2d(void (*kernel)(KArgs...), dim3 grid, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...) == cudaSuccess
+               ? SMCSD_OK : SMCSD_ECUDA;
+}
+
+template <typename... KArgs, typename... Args>
 smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaStream_t st,
                     Args &&...args) {
     return launch_pdl_b(kernel, grid, smem, st, (unsigned)kThreads, std::forward<Args>(args)...);
@@ -507,9 +522,12 @@ smcsd_rc smcsd_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages
     q.freed = freed; q.status = status;
     q.P = P; q.N = N; q.max_pages = max_pages; q.num_pages = num_pages;
     cudaStream_t st = as_stream(stream);
-    smcsd_rc rc = launch_pdl(k_paged_gather, (unsigned)P, 0, st, q);
+    if ((int64_t)N * max_pages >= (1ll << 31) || P > 65535) return SMCSD_EINVAL;
+    if (status && cudaMemsetAsync(status, 0, (size_t)P * sizeof(uint32_t), st) != cudaSuccess) return SMCSD_ECUDA;
+    const dim3 grid((unsigned)cdiv((int64_t)N * max_pages, kThreads), (unsigned)P);
+    smcsd_rc rc = launch_pdl_2d(k_paged_gather, grid, st, q);
     if (rc != SMCSD_OK || !freed) return rc;
-    return launch_pdl(k_paged_freed, (unsigned)P, 0, st, q);
+    return launch_pdl_2d(k_paged_freed, grid, st, q);
 }
 
 size_t smcsd_kv_append_workspace_bytes(int P, int N, int num_pages, int max_pages) {

@@ -1815,15 +1815,15 @@ struct PagedParams {
     int P, N, max_pages, num_pages;
 };
 
+// grid = (ceil(N * max_pages / kThreads), P): one (particle, slot) entry per thread, so a long
+// list's loads are independent.  status[p] was zeroed by the caller's stream (memset) before.
 __global__ void __launch_bounds__(kThreads) k_paged_gather(const __grid_constant__ PagedParams q) {
-    __shared__ uint32_t s_st;
-    const int p = blockIdx.x, tid = threadIdx.x, N = q.N, MP = q.max_pages;
-    if (tid == 0) s_st = 0;
+    const int p = blockIdx.y, N = q.N, MP = q.max_pages;
     pdl_wait();
-    __syncthreads();
     uint32_t st = 0;
     const int64_t base = (int64_t)p * N;
-    for (int64_t e = tid; e < (int64_t)N * MP; e += kThreads) {
+    const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (e < (int64_t)N * MP) {
         const int n = (int)(e / MP), i = (int)(e - (int64_t)n * MP);
         // new list of n = old list of its ancestor
         const int a = q.idx[base + n];
@@ -1852,23 +1852,23 @@ __global__ void __launch_bounds__(kThreads) k_paged_gather(const __grid_constant
             else atomicSub(&q.refcount[og], 1);
         }
     }
-    if (st) atomicOr(&s_st, st);
-    __syncthreads();
-    if (tid == 0 && q.status) q.status[p] = s_st;
+    st = __reduce_or_sync(0xffffffffu, st);
+    if (st && (threadIdx.x & 31) == 0 && q.status) atomicOr(&q.status[p], st);
     pdl_trigger();
 }
 
 __global__ void __launch_bounds__(kThreads) k_paged_freed(const __grid_constant__ PagedParams q) {
-    const int p = blockIdx.x, tid = threadIdx.x, N = q.N, MP = q.max_pages;
+    const int p = blockIdx.y, N = q.N, MP = q.max_pages;
     pdl_wait();
     const int64_t base = (int64_t)p * N;
-    for (int64_t e = tid; e < (int64_t)N * MP; e += kThreads) {
+    const int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (e < (int64_t)N * MP) {
         const int n = (int)(e / MP), i = (int)(e - (int64_t)n * MP);
         const int olen = q.n_src[base + n];
-        if (olen < 0 || olen > MP || i >= olen) continue;
-        const int32_t og = q.table_src[(base + n) * MP + i];
-        if (og < 0 || og >= q.num_pages) continue;
-        q.freed[og] = (uint8_t)(__ldcg(&q.refcount[og]) == 0);
+        if (olen >= 0 && olen <= MP && i < olen) {
+            const int32_t og = q.table_src[(base + n) * MP + i];
+            if (og >= 0 && og < q.num_pages) q.freed[og] = (uint8_t)(__ldcg(&q.refcount[og]) == 0);
+        }
     }
     pdl_trigger();
 }

@@ -93,16 +93,33 @@ __global__ void __launch_bounds__(kThreads) k_append_plan(const __grid_constant_
     // ---- 1. validation; appenders of a partial tail count themselves on the tail page.  The
     // page ids of every list are checked over (particle, slot) pairs, so the loads of a long
     // list are independent (not one dependent chain per particle).
-    for (int64_t e = tid; e < (int64_t)PN * MP; e += kThreads) {
-        const int pn = (int)(e / MP), i = (int)(e - (int64_t)pn * MP);
-        const int np = q.n_pages[pn];
-        if (i < np && np <= MP) {
-            const int pg = q.table[e];
-            if (pg < 0 || pg >= q.num_pages || __ldcg(&q.refcount[pg]) < 1) {
-                atomicOr(&q.status[pn / q.N], ST_BAD_PAGE);
-                s_bad = 1;
+    constexpr int kU = 8;                                      // entries in flight per thread
+    for (int64_t e0 = tid; e0 < (int64_t)PN * MP; e0 += (int64_t)kU * kThreads) {
+        int pg[kU], rc[kU], pnv[kU];
+        bool chk[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t e = e0 + (int64_t)u * kThreads;
+            chk[u] = false;
+            pnv[u] = 0;
+            pg[u] = -1;
+            if (e < (int64_t)PN * MP) {
+                const int pn = (int)(e / MP), i = (int)(e - (int64_t)pn * MP);
+                const int np = q.n_pages[pn];
+                pnv[u] = pn;
+                chk[u] = i < np && np <= MP;
+                pg[u] = chk[u] ? q.table[e] : -1;
             }
         }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            rc[u] = chk[u] && pg[u] >= 0 && pg[u] < q.num_pages ? __ldcg(&q.refcount[pg[u]]) : 1;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (chk[u] && (pg[u] < 0 || pg[u] >= q.num_pages || rc[u] < 1)) {
+                atomicOr(&q.status[pnv[u] / q.N], ST_BAD_PAGE);
+                s_bad = 1;
+            }
     }
     __syncthreads();
     for (int pn = tid; pn < PN; pn += kThreads) {
