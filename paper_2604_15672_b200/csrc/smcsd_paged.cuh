@@ -24,9 +24,9 @@
 namespace smcsd {
 
 constexpr uint32_t ST_OUT_OF_PAGES = 128u;
-constexpr int kFreeChunk = 4096;                // pages per free-count chunk
+constexpr int kFreeChunk = 1024;                // pages per free-count chunk (4 per thread)
 constexpr int kMaxPools = 64;                   // KV pool descriptors per call
-constexpr int kCowPlanesPerCta = 8;
+constexpr int kCowPlanesPerCta = 2;
 
 struct KvPool {
     char *base;
@@ -58,10 +58,14 @@ __global__ void __launch_bounds__(kThreads) k_append_count(const __grid_constant
     pdl_wait();                                 // refcounts may come from the reindex before
     const int base = blockIdx.x * kFreeChunk;
     int c = 0;
-    for (int i = threadIdx.x; i < kFreeChunk; i += kThreads) {
-        const int pg = base + i;
-        if (pg < q.num_pages) c += __ldcg(&q.refcount[pg]) == 0;
+    int v[kFreeChunk / kThreads];
+#pragma unroll
+    for (int u = 0; u < kFreeChunk / kThreads; ++u) {          // all loads first
+        const int pg = base + u * kThreads + threadIdx.x;
+        v[u] = pg < q.num_pages ? __ldcg(&q.refcount[pg]) : 1;
     }
+#pragma unroll
+    for (int u = 0; u < kFreeChunk / kThreads; ++u) c += v[u] == 0;
     c = __reduce_add_sync(0xffffffffu, c);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
     __syncthreads();
