@@ -319,25 +319,27 @@ SMCSD_API smcsd_rc smcsd_powersmc_weights(const void *logits, int64_t ld, int ro
 /* ---- S10 fused into K1: tensor-parallel step over peer memory (NVLink P2P) -------------------
  * The north star's vocab-sharded config: every rank holds columns [v_begin, v_begin + v_len)
  * of every logit row.  Instead of partial -> NCCL all_gather -> combine, K1 itself pushes each
- * (row, segment) partial {m, s, x_d} (16 B) straight into every rank's exchange buffer with
- * plain stores through peer mappings, then its last CTA publishes the epoch in every rank's
- * flag word (one fence.acq_rel.sys, then st.relaxed.sys).  The tail waits on its own flags --
- * they are its only dependency on K1 (ld.acquire.sys, bounded: 20 s -> SMCSD_ST_EXCHANGE) --
- * and merges the G * xnseg parts of each row in rank order -- the global
+ * (row, segment) partial straight into every rank's exchange buffer through peer mappings, as
+ * two 8-byte words {m, s} and {x_d, 1} (st.relaxed.sys: single-copy atomic, and both words are
+ * nonzero whenever written).  There is no fence, flag or collective: each rank's tail polls
+ * the words of its rows itself (ld.relaxed.sys; bounded: 20 s -> SMCSD_ST_EXCHANGE), zeroes
+ * them after reading, and merges the G * xnseg parts of each row in rank order -- the global
  * column order -- so every rank computes identical weights, ancestors and resets (same Philox
- * counters), with no collective call.  Two launches per step, like smcsd_step.
+ * counters).  Two launches per step, like smcsd_step.
  *
  * Exchange buffer (one per rank, caller-allocated, 16-byte aligned, smcsd_tp_exchange_bytes):
- * 256 B of flags then two parity halves (epoch & 1) of [2*P*N*K][G*xnseg] float4.  Initialise
- * once with smcsd_tp_exchange_init, share it with smcsd_ipc_export / smcsd_ipc_open (plumbing;
- * the handles travel over torch.distributed).  xnseg >= ceil(v_len / SMCSD_SEGMENT) on every
- * rank (the same value everywhere); slots a rank never writes stay neutral.
+ * 256 B of control words then two parity halves (epoch & 1) of [2*P*N*K][G*xnseg] 16-byte
+ * slots.  Initialise once with smcsd_tp_exchange_init (all zero = nothing written), share it
+ * with smcsd_ipc_export / smcsd_ipc_open (plumbing; the handles travel over torch.distributed).
+ * xnseg >= ceil(v_len / SMCSD_SEGMENT) on every rank (the same value everywhere); a rank with
+ * fewer segments fills its unused slots with neutral parts.
  * epoch: 0 = device-resident epoch (recommended): each rank's buffer holds the last epoch it
  *   completed, advanced by the tail's last CTA, so the call can be captured in a CUDA graph
  *   and replayed (every replay is the next epoch).  >= 1 = explicit host epoch, +1 per call,
  *   identical on every rank; then a captured graph would replay a stale epoch and must not be
  *   used.  Do not mix the two modes on one buffer.  A rank may run at most one step ahead of
- *   another (the parity halves make that safe). */
+ *   another: it writes the other parity half, which every reader has zeroed before (its K1 of
+ *   step e + 2 needs our pushes of step e + 1, made after our tail of step e finished). */
 SMCSD_API size_t smcsd_tp_exchange_bytes(int P, int N, int K, int G, int xnseg);
 SMCSD_API smcsd_rc smcsd_tp_exchange_init(void *xbuf, size_t xbuf_bytes, void *stream);
 /* CUDA IPC plumbing.  smcsd_ipc_export writes smcsd_ipc_handle_bytes() opaque host bytes naming

@@ -141,6 +141,14 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t *local, unsigned rank, u
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(r), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys_u64(void *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const void *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -581,7 +589,21 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                         out.z = z * m.c;
                     }
                     if (lane < prm.xG) {
-                        xdst[lane][(size_t)row * prm.xG * prm.xnseg + prm.xrank * prm.xnseg + sg] = out;
+                        // two single-copy-atomic 8-byte words, both nonzero whenever written
+                        // ({m, s}: m finite => s >= 1, an empty segment has m = -inf; {x, 1}),
+                        // so the tail polls the data itself -- no fence or flag per step
+                        float4 *slot = xdst[lane] + (size_t)row * prm.xG * prm.xnseg + prm.xrank * prm.xnseg + sg;
+                        st_relaxed_sys_u64(slot, (unsigned long long)__float_as_uint(out.x) |
+                                                 ((unsigned long long)__float_as_uint(out.y) << 32));
+                        st_relaxed_sys_u64(reinterpret_cast<unsigned long long *>(slot) + 1,
+                                           (unsigned long long)__float_as_uint(out.z) | (1ull << 32));
+                        // this rank's shard has fewer segments than the exchange's slots: the
+                        // row's last segment also fills the unused slots with neutral parts
+                        for (int u = sg + 1; sg == prm.nseg - 1 && u < prm.xnseg; ++u) {
+                            st_relaxed_sys_u64(slot + (u - sg), 0xFF800000ull);        // {-inf, 0}
+                            st_relaxed_sys_u64(reinterpret_cast<unsigned long long *>(slot + (u - sg)) + 1,
+                                               0xFF800000ull | (1ull << 32));          // {-inf, 1}
+                        }
                     }
                     if (lane == 0) done[s] = 0;
                 } else if (lane == 0) {
@@ -594,29 +616,7 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
         }
     }
     if (tid == 0) SMCSD_TRACE_AT(1024 + (blockIdx.x & 1023));    // K1 CTA done
-    if (XP) {
-        // the tail may be scheduled now: in this mode its only dependency on this grid is the
-        // epoch flags published below
-        pdl_trigger();
-        // Release chain (PTX memory model): the CTA barrier orders every thread's pushes before
-        // thread 0's gpu-scope release fence + count; the CTA that completes the count
-        // acquires it and its one system-scope fence is cumulative over all of them, so the
-        // relaxed system-scope flag stores after it publish every rank's pushes (the tail
-        // reads the flags with ld.acquire.sys).  One fence per CTA at gpu scope and one at
-        // system scope per launch: a system fence in every thread cost ~10 us (measured).
-        __syncthreads();
-        if (tid == 0) {
-            fence_acq_rel_gpu();
-            if (atomicAdd(prm.xctr, 1u) == gridDim.x - 1) {
-                SMCSD_TRACE_AT(2060);                       // last K1 CTA counted
-                fence_acq_rel_sys();
-                SMCSD_TRACE_AT(2061);                       // system fence done
-                for (int g = 0; g < prm.xG; ++g)
-                    st_relaxed_sys(reinterpret_cast<uint32_t *>(prm.xpeer[g]) + prm.xrank, *xep);
-                *prm.xctr = 0u;
-            }
-        }
-    }
+    if (XP) pdl_trigger();                 // the tail's only dependency is the pushed words
     if (!XP) pdl_trigger();
 }
 
@@ -948,6 +948,15 @@ constexpr int kPairsPerCta = 32;
 // S10, device epoch: every tail CTA counts itself once it no longer reads the exchange buffer;
 // the last one records the epoch as this rank's completed one (the next step's K1 reads it after
 // griddepcontrol.wait, i.e. after this whole grid) and re-arms the count.
+// S10: re-arm K1's work counter once this rank's K1 grid has completed (CTA 0, at its exit:
+// off the critical path; the next step's K1 reads the counter after its own griddepcontrol.wait)
+__device__ __forceinline__ void x_tail_rearm(const Params &prm) {
+    if (prm.xlocal && prm.work_ctr && blockIdx.x == 0 && threadIdx.x == 0) {
+        pdl_wait();
+        *prm.work_ctr = 0u;
+    }
+}
+
 __device__ __forceinline__ void x_tail_done(const Params &prm, uint32_t xe) {
     if (!prm.xlocal || prm.xepoch) return;
     __syncthreads();
@@ -958,6 +967,74 @@ __device__ __forceinline__ void x_tail_done(const Params &prm, uint32_t xe) {
             w[kXEpochWord] = xe;
         }
     }
+}
+
+// S10 exchange slots (smcsd_tp_step): a slot is two 8-byte words {m, s}, {x, 1}, both nonzero
+// once written by the owning rank's K1 (single-copy-atomic relaxed system-scope stores); the
+// tail polls them and zeroes them after reading (each slot has one reader per step), so the
+// parity half is zero again before any rank can write it next (two steps later).  Bounded: a
+// slot still empty after kXTimeoutNs returns a neutral part and `true` (-> SMCSD_ST_EXCHANGE).
+__device__ __forceinline__ float4 xp_decode(unsigned long long a, unsigned long long b) {
+    return make_float4(__uint_as_float((uint32_t)a), __uint_as_float((uint32_t)(a >> 32)),
+                       __uint_as_float((uint32_t)b), 0.0f);
+}
+__device__ __forceinline__ bool xp_take4(const float4 *pr, int64_t stride, int pi0, int nparts, float4 (&t)[4]) {
+    const unsigned long long *w[4];
+    unsigned long long a[4], b[4];
+    bool nd[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        nd[k] = pi0 + k < nparts;
+        w[k] = reinterpret_cast<const unsigned long long *>(pr + (nd[k] ? (int64_t)(pi0 + k) * stride : 0));
+        a[k] = nd[k] ? ld_relaxed_sys_u64(w[k]) : 1ull;
+        b[k] = nd[k] ? ld_relaxed_sys_u64(w[k] + 1) : 1ull;
+    }
+    bool late = false;
+    uint64_t t0 = 0;
+    for (;;) {
+        bool all = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) all &= a[k] != 0ull && b[k] != 0ull;
+        if (all) break;
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > kXTimeoutNs) { late = true; break; }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (a[k] == 0ull) a[k] = ld_relaxed_sys_u64(w[k]);
+            if (b[k] == 0ull) b[k] = ld_relaxed_sys_u64(w[k] + 1);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        t[k] = nd[k] && a[k] && b[k] ? xp_decode(a[k], b[k]) : make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
+        if (nd[k]) {
+            unsigned long long *ww = const_cast<unsigned long long *>(w[k]);
+            ww[0] = 0ull;
+            ww[1] = 0ull;
+        }
+    }
+    return late;
+}
+// one slot, polled (no zeroing): the first pass of a row with more than 16 parts
+__device__ __forceinline__ float4 xp_peek(const float4 *slot, bool &late) {
+    const unsigned long long *w = reinterpret_cast<const unsigned long long *>(slot);
+    unsigned long long a = ld_relaxed_sys_u64(w), b = ld_relaxed_sys_u64(w + 1);
+    const uint64_t t0 = globaltimer_ns();
+    while (a == 0ull || b == 0ull) {
+        if (globaltimer_ns() - t0 > kXTimeoutNs) { late = true; return make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f); }
+        if (a == 0ull) a = ld_relaxed_sys_u64(w);
+        if (b == 0ull) b = ld_relaxed_sys_u64(w + 1);
+    }
+    return xp_decode(a, b);
+}
+// the second pass: read (already seen nonzero) and zero
+__device__ __forceinline__ float4 xp_read_zero(const float4 *slot) {
+    unsigned long long *w = reinterpret_cast<unsigned long long *>(const_cast<float4 *>(slot));
+    const unsigned long long a = ld_relaxed_sys_u64(w), b = ld_relaxed_sys_u64(w + 1);
+    w[0] = 0ull;
+    w[1] = 0ull;
+    return a && b ? xp_decode(a, b) : make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
 }
 
 __device__ __forceinline__ float3 lane_premerge(const Params &prm, int64_t grow, int li) {
@@ -1221,9 +1298,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         if (resample_mode) tail_prologue(prm, p, sh);
     }
     if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2048);      // tail CTA resident
-    // S10 (xlocal): the epoch flags are the dependency -- every rank's flag, this rank's
-    // included, is released after all of that rank's K1 CTAs pushed their partials and left
-    // the work loop -- so the tail does not also wait for K1's grid to complete and flush.
+    // S10 (xlocal): the pushed words themselves are the dependency (the tail polls them), so
+    // the tail does not wait for K1's grid to complete and flush.
     if (!prm.xlocal) pdl_wait();
     if (tid == 0 && blockIdx.x == 0) {
         SMCSD_TRACE_AT(2049);                                   // predecessor complete
@@ -1231,32 +1307,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         if (prm.work_ctr && !prm.xlocal) *prm.work_ctr = 0u;    // re-arm K1's counter
     }
     if (prm.xlocal) {
-        // S10: wait until every rank has published this epoch's partials (acquire, system
-        // scope; bounded: a missing peer raises ST_EXCHANGE instead of hanging the GPU)
-        if (tid == 0) {
-            // (device epoch: the word was last advanced by the previous step's tail, which
-            // completed before this step's K1 passed its griddepcontrol.wait)
-            const uint32_t xe = x_epoch(prm);
-            s_xe = xe;
-            const uint32_t *fl = reinterpret_cast<const uint32_t *>(prm.xlocal);
-            const uint64_t t0 = globaltimer_ns();
-            bool late = false;
-            for (int g = 0; g < prm.xG; ++g)
-                while ((int)(ld_acquire_sys(fl + g) - xe) < 0) {
-                    if (globaltimer_ns() - t0 > kXTimeoutNs) {
-                        atomicOr(&prm.st_ws[p], ST_EXCHANGE);
-                        late = true;
-                        break;
-                    }
-                    __nanosleep(64);
-                }
-            // re-arm K1's counter once this rank's K1 has left its work loop: its own flag
-            // says so; after a timeout, wait for the grid instead
-            if (blockIdx.x == 0 && prm.work_ctr) {
-                if (late) pdl_wait();
-                *prm.work_ctr = 0u;
-            }
-        }
+        // this launch's epoch (device epoch: advanced by the previous step's tail, which
+        // completed before this step's K1 passed its griddepcontrol.wait) picks the half
+        if (tid == 0) s_xe = x_epoch(prm);
         __syncthreads();
     }
 
@@ -1277,11 +1330,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         if (qq < nq) {
             if (prm.nparts <= 16) {
                 float4 t[4];
+                if (prm.xlocal) {
+                    if (xp_take4(pr, prm.part_seg_stride, 4 * l4, prm.nparts, t)) atomicOr(&prm.st_ws[p], ST_EXCHANGE);
+                } else {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int pi = 4 * l4 + k;
-                    t[k] = pi < prm.nparts ? __ldcg(pr + (int64_t)pi * prm.part_seg_stride)
-                                           : make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
+                    for (int k = 0; k < 4; ++k) {
+                        const int pi = 4 * l4 + k;
+                        t[k] = pi < prm.nparts ? __ldcg(pr + (int64_t)pi * prm.part_seg_stride)
+                                               : make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -1292,11 +1349,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
                 for (int k = 0; k < 4; ++k)
                     Sl = __fmaf_rn(t[k].y, t[k].x == Ml ? 1.0f : ex2_approx(t[k].x - Ml), Sl);
             } else {
+                bool late = false;
                 for (int c = 0; 4 * l4 + 16 * c < prm.nparts; ++c)
                     for (int k = 0; k < 4; ++k) {
                         const int pi = 4 * l4 + 16 * c + k;
                         if (pi < prm.nparts) {
-                            const float4 t = __ldcg(pr + (int64_t)pi * prm.part_seg_stride);
+                            const float4 *sp = pr + (int64_t)pi * prm.part_seg_stride;
+                            const float4 t = prm.xlocal ? xp_peek(sp, late) : __ldcg(sp);
                             Ml = fmaxf(Ml, t.x);
                             Xl = fmaxf(Xl, t.z);
                         }
@@ -1305,10 +1364,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
                     for (int k = 0; k < 4; ++k) {
                         const int pi = 4 * l4 + 16 * c + k;
                         if (pi < prm.nparts) {
-                            const float4 t = __ldcg(pr + (int64_t)pi * prm.part_seg_stride);
+                            const float4 *sp = pr + (int64_t)pi * prm.part_seg_stride;
+                            const float4 t = prm.xlocal ? xp_read_zero(sp) : __ldcg(sp);
                             Sl = __fmaf_rn(t.y, t.x == Ml ? 1.0f : ex2_approx(t.x - Ml), Sl);
                         }
                     }
+                if (late) atomicOr(&prm.st_ws[p], ST_EXCHANGE);
             }
         }
         float M = fmaxf(Ml, __shfl_xor_sync(0xffffffffu, Ml, 2));
@@ -1434,6 +1495,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2206);
     if (!s_last) {
+        x_tail_rearm(prm);
         x_tail_done(prm, s_xe);
         pdl_trigger();
         return;
@@ -1499,6 +1561,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         else prm.status[p] = sh.st;
     }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);
+    x_tail_rearm(prm);
     x_tail_done(prm, s_xe);
     pdl_trigger();
 }
@@ -1745,12 +1808,12 @@ __global__ void __launch_bounds__(kThreads) k_partials_rescale(const float4 *loc
     }
 }
 
-// Exchange-buffer init: flags 0, every partial slot neutral {-inf, 0, -inf, 0}.
+// Exchange-buffer init: control words and every slot zero (= not yet written).
 __global__ void k_xinit(char *base, size_t n_parts) {
     if (blockIdx.x == 0 && threadIdx.x < kXFlagBytes / 4) reinterpret_cast<uint32_t *>(base)[threadIdx.x] = 0u;
     float4 *parts = reinterpret_cast<float4 *>(base + kXFlagBytes);
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_parts; i += (size_t)gridDim.x * blockDim.x)
-        parts[i] = make_float4(-INFINITY, 0.0f, -INFINITY, 0.0f);
+        parts[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 }
 
 // Terminal selection: one index per prompt from the normalised weights by the
