@@ -733,8 +733,9 @@ def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
                                                "exchange_plus_tail_ms": round(msf - ms_k1, 4),
                                                "note": "k1_shard_ms: smcsd_weights_partial on the "
                                                        "same shard timed alone (K1 + row merge)"},
-                                 "path": "smcsd_tp_step: K1 pushes partials to peers (P2P "
-                                         "stores + release flags), tail waits (acquire) + S2-S7"}
+                                 "path": "smcsd_tp_step: K1 pushes each partial to every rank as "
+                                         "two tagged 8-byte words (P2P relaxed stores, no fence or "
+                                         "flag); the tail polls them + S2-S7"}
         # the product path is the line's cfg5 figure
         res["ms_per_step"] = round(msf, 4)
         res["steps_per_s"] = round(1e3 / msf, 1)
