@@ -41,9 +41,10 @@ for (P, N, K, V, dt) in ((1, 4, 4, 1000, torch.float32), (2, 16, 8, 20001, torch
     refc = torch.ones(P * N * PG, dtype=torch.int32, device=dev)
     smc.smcsd_kv_reindex_paged(tab, npg, refc, o.ancestors, freed=torch.zeros(P * N * PG, dtype=torch.uint8, device=dev))
     # paged append with copy-on-write of shared partial tails (after the paged resample above)
-    td, nd, _ = smc.smcsd_kv_reindex_paged(tab, npg, refc, o.ancestors)
+    refc_b = torch.ones(P * N * PG, dtype=torch.int32, device=dev)
+    td, nd, _ = smc.smcsd_kv_reindex_paged(tab, npg, refc_b, o.ancestors)
     sl = torch.full((P, N), PG * 16 - 5, dtype=torch.int32, device=dev)
-    rc2 = torch.cat([refc, torch.zeros(P * N * 2, dtype=torch.int32, device=dev)])
+    rc2 = torch.cat([refc_b, torch.zeros(P * N * 2, dtype=torch.int32, device=dev)])
     pool = synth.kv_bits((2, rc2.numel(), 16, 2, 16), seed=3).to(dev)
     smc.smcsd_kv_append_paged(td, nd, sl, rc2, torch.full((P, N), 9, dtype=torch.int32, device=dev),
                               page_size=16, pools=(smc.kv_pool(pool, **smc.paged_pool_geometry(pool)),))
