@@ -286,8 +286,9 @@ SMCSD_API smcsd_rc smcsd_kv_reindex_paged(const int32_t *table_src, const int32_
  * All-or-nothing: if any particle's state is invalid (page id outside [0, num_pages) or with
  * refcount < 1, n_pages != ceil(seq_len / page_size), n_new outside [0, max_new], more than
  * max_pages pages) its prompt gets SMCSD_ST_BAD_PAGE; if fewer pages are free than the call
- * needs every prompt gets SMCSD_ST_OUT_OF_PAGES; then *result (device int32) = 1 and nothing
- * is modified (slot_mapping and the copy list are not written).  *result = 0 on success.
+ * needs every prompt gets SMCSD_ST_OUT_OF_PAGES; then *result (device int32) = 1, nothing is
+ * modified, no content is copied, the copy list reads "none" (-1 / -1 / 0) and slot_mapping
+ * is not written.  *result = 0 on success.
  * workspace: smcsd_kv_append_workspace_bytes(P, N, num_pages, max_pages) bytes, zeroed once
  * (smcsd_workspace_init) -- the call leaves it zeroed.  num_pages * page_size < 2^31. */
 typedef struct {

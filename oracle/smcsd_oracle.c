@@ -786,8 +786,8 @@ void orc_kv_reindex_paged(const int32_t *table_src, const int32_t *n_pages_src, 
 /* The call is all-or-nothing: if any particle's state is invalid (page id out of range or   */
 /* with refcount < 1, n_pages != ceil(seq_len / page_size), n_new < 0 or > max_new, or the   */
 /* list would exceed max_pages) its prompt gets ORC_ST_BAD_PAGE; if the pool has fewer free  */
-/* pages than the call needs every prompt gets ORC_ST_OUT_OF_PAGES; then *result = 1 and     */
-/* nothing changes.  No page is freed here (copy-on-write only leaves shared pages).         */
+/* pages than the call needs every prompt gets ORC_ST_OUT_OF_PAGES; then *result = 1,        */
+/* nothing changes and the copy list reads "none" (-1, -1, 0).  No page is freed here.        */
 /* ------------------------------------------------------------------------------------ */
 #define ORC_ST_OUT_OF_PAGES 128u
 static int lowest_free(const int32_t *refcount, int num_pages, int from)
@@ -849,7 +849,14 @@ void orc_kv_append_paged(int32_t *table, int32_t *n_pages, int32_t *seq_len, int
         }
     }
     *result = ok ? 0 : 1;
-    if (!ok) return;
+    if (!ok) {
+        for (int64_t pn = 0; pn < (int64_t)P * N; ++pn) {   /* the copy list reads "none" */
+            cow_src[pn] = -1;
+            cow_dst[pn] = -1;
+            cow_tokens[pn] = 0;
+        }
+        return;
+    }
     int cursor = 0;                    /* pages below it are all in use (lowest-id allocation) */
     for (int p = 0; p < P; ++p)
         for (int n = 0; n < N; ++n) {

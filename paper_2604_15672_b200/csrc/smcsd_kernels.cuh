@@ -34,7 +34,12 @@ constexpr uint32_t ST_EXCHANGE = 32u;                         // S10 peer flag w
 constexpr uint32_t ST_BAD_INDEX = 64u;                        // reindex: src_index out of range / hazard
 constexpr uint64_t kXTimeoutNs = 20000000000ull;              // 20 s
 #ifndef SMCSD_PHASE
+#ifdef SMCSD_TRACE
+// S4-S7 phase clocks of prompt 0 (trace build): g_trace[2300 + i]
+#define SMCSD_PHASE(i) do { if (lane == 0 && p == 0) g_trace[2300 + (i)] = clock64(); } while (0)
+#else
 #define SMCSD_PHASE(i) do { } while (0)
+#endif
 #endif
 constexpr double kLn2 = 0.693147180559945309417232121458176568;
 constexpr int kRowStatSmem = 2048;                           // rows whose S2 stats fit in smem
@@ -821,11 +826,14 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
     for (int n = b0; n < b1; ++n) sh.e[n] = exp(__dsub_rn((double)sh.lam[n], M));
     __syncwarp();
     SMCSD_PHASE(2);
-    // sequential fp64 prefix and sum of squares in particle order (reading G6): one lane
-    double S = 0.0, ess = 0.0;
+    // sequential fp64 prefix and sum of squares in particle order (reading G6): one lane.  The
+    // ESS division is on the critical path only when it decides (eta finite); ESS and lse are
+    // stored after the ancestors otherwise (the log is ~270 cycles of dependent latency)
+    double S = 0.0, ess = 0.0, sq = 0.0;
     int do_res = 0;
+    const bool ess_decides = !(prm.eta == INFINITY);
     if (lane == 0) {
-        double acc = 0.0, sq = 0.0;
+        double acc = 0.0;
         for (int m = 0; m < N; ++m) {
             const double e = sh.e[m];
             acc = __dadd_rn(acc, e);
@@ -833,19 +841,29 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
             sh.C[m] = acc;
         }
         S = acc;
-        ess = __ddiv_rn(__dmul_rn(S, S), sq);
-        do_res = resample_mode && ess < prm.eta;
-        if (prm.ess) prm.ess[p] = ess;
-        if (prm.lse) prm.lse[p] = __dadd_rn(M, log(S));
+        if (ess_decides) ess = __ddiv_rn(__dmul_rn(S, S), sq);
+        do_res = resample_mode && (ess_decides ? ess < prm.eta : true);
     }
     SMCSD_PHASE(3);
     S = __shfl_sync(FULL, S, 0);
     do_res = __shfl_sync(FULL, do_res, 0);
     __syncwarp();
+    // ESS and lse (lane 0), after the work that needs only S and the decision
+    auto store_stats = [&]() {
+        if (lane == 0) {
+            const double e2 = ess_decides ? ess : __ddiv_rn(__dmul_rn(S, S), sq);
+            if (prm.ess) prm.ess[p] = e2;
+            if (prm.lse) prm.lse[p] = __dadd_rn(M, log(S));
+        }
+    };
     if (prm.wnorm)
         for (int n = b0; n < b1; ++n) prm.wnorm[base + n] = (float)__ddiv_rn(sh.e[n], S);
-    if (!resample_mode) return;
+    if (!resample_mode) {
+        store_stats();
+        return;
+    }
     if (!do_res) {
+        store_stats();
         for (int n = b0; n < b1; ++n) {
             prm.ancestors[base + n] = n;
             if (prm.offspring) prm.offspring[base + n] = 1;
@@ -932,6 +950,7 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
         prm.resampled[p] = 1;
         if (prm.n_ties) prm.n_ties[p] = ties;
     }
+    store_stats();
     SMCSD_PHASE(8);
 }
 

@@ -185,6 +185,11 @@ __global__ void __launch_bounds__(kThreads) k_append_plan(const __grid_constant_
         }
         if (!bad_any)
             for (int p = tid; p < q.P; p += kThreads) q.status[p] |= ST_OUT_OF_PAGES;
+        for (int pn = tid; pn < PN; pn += kThreads) {           // no copy-on-write to run
+            q.cow_src[pn] = -1;
+            q.cow_dst[pn] = -1;
+            q.cow_tokens[pn] = 0;
+        }
         if (tid == 0) *q.result = 1;
         pdl_trigger();
         return;
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_append_cow(const __grid_constant__
     pdl_wait();
     const int pn = blockIdx.x;
     const int cd = q.cow_dst[pn];
-    if (cd < 0) return;
+    if (cd < 0 || *q.result != 0) return;
     const int cs = q.cow_src[pn], ct = q.cow_tokens[pn];
     const int64_t pl0 = (int64_t)blockIdx.y * kCowPlanesPerCta;
     const int npl = (int)min((int64_t)kCowPlanesPerCta, q.total_planes - pl0);

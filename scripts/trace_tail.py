@@ -69,3 +69,8 @@ ck = t[2200:2207]
 if ck[0]:
     print("chunk 0 clocks after pdl_wait: " + "  ".join(
         f"{nm} {ck[i] - ck[0]}" for i, nm in enumerate(["wait", "flags", "S2 merge", "ell", "terms", "fence", "counter"]) if ck[i]))
+
+ph = t[2300:2309]
+if ph[0] and ph[1]:
+    print("S4-S7 phase clocks (prompt 0, from start): " + "  ".join(
+        f"{nm} {ph[i] - ph[0]}" for i, nm in enumerate(["start", "M", "exp", "prefix+ess", "wnorm", "C", "u+search", "plan", "S7"]) if ph[i]))

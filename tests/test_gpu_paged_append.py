@@ -49,8 +49,10 @@ def _both(smc, orc, st, n_new, page, pool=None, max_new=None):
 def _assert_same(gpu, ref, pool=None):
     assert gpu["result"] == ref["result"]
     assert np.array_equal(gpu["status"], ref["status"])
-    for k in ("table", "n_pages", "seq_len", "refcount"):
+    for k in ("table", "n_pages", "seq_len", "refcount", "cow_src", "cow_dst", "cow_tokens"):
         assert np.array_equal(gpu[k], ref[k]), k
+    if pool is not None and ref["result"] != 0:
+        assert np.array_equal(gpu["pool"], pool)                 # an aborted call copies nothing
     if ref["result"] == 0:
         for k in ("slot_mapping", "cow_src", "cow_dst", "cow_tokens"):
             assert np.array_equal(gpu[k], ref[k]), k
@@ -147,8 +149,9 @@ def test_all_or_nothing(smc, orc):
     P, N, MP, NUM, page = 2, 2, 2, 3, 16
     base = (np.full((P, N, MP), -1, np.int32), np.zeros((P, N), np.int32), np.zeros((P, N), np.int32),
             np.zeros(NUM, np.int32))
-    gpu, ref = _both(smc, orc, base, [[16, 16], [16, 16]], page)            # 4 pages > 3 free
-    _assert_same(gpu, ref)
+    pool = _kv_pool(1, NUM, page, 1, 16, seed=2)
+    gpu, ref = _both(smc, orc, base, [[16, 16], [16, 16]], page, pool=pool.copy())   # 4 pages > 3 free
+    _assert_same(gpu, ref, pool)
     assert ref["result"] == 1 and ref["status"].tolist() == [128, 128]
     gpu, ref = _both(smc, orc, base, [[0, 48], [0, 0]], page)                # > max_pages
     _assert_same(gpu, ref)

@@ -151,6 +151,7 @@ def test_all_or_nothing_failures(orc):
     out, _ = _append(orc, (table, npg, sl, rc), [[PAGE, PAGE], [PAGE, PAGE]])     # 4 pages > 3
     assert out["result"] == 1 and out["status"].tolist() == [128, 128]
     assert (out["refcount"] == 0).all() and (out["n_pages"] == 0).all()
+    assert (out["cow_dst"] == -1).all() and (out["cow_src"] == -1).all() and (out["cow_tokens"] == 0).all()
     out, _ = _append(orc, (table, npg, sl, rc), [[0, 3 * PAGE], [0, 0]])          # > max_pages
     assert out["result"] == 1 and out["status"].tolist() == [16, 0]
     npg2 = npg.copy(); npg2[1, 0] = 1                                              # inconsistent
