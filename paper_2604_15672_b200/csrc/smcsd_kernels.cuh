@@ -826,14 +826,11 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
     for (int n = b0; n < b1; ++n) sh.e[n] = exp(__dsub_rn((double)sh.lam[n], M));
     __syncwarp();
     SMCSD_PHASE(2);
-    // sequential fp64 prefix and sum of squares in particle order (reading G6): one lane.  The
-    // ESS division is on the critical path only when it decides (eta finite); ESS and lse are
-    // stored after the ancestors otherwise (the log is ~270 cycles of dependent latency)
-    double S = 0.0, ess = 0.0, sq = 0.0;
+    // sequential fp64 prefix and sum of squares in particle order (reading G6): one lane
+    double S = 0.0, ess = 0.0;
     int do_res = 0;
-    const bool ess_decides = !(prm.eta == INFINITY);
     if (lane == 0) {
-        double acc = 0.0;
+        double acc = 0.0, sq = 0.0;
         for (int m = 0; m < N; ++m) {
             const double e = sh.e[m];
             acc = __dadd_rn(acc, e);
@@ -841,29 +838,19 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
             sh.C[m] = acc;
         }
         S = acc;
-        if (ess_decides) ess = __ddiv_rn(__dmul_rn(S, S), sq);
-        do_res = resample_mode && (ess_decides ? ess < prm.eta : true);
+        ess = __ddiv_rn(__dmul_rn(S, S), sq);
+        do_res = resample_mode && ess < prm.eta;
+        if (prm.ess) prm.ess[p] = ess;
+        if (prm.lse) prm.lse[p] = __dadd_rn(M, log(S));
     }
     SMCSD_PHASE(3);
     S = __shfl_sync(FULL, S, 0);
     do_res = __shfl_sync(FULL, do_res, 0);
     __syncwarp();
-    // ESS and lse (lane 0), after the work that needs only S and the decision
-    auto store_stats = [&]() {
-        if (lane == 0) {
-            const double e2 = ess_decides ? ess : __ddiv_rn(__dmul_rn(S, S), sq);
-            if (prm.ess) prm.ess[p] = e2;
-            if (prm.lse) prm.lse[p] = __dadd_rn(M, log(S));
-        }
-    };
     if (prm.wnorm)
         for (int n = b0; n < b1; ++n) prm.wnorm[base + n] = (float)__ddiv_rn(sh.e[n], S);
-    if (!resample_mode) {
-        store_stats();
-        return;
-    }
+    if (!resample_mode) return;
     if (!do_res) {
-        store_stats();
         for (int n = b0; n < b1; ++n) {
             prm.ancestors[base + n] = n;
             if (prm.offspring) prm.offspring[base + n] = 1;
@@ -950,7 +937,6 @@ __device__ __forceinline__ void normalise_resample(const Params &prm, int p, boo
         prm.resampled[p] = 1;
         if (prm.n_ties) prm.n_ties[p] = ties;
     }
-    store_stats();
     SMCSD_PHASE(8);
 }
 
