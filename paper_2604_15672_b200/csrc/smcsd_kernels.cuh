@@ -1280,6 +1280,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     const int q0 = c * kPairsPerCta, nq = min(kPairsPerCta, NK - q0);
     const double qnan = __longlong_as_double(0x7ff8000000000000ll);
     const bool s3_local = cluster && (kPairsPerCta % K) == 0;   // uniform
+    // Distributed shared memory may only be written once the target CTA has started: every
+    // thread arrives on the cluster barrier now and waits before the first remote store (the
+    // other CTAs have long arrived by then, so the wait does not stall)
+    if (s3_local) asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
     {
 
     // ---- inputs (not produced by the predecessor): before the wait
@@ -1436,6 +1440,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     }
     if (s3_local) {
         if (st) atomicOr(&s_cst, st);
+        asm volatile("barrier.cluster.wait;" ::: "memory");     // every CTA of the cluster started
         __syncthreads();
         // S3 for this chunk's whole particles, exactly as the rank-0 loop below does it
         const int np_chunk = nq / K;
