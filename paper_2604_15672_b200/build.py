@@ -39,10 +39,15 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     """Build libsmcsd.so (or, with trace=True, the %globaltimer-instrumented debug variant
     libsmcsd_trace.so used only by scripts/trace_tail.py)."""
     lib = LIB.replace(".so", "_trace.so") if trace else LIB
-    if not force and not trace and not _stale():
+    ab = os.environ.get("SMCSD_AB_DEFS") if not trace else None      # A/B variant: libsmcsd_ab.so
+    if ab:
+        lib = LIB.replace(".so", "_ab.so")
+    if not force and not trace and not ab and not _stale():
         return LIB
     tmp = lib + ".tmp"
     extra = ["-DSMCSD_TRACE"] if trace else []
+    if ab:
+        extra += ["-D" + x for x in ab.split(",")]
     if trace and os.environ.get("SMCSD_TRACE_TWICE"):
         extra.append("-DSMCSD_TRACE_TWICE")
     if trace and os.environ.get("SMCSD_EXTRA_DEFS"):                  # timing experiments

@@ -17,6 +17,7 @@ using namespace smcsd;
 namespace {
 
 constexpr double kLog2e = 1.442695040888963407359924681001892137;
+constexpr int64_t kLateClaimItemsPerCta = 32;
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -156,7 +157,11 @@ smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
         ctas[dev] = occ * sms;
     }
     const int64_t grid = items < ctas[dev] ? items : ctas[dev];
-    return launch_pdl_b(k_rowstats<DT, PW, XP>, (unsigned)grid, smem, st, (unsigned)kK1Threads, prm);
+    // latency-bound streams (<= kLateClaimItemsPerCta items per CTA) claim items late
+    // (profiles/r02v_ab_late_claim.txt: cfg2 -0.3 us; long streams +1-3 % with it, so not there)
+    Params p2 = prm;
+    p2.late_claim = items <= kLateClaimItemsPerCta * grid;
+    return launch_pdl_b(k_rowstats<DT, PW, XP>, (unsigned)grid, smem, st, (unsigned)kK1Threads, p2);
 }
 
 // K2 tail: one CTA per 32 (particle, position) pairs of each prompt (k_tail), or one CTA per

@@ -90,6 +90,7 @@ struct Params {
     float alpha_f;                              // PowerSMC exponent (K1 second sum)
     int32_t *selected;                          // smcsd_select output [P]
     int x_from_logits;                          // 1: tail loads t_d from the logits; 0: from parts
+    int late_claim;                             // K1: claim items only when a ring slot is free
     unsigned *work_ctr;                         // K1 dynamic work counter (re-armed by K2)
     unsigned *prompt_ctr;                       // [P] K2 chunk completion counters
     uint32_t *st_ws;                            // [P] K2 status accumulation
@@ -502,6 +503,11 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
             for (long long it = 0;; ++it) {
                 const int s = (int)(it % kStages);
                 mbar_wait(&empty[s], (uint32_t)(((it / kStages) & 1) ^ 1));   // slot released
+                // short streams (a few items per CTA: the latency-bound single-prompt steps)
+                // claim the next item only once a slot is free, so no CTA holds an item while
+                // its ring is full and the last items go to CTAs that can start them at once;
+                // long streams claim one item ahead (hides the atomic behind the copies)
+                if (!XP && prm.late_claim && it > 0) item = (long long)gridDim.x + atomicAdd(prm.work_ctr, 1u);
                 StageMeta m;
                 m.item = item < total ? item : -1;
                 m.valid = 0;
@@ -531,7 +537,7 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                     mbar_arrive(&full[s]);                    // metadata only (release)
                 }
                 if (item >= total) break;
-                item = (long long)gridDim.x + atomicAdd(prm.work_ctr, 1u);
+                if (XP || !prm.late_claim) item = (long long)gridDim.x + atomicAdd(prm.work_ctr, 1u);
                 if (XP && item < total) xtok = xp_token<DT>(prm, item);   // used after the next wait
             }
         }
