@@ -11,6 +11,7 @@
 #include "smcsd.h"
 #include "smcsd_kernels.cuh"
 #include "smcsd_paged.cuh"
+#include "smcsd_lt.cuh"
 
 using namespace smcsd;
 
@@ -25,7 +26,7 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 struct WsLayout {
-    size_t ctr, pctr, pst, parts, ell, lam, e, c, rowstat, total;
+    size_t ctr, pctr, pst, parts, ell, lam, e, c, rowstat, words, total;
 };
 
 WsLayout ws_layout(int P, int N, int K, int64_t v_len) {
@@ -42,6 +43,7 @@ WsLayout ws_layout(int P, int N, int K, int64_t v_len) {
     L.e = off;        off += align256((size_t)P * N * sizeof(double));
     L.c = off;        off += align256((size_t)P * N * sizeof(double));
     L.rowstat = off;  off += align256(rows * sizeof(float4));
+    L.words = off;    off += align256(rows * nseg * sizeof(unsigned long long));   // LT words
     L.total = off;
     return L;
 }
@@ -58,7 +60,9 @@ void bind_workspace(Params &prm, void *ws, const WsLayout &L) {
     prm.prompt_ctr = reinterpret_cast<unsigned *>(b + L.pctr);
     prm.st_ws = reinterpret_cast<uint32_t *>(b + L.pst);
     prm.xctr = reinterpret_cast<unsigned *>(b + L.ctr + 64);
+    prm.lt_words = nullptr;                     // set by lt_mode() when the latency tail runs
 }
+
 
 bool valid_temp(float t) { return std::isfinite(t) && t > 0.0f; }
 
@@ -151,6 +155,7 @@ smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
     if (ctas[dev] == 0) {
         int occ = 0, sms = 0;
         if (cudaFuncSetAttribute(k_rowstats<DT, PW, XP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+            cudaFuncSetAttribute(k_rowstats<DT, PW, XP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT, PW, XP>, kK1Threads, smem) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || occ < 1)
             return SMCSD_ECUDA;
@@ -199,6 +204,32 @@ smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
 #endif
     if (cl) return launch_pdl_cluster(k_tail, (unsigned)grid, (unsigned)chunks, st, prm, resample_mode, chunks, bonus_ctas, 1);
     return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks, bonus_ctas, 0);
+}
+
+// The latency tail (smcsd_lt.cuh) replaces K2 for small steps: N <= 32 (lane per particle),
+// 2NK <= 1024 rows and <= 32 segments per row per prompt, one CTA per prompt beside K1, no bonus
+// rows, no exchange.
+int g_latency_tail = 0;                          // smcsd_set_latency_tail (experimental, off)
+
+bool lt_mode(Params &prm, void *ws, const WsLayout &L) {
+    const bool ok = g_latency_tail && prm.N <= kLtMaxN && 2 * prm.N * prm.K <= kLtMaxRows && prm.nseg <= kLtMaxParts &&
+                    prm.P <= kLtMaxP && !prm.bonus_tok && !prm.xpeer && prm.x_from_logits && prm.n_models == 2;
+    prm.lt_words = ok ? reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + L.words) : nullptr;
+    return ok;
+}
+
+smcsd_rc launch_lt(const Params &prm, int resample_mode, cudaStream_t st) {
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
+    if (!attr_set[dev]) {
+        // the same shared-memory carveout as K1, so that the SM configuration K1's CTAs run
+        // under admits this CTA beside them
+        if (cudaFuncSetAttribute(k_lt, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+            return SMCSD_ECUDA;
+        attr_set[dev] = true;
+    }
+    return launch_pdl_b(k_lt, (unsigned)prm.P, 0, st, (unsigned)kLtThreads, prm, resample_mode);
 }
 
 template <int PW>
@@ -306,9 +337,10 @@ smcsd_rc smcsd_weights(const void *logits_p, int64_t ld_p, int rows_per_particle
     prm.nparts = prm.nseg;
     const int64_t items = 2ll * P * N * K * prm.nseg;
     cudaStream_t st = as_stream(stream);
+    const bool lt = lt_mode(prm, workspace, L);
     rc = launch_rowstats(prm, dtype, items, st);
     if (rc != SMCSD_OK) return rc;
-    return launch_tail(prm, 0, st);
+    return lt ? launch_lt(prm, 0, st) : launch_tail(prm, 0, st);
 }
 
 smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t prompt_base, float eta,
@@ -373,9 +405,10 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
     prm.parts = prm.part_ws; prm.part_row_stride = prm.nseg; prm.part_seg_stride = 1;
     prm.nparts = prm.nseg;
     cudaStream_t st = as_stream(stream);
+    const bool lt = lt_mode(prm, workspace, L);
     rc = launch_rowstats(prm, dtype, prm.main_items + prm.bonus_items, st);
     if (rc != SMCSD_OK) return rc;
-    return launch_tail(prm, 1, st);
+    return lt ? launch_lt(prm, 1, st) : launch_tail(prm, 1, st);
 }
 
 smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
@@ -759,6 +792,12 @@ const char *smcsd_strerror(smcsd_rc rc) {
         case SMCSD_ENOSYS: return "not implemented in this build";
     }
     return "unknown smcsd_rc";
+}
+
+int smcsd_set_latency_tail(int enable) {
+    const int prev = g_latency_tail;
+    g_latency_tail = enable != 0;
+    return prev;
 }
 
 const char *smcsd_version(void) { return "smcsd 0.1 sm_100a"; }

@@ -41,6 +41,9 @@ constexpr uint64_t kXTimeoutNs = 20000000000ull;              // 20 s
 #define SMCSD_PHASE(i) do { } while (0)
 #endif
 #endif
+}  // namespace smcsd
+#include "smcsd_warp_tail.cuh"
+namespace smcsd {
 constexpr double kLn2 = 0.693147180559945309417232121458176568;
 constexpr int kRowStatSmem = 2048;                           // rows whose S2 stats fit in smem
 
@@ -78,6 +81,8 @@ struct Params {
     int nparts;
     // ---- workspace
     float4 *part_ws;                            // [P*2*N*K*nseg]
+    unsigned long long *lt_words;               // LT (smcsd_lt.cuh): [P*2*N*K*nseg] {m, s} words
+                                                // K1 publishes, zero between steps; or null
     double *ell_ws;                             // [P*2*N*K]
     float *lam_ws;                              // [P*N]   (N > kTailMaxN path)
     double *e_ws, *c_ws;                        // [P*N]
@@ -149,6 +154,9 @@ __device__ __forceinline__ void st_cluster_u32(uint32_t *local, unsigned rank, u
 }
 __device__ __forceinline__ void st_relaxed_sys_u64(void *p, unsigned long long v) {
     asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu_b64(void *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const void *p) {
     unsigned long long v;
@@ -471,6 +479,13 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
     }
     uint32_t *xep = reinterpret_cast<uint32_t *>(xdst + kXMaxG);     // S10: this launch's epoch
     __syncthreads();
+    if (!XP && PW == 0 && prm.lt_words) {
+        // LT mode: the latency tail runs beside this grid (it polls lt_words), so let it launch
+        // now -- after the wait, so that it too sees the predecessor's outputs.  Every thread
+        // (the consumers would wait for the producer's first copy anyway).
+        pdl_wait();
+        pdl_trigger();
+    }
     if (XP && warp < kWarps) {
         // consumers only (named barrier 1), so the producer's first TMA is not held back: the
         // epoch word is advanced by the previous step's tail, so read it after that completes,
@@ -618,7 +633,17 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                     }
                     if (lane == 0) done[s] = 0;
                 } else if (lane == 0) {
-                    prm.part_ws[m.item] = out;
+                    if (PW == 0 && prm.lt_words) {            // LT: data and flag in one word,
+                        // segment-major ([seg][row]) so that the latency tail's row-per-thread
+                        // reads are coalesced
+                        const unsigned row = fastdiv((unsigned)m.item, prm.mg_nseg, prm.sh_nseg);
+                        const unsigned sg = (unsigned)m.item - row * (unsigned)prm.nseg;
+                        st_relaxed_gpu_b64(prm.lt_words + (size_t)sg * (unsigned)(2 * prm.P * prm.N * prm.K) + row,
+                                           (unsigned long long)__float_as_uint(out.x) |
+                                           ((unsigned long long)__float_as_uint(out.y) << 32));
+                    }
+                    else
+                        prm.part_ws[m.item] = out;
                     done[s] = 0;
                 }
                 __syncwarp();
@@ -792,6 +817,30 @@ __device__ __forceinline__ void tail_prologue(const Params &prm, int p, TailSmem
     }
     sh.U = (double)x * 2.3283064365386962890625e-10;          // 2^-32, exact
     sh.reset = (float)(-log((double)prm.N));
+}
+
+// Uniform of particle n (weight-independent): systematic u_n = (n + U) / N with U = word 0 of
+// Philox(step, prompt, 0) (or uniforms[p]) times 2^-32; multinomial u_n = word n & 3 of
+// Philox(step, prompt, 1 + n / 4) (or uniforms[p][n]) times 2^-32.  Exactly the values
+// normalise_resample forms.
+__device__ __forceinline__ double tail_uniform(const Params &prm, int p, int n) {
+    const uint64_t gp = (uint64_t)(prm.prompt_base + p);
+    const uint2 key = make_uint2((uint32_t)prm.seed, (uint32_t)(prm.seed >> 32));
+    uint32_t x;
+    if (prm.scheme == 0) {
+        x = prm.uniforms ? prm.uniforms[p]
+                         : philox4x32_10(make_uint4((uint32_t)prm.step, (uint32_t)(prm.step >> 32), (uint32_t)gp, 0u), key).x;
+        return __ddiv_rn(__dadd_rn((double)n, (double)x * 2.3283064365386962890625e-10), (double)prm.N);
+    }
+    if (prm.uniforms) {
+        x = n < prm.N ? prm.uniforms[(int64_t)p * prm.N + n] : 0u;
+    } else {
+        const uint4 r = philox4x32_10(
+            make_uint4((uint32_t)prm.step, (uint32_t)(prm.step >> 32), (uint32_t)gp, 1u + (uint32_t)(n >> 2)), key);
+        const int w = n & 3;
+        x = w == 0 ? r.x : w == 1 ? r.y : w == 2 ? r.z : r.w;
+    }
+    return (double)x * 2.3283064365386962890625e-10;
 }
 
 __device__ __forceinline__ void normalise_resample(const Params &prm, int p, bool resample_mode, TailSmem &sh) {
@@ -1266,6 +1315,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     __shared__ double term_s[kPairsPerCta];
     __shared__ uint32_t s_cst;                                  // this chunk's status bits
     __shared__ uint32_t s_flags[16];                            // rank 0: every chunk's bits
+    __shared__ __align__(16) WtSmem wts;                        // N <= 32: warp-synchronous S4-S7
     const int tid = threadIdx.x;
     const int N = prm.N, K = prm.K, NK = N * K, rows = 2 * NK;
     const int chunk_ctas = prm.P * chunks_per_prompt;
@@ -1290,6 +1340,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     // thread arrives on the cluster barrier now and waits before the first remote store (the
     // other CTAs have long arrived by then, so the wait does not stall)
     if (s3_local) asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+    // N <= 32: this lane's uniform for warp_tail (weight-independent, drawn before the wait)
+    const double u_lane = (N <= 32 && resample_mode && tid < 32) ? tail_uniform(prm, p, tid) : 0.0;
     {
 
     // ---- inputs (not produced by the predecessor): before the wait
@@ -1311,6 +1363,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         sh.st = 0;
         s_cst = 0;
         if (resample_mode) tail_prologue(prm, p, sh);
+        wts.a = WtArgs{prm.logw_out, prm.wnorm, prm.lse, prm.ess, prm.ancestors, prm.offspring,
+                       prm.slot_src, prm.n_ties, prm.resampled, prm.eta, prm.N, prm.scheme};
+        wts.st = 0u;
     }
     if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2048);      // tail CTA resident
     // S10 (xlocal): the pushed words themselves are the dependency (the tail polls them), so
@@ -1570,11 +1625,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     __syncthreads();
     }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2051);
-    normalise_resample(prm, p, resample_mode != 0, sh);
+    if (N <= 32) {
+        if (tid < 64) warp_tail(tid >> 5, p, resample_mode, 0, sh.lam[tid & 31], u_lane, sh.reset, wts);
+    } else {
+        normalise_resample(prm, p, resample_mode != 0, sh);
+    }
     __syncthreads();
     if (tid == 0) {
-        if (bonus_ctas) atomicOr(&prm.status[p], sh.st);
-        else prm.status[p] = sh.st;
+        const uint32_t st_all = sh.st | wts.st;
+        if (bonus_ctas) atomicOr(&prm.status[p], st_all);
+        else prm.status[p] = st_all;
     }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);
     x_tail_rearm(prm);

@@ -17,6 +17,8 @@ P, N, K, V = int(os.environ.get("P", 1)), int(os.environ.get("N", 16)), 8, 12825
 dev = torch.device("cuda")
 ring = [synth.lm_logits(P, N, K, V, device=dev, seed=100 + r) for r in range(6)]
 lib = ctypes.CDLL(smc.lib_path)
+if os.environ.get("SMCSD_LT"):
+    smc.smcsd_set_latency_tail(True)
 buf = (ctypes.c_ulonglong * 4096)()
 flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)
 TP = os.environ.get("TP")            # fused-exchange smcsd_tp_step at G = 1 instead of smcsd_step
@@ -60,7 +62,8 @@ e = sorted(us(x) for x in ends)
 print(f"K1 CTAs {len(starts)}: start spread {s[-1]:.2f} us; done min {e[0]:.2f} median {e[len(e)//2]:.2f} "
       f"p90 {e[int(len(e)*0.9)]:.2f} max {e[-1]:.2f} us")
 names = {2060: "TP: last K1 CTA counted", 2061: "TP: system fence done", 2048: "tail CTA resident", 2049: "tail after pdl_wait", 2053: "chunk 0 S2+terms done", 2050: "last CTA of prompt 0", 2051: "after S3",
-         2052: "after S4-S7"}
+         2052: "after S4-S7", 2400: "LT CTA resident", 2401: "LT inputs+warm-up", 2402: "LT S2+S3 done",
+         2403: "LT S4-S7 done"}
 for k, nm in names.items():
     if not t[k]:
         continue
@@ -71,6 +74,16 @@ if ck[0]:
         f"{nm} {ck[i] - ck[0]}" for i, nm in enumerate(["wait", "flags", "S2 merge", "ell", "terms", "fence", "counter"]) if ck[i]))
 
 ph = t[2300:2309]
+PHASES = (["start", "exp", "prefix+ess", "anc+ties", "offspring+plan", "S7 stores", "ess/lse/wnorm"] if t[2400] else
+          ["start", "M", "exp", "prefix+ess", "wnorm", "C", "u+search", "plan", "S7"])
 if ph[0] and ph[1]:
     print("S4-S7 phase clocks (prompt 0, from start): " + "  ".join(
-        f"{nm} {ph[i] - ph[0]}" for i, nm in enumerate(["start", "M", "exp", "prefix+ess", "wnorm", "C", "u+search", "plan", "S7"]) if ph[i]))
+        f"{nm} {ph[i] - ph[0]}" for i, nm in enumerate(PHASES) if ph[i]))
+
+lp_ = [t[2410 + i] for i in range(64) if t[2410 + i]]
+if lp_:
+    print("LT pass ends (us): " + " ".join(f"{us(x):.2f}" for x in lp_))
+
+c = t[2490:2495]
+if c[0]:
+    print("LT last row clocks: poll %d  merge+ell %d | tid0: barrier->S3 done %d" % (c[1] - c[0], c[2] - c[1], c[4] - c[3]))

@@ -1,0 +1,96 @@
+"""GPU: the latency tail (smcsd_lt.cuh, smcsd_set_latency_tail) -- S2-S7 in a kernel that runs
+beside K1 and polls K1's {m, s} words -- against the two-kernel path (bit-identical outputs) and
+against the CPU oracle (staged protocol: the oracle's S4-S7 from the GPU's logw_pre gives the same
+ancestry).  Also the word array is left zero (the next call depends on it)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from gpu_util import max_abs, np_, to_host
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("logw", "logw_pre", "logp_tok", "logq_tok", "lse", "ess", "wnorm", "status", "ancestors",
+          "offspring", "slot_src", "resampled", "n_ties")
+
+
+@pytest.fixture(scope="module")
+def smc():
+    import paper_2604_15672_b200 as m
+    assert torch.cuda.is_available()
+    prev = m.smcsd_set_latency_tail(False)
+    yield m
+    m.smcsd_set_latency_tail(prev)
+
+
+def _bits(t):
+    return t.view(torch.uint8) if t.is_floating_point() else t
+
+
+def _run(smc, lt, mode, lp, lq, tok, ws, **kw):
+    smc.smcsd_set_latency_tail(lt)
+    try:
+        if mode == "step":
+            o = smc.smcsd_step(lp, lq, tok, workspace=ws, **kw)
+        else:
+            kw = {k: v for k, v in kw.items() if k in ("V", "n_drafted", "logw_prev", "alpha", "inv_temp_p")}
+            o = smc.smcsd_weights(lp, lq, tok, workspace=ws, **kw)
+        torch.cuda.synchronize()
+    finally:
+        smc.smcsd_set_latency_tail(False)
+    return {f: getattr(o, f).clone() for f in FIELDS if getattr(o, f, None) is not None}
+
+
+@pytest.mark.parametrize("P,N,K,V,dtype,extra", [
+    (1, 16, 8, 128256, torch.bfloat16, {}),                                  # cfg2
+    (1, 4, 4, 1000, torch.float32, {}),                                      # one pass, cfg1-like
+    (3, 32, 8, 50001, torch.bfloat16, {}),                                   # 4 passes, ragged V
+    (2, 7, 3, 20001, torch.float32, {"scheme": 1}),                          # multinomial
+    (1, 1, 1, 7, torch.float32, {}),                                         # N = 1, V < vector
+    (4, 32, 16, 128256, torch.bfloat16, {"eta": None}),                      # eta = N/2, 1024 rows
+    (2, 12, 8, 131072, torch.bfloat16, {}),                                  # 16 full segments
+    (5, 8, 16, 32000, torch.bfloat16, {"alpha": 0.7, "inv_temp_p": 1.3}),
+])
+@pytest.mark.parametrize("mode", ["step", "weights"])
+def test_latency_tail_bit_identical(smc, P, N, K, V, dtype, extra, mode):
+    dev = torch.device("cuda")
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=dtype, seed=900 + N + V, bonus=False)
+    lp, lq, tok = lp.to(dev), lq.to(dev), tok.to(dev)
+    g = torch.Generator().manual_seed(N * 7 + K)
+    nd = torch.randint(0, K + 1, (P, N), dtype=torch.int32, generator=g).to(dev)
+    prev = (torch.randn(P, N, generator=g) * 0.3).to(dev)
+    for ndv in (None, nd):
+        kw = dict(V=V, n_drafted=ndv, logw_prev=prev, step=3, eta=extra.get("eta", math.inf))
+        kw.update({k: v for k, v in extra.items() if k != "eta"})
+        ws = smc.Workspace(dev)
+        ref = _run(smc, False, mode, lp, lq, tok, ws, **kw)
+        for rep in range(2):                     # twice on one workspace: the words were re-zeroed
+            got = _run(smc, True, mode, lp, lq, tok, ws, **kw)
+            for f in ref:
+                assert torch.equal(_bits(ref[f]), _bits(got[f])), (f, rep, ndv is not None)
+
+
+def test_latency_tail_staged_oracle_parity(smc, orc):
+    # the GPU's lam' (logw_pre) within 1e-4 of the oracle's, and the oracle's S4-S7 from it gives
+    # the GPU's ancestry bit-exactly (reading G7: no ties here)
+    P, N, K, V = 2, 16, 8, 128256
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=31, bonus=False)
+    dev = torch.device("cuda")
+    prev = synth.uniform_prior(P, N)
+    smc.smcsd_set_latency_tail(True)
+    try:
+        out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, logw_prev=prev.to(dev),
+                             eta=math.inf, seed=7, step=4, prompt_base=11)
+        torch.cuda.synchronize()
+    finally:
+        smc.smcsd_set_latency_tail(False)
+    ref_w = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, logw_prev=prev.numpy())
+    assert max_abs(np_(out.logw_pre), ref_w["logw"]) <= 1e-4
+    staged = orc.resample(np_(out.logw_pre), eta=math.inf, seed=7, step=4, prompt_base=11)
+    assert np.array_equal(np_(out.ancestors), staged["ancestors"])
+    assert np.array_equal(np_(out.slot_src), staged["slot_src"])
+    assert np.array_equal(np_(out.n_ties), staged["n_ties"])
+    assert np.all(np_(out.status) == 0)
