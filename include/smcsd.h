@@ -370,6 +370,16 @@ SMCSD_API smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_pe
                        int32_t *slot_src, uint8_t *resampled, int32_t *n_ties,
                        void *workspace, size_t workspace_bytes, void *stream);
 
+/* Polling tail switch (process-wide; default 1 = on).  With it on, smcsd_step and smcsd_weights
+ * calls without the bonus token, with at most 16 segments per row (V <= 131072) and N <= 1024
+ * let K1 publish each (row, segment) {m, s} as one 8-byte word and launch the tail at once; the
+ * tail polls those words instead of waiting for K1's grid to complete and flush (results are
+ * bit-identical).  The words live in the workspace and are zero between calls (the tail clears
+ * them); after a call that returned an error, re-initialise the workspace.  0 restores the
+ * wait-for-K1 tail (A/B timing, tests).  Not synchronised with calls in flight on other host
+ * threads.  Returns the previous setting. */
+SMCSD_API int smcsd_set_poll_tail(int enable);
+
 /* Latency tail switch (process-wide; default 0 = off, experimental).  With it on, smcsd_step and smcsd_weights
  * run S2-S7 of small calls (N <= 32, 2*N*K <= 1024, ceil(V / 8192) <= 32, P <= 148, no bonus
  * token) in a kernel that runs beside K1 and polls K1's per-segment {m, s} words instead of

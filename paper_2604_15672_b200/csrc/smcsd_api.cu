@@ -60,7 +60,7 @@ void bind_workspace(Params &prm, void *ws, const WsLayout &L) {
     prm.prompt_ctr = reinterpret_cast<unsigned *>(b + L.pctr);
     prm.st_ws = reinterpret_cast<uint32_t *>(b + L.pst);
     prm.xctr = reinterpret_cast<unsigned *>(b + L.ctr + 64);
-    prm.lt_words = nullptr;                     // set by lt_mode() when the latency tail runs
+    prm.lt_words = nullptr;                     // set by tail_mode() for the polling tails
 }
 
 
@@ -210,12 +210,31 @@ smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
 // 2NK <= 1024 rows and <= 32 segments per row per prompt, one CTA per prompt beside K1, no bonus
 // rows, no exchange.
 int g_latency_tail = 0;                          // smcsd_set_latency_tail (experimental, off)
+#ifndef SMCSD_NO_POLL_TAIL
+int g_poll_tail = 1;                             // smcsd_set_poll_tail
+#else
+int g_poll_tail = 0;
+#endif
 
-bool lt_mode(Params &prm, void *ws, const WsLayout &L) {
-    const bool ok = g_latency_tail && prm.N <= kLtMaxN && 2 * prm.N * prm.K <= kLtMaxRows && prm.nseg <= kLtMaxParts &&
-                    prm.P <= kLtMaxP && !prm.bonus_tok && !prm.xpeer && prm.x_from_logits && prm.n_models == 2;
-    prm.lt_words = ok ? reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + L.words) : nullptr;
-    return ok;
+// Tail modes of smcsd_step / smcsd_weights.  K1 publishes {m, s} words (prm.lt_words) and
+// launches its dependents at once in both polling modes:
+//   TAIL_LT    -- k_lt (smcsd_lt.cuh), experimental, smcsd_set_latency_tail;
+//   TAIL_POLL  -- k_tail polls the words instead of waiting for K1's grid (no bonus rows, at
+//                 most 16 segments per row: one word per lane per part group);
+//   TAIL_WAIT  -- k_tail behind griddepcontrol.wait on K1's float4 partials (every other call).
+enum TailMode { TAIL_WAIT = 0, TAIL_POLL = 1, TAIL_LT = 2 };
+
+TailMode tail_mode(Params &prm, void *ws, const WsLayout &L) {
+    prm.lt_words = nullptr;
+    const bool common = !prm.bonus_tok && !prm.xpeer && prm.x_from_logits && prm.n_models == 2;
+    TailMode m = TAIL_WAIT;
+    if (common && g_latency_tail && prm.N <= kLtMaxN && 2 * prm.N * prm.K <= kLtMaxRows &&
+        prm.nseg <= kLtMaxParts && prm.P <= kLtMaxP)
+        m = TAIL_LT;
+    else if (common && g_poll_tail && prm.nseg <= 16 && prm.N <= kTailMaxN)
+        m = TAIL_POLL;
+    if (m != TAIL_WAIT) prm.lt_words = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + L.words);
+    return m;
 }
 
 smcsd_rc launch_lt(const Params &prm, int resample_mode, cudaStream_t st) {
@@ -337,10 +356,10 @@ smcsd_rc smcsd_weights(const void *logits_p, int64_t ld_p, int rows_per_particle
     prm.nparts = prm.nseg;
     const int64_t items = 2ll * P * N * K * prm.nseg;
     cudaStream_t st = as_stream(stream);
-    const bool lt = lt_mode(prm, workspace, L);
+    const TailMode tm = tail_mode(prm, workspace, L);
     rc = launch_rowstats(prm, dtype, items, st);
     if (rc != SMCSD_OK) return rc;
-    return lt ? launch_lt(prm, 0, st) : launch_tail(prm, 0, st);
+    return tm == TAIL_LT ? launch_lt(prm, 0, st) : launch_tail(prm, 0, st);
 }
 
 smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t prompt_base, float eta,
@@ -405,10 +424,10 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
     prm.parts = prm.part_ws; prm.part_row_stride = prm.nseg; prm.part_seg_stride = 1;
     prm.nparts = prm.nseg;
     cudaStream_t st = as_stream(stream);
-    const bool lt = lt_mode(prm, workspace, L);
+    const TailMode tm = tail_mode(prm, workspace, L);
     rc = launch_rowstats(prm, dtype, prm.main_items + prm.bonus_items, st);
     if (rc != SMCSD_OK) return rc;
-    return lt ? launch_lt(prm, 1, st) : launch_tail(prm, 1, st);
+    return tm == TAIL_LT ? launch_lt(prm, 1, st) : launch_tail(prm, 1, st);
 }
 
 smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
@@ -792,6 +811,12 @@ const char *smcsd_strerror(smcsd_rc rc) {
         case SMCSD_ENOSYS: return "not implemented in this build";
     }
     return "unknown smcsd_rc";
+}
+
+int smcsd_set_poll_tail(int enable) {
+    const int prev = g_poll_tail;
+    g_poll_tail = enable != 0;
+    return prev;
 }
 
 int smcsd_set_latency_tail(int enable) {

@@ -158,6 +158,11 @@ __device__ __forceinline__ void st_relaxed_sys_u64(void *p, unsigned long long v
 __device__ __forceinline__ void st_relaxed_gpu_b64(void *p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_b64(const void *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const void *p) {
     unsigned long long v;
     asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1011,7 +1016,7 @@ constexpr int kPairsPerCta = 32;
 // S10: re-arm K1's work counter once this rank's K1 grid has completed (CTA 0, at its exit:
 // off the critical path; the next step's K1 reads the counter after its own griddepcontrol.wait)
 __device__ __forceinline__ void x_tail_rearm(const Params &prm) {
-    if (prm.xlocal && prm.work_ctr && blockIdx.x == 0 && threadIdx.x == 0) {
+    if ((prm.xlocal || prm.lt_words) && prm.work_ctr && blockIdx.x == 0 && threadIdx.x == 0) {
         pdl_wait();
         *prm.work_ctr = 0u;
     }
@@ -1038,6 +1043,41 @@ __device__ __forceinline__ float4 xp_decode(unsigned long long a, unsigned long 
     return make_float4(__uint_as_float((uint32_t)a), __uint_as_float((uint32_t)(a >> 32)),
                        __uint_as_float((uint32_t)b), 0.0f);
 }
+// Polling tail (prm.lt_words): parts pi0 .. pi0+3 of global row g from K1's segment-major
+// {m, s} words (nonzero once written; zeroed here for the next step).  Returns true on timeout
+// (the missing parts become neutral {-inf, 0}).
+__device__ __forceinline__ bool lt_take4(unsigned long long *words, int64_t total_rows, int64_t g, int pi0,
+                                         int nparts, float4 (&t)[4]) {
+    unsigned long long a[4];
+    bool nd[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        nd[k] = pi0 + k < nparts;
+        a[k] = nd[k] ? ld_relaxed_gpu_b64(words + (pi0 + k) * total_rows + g) : 0x00000000FF800000ull;
+    }
+    bool late = false;
+    uint64_t t0 = 0;
+    for (;;) {
+        bool all = true;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) all &= a[k] != 0ull;
+        if (all) break;
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > kXTimeoutNs) { late = true; break; }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (a[k] == 0ull) a[k] = ld_relaxed_gpu_b64(words + (pi0 + k) * total_rows + g);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (a[k] == 0ull) a[k] = 0x00000000FF800000ull;
+        t[k] = make_float4(__uint_as_float((uint32_t)a[k]), __uint_as_float((uint32_t)(a[k] >> 32)), -INFINITY, 0.0f);
+        if (nd[k]) __stcg(words + (pi0 + k) * total_rows + g, 0ull);
+    }
+    return late;
+}
+
 __device__ __forceinline__ bool xp_take4(const float4 *pr, int64_t stride, int pi0, int nparts, float4 (&t)[4]) {
     const unsigned long long *w[4];
     unsigned long long a[4], b[4];
@@ -1342,13 +1382,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     if (s3_local) asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
     // N <= 32: this lane's uniform for warp_tail (weight-independent, drawn before the wait)
     const double u_lane = (N <= 32 && resample_mode && tid < 32) ? tail_uniform(prm, p, tid) : 0.0;
+    int lr_model = 0, lr_q = 0;
+    int64_t lr_pn = 0;
+    float prev3 = 0.0f;                                         // S3 in the chunk: lam_prev, then lam'
+    const bool row_thread = tid < 2 * kPairsPerCta && (tid & (kPairsPerCta - 1)) < nq;
     {
 
     // ---- inputs (not produced by the predecessor): before the wait
-    int lr_model = 0, lr_q = 0, lr_kn = 0;
-    int64_t lr_pn = 0, lr_d = -1;
+    int lr_kn = 0;
+    int64_t lr_d = -1;
     float x_pre = -INFINITY;
-    const bool row_thread = tid < 2 * kPairsPerCta && (tid & (kPairsPerCta - 1)) < nq;
     if (row_thread) {
         lr_model = tid / kPairsPerCta;
         lr_q = q0 + (tid & (kPairsPerCta - 1));
@@ -1358,6 +1401,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         lr_d = prm.tokens[lr_pn * K + j];
         if (prm.x_from_logits && lr_kn >= 0 && lr_kn <= K && j < lr_kn && lr_d >= 0 && lr_d < prm.V)
             x_pre = load_x(prm, lr_model, lr_pn, j, lr_d);
+    }
+    // k_n of this thread's pair (terms) and, with S3 in the chunk, of its particle and lam_prev
+    // (logw_prev may be the previous step's output: complete before K1 launched this grid)
+    const int kn_t = tid < nq ? drafted_len(prm, (int64_t)p * N + (q0 + tid) / K) : 0;
+    int kn3 = 0;
+    if (s3_local && tid < nq / K) {
+        const int64_t pn = (int64_t)p * N + q0 / K + tid;
+        kn3 = drafted_len(prm, pn);
+        prev3 = prm.logw_prev ? prm.logw_prev[pn] : (float)(-log((double)N));
     }
     if (tid == 0) {
         sh.st = 0;
@@ -1370,11 +1422,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2048);      // tail CTA resident
     // S10 (xlocal): the pushed words themselves are the dependency (the tail polls them), so
     // the tail does not wait for K1's grid to complete and flush.
-    if (!prm.xlocal) pdl_wait();
+    // Polling tail (lt_words): likewise K1's {m, s} words are the dependency; K1's counter is
+    // re-armed at exit, once K1's grid has completed (x_tail_rearm).
+    if (!prm.xlocal && !prm.lt_words) pdl_wait();
     if (tid == 0 && blockIdx.x == 0) {
         SMCSD_TRACE_AT(2049);                                   // predecessor complete
         SMCSD_CLK_AT(2200);
-        if (prm.work_ctr && !prm.xlocal) *prm.work_ctr = 0u;    // re-arm K1's counter
+        if (prm.work_ctr && !prm.xlocal && !prm.lt_words) *prm.work_ctr = 0u;    // re-arm K1's counter
     }
     if (prm.xlocal) {
         // this launch's epoch (device epoch: advanced by the previous step's tail, which
@@ -1391,6 +1445,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2201);
     // S10 with the device epoch: this epoch's parity half of the exchange buffer
     const float4 *parts = prm.xlocal && !prm.xepoch ? prm.parts + (int64_t)(s_xe & 1u) * prm.xhalf : prm.parts;
+    bool s2_late = false;                                       // polling tail: a word timed out
     {
         const int l4 = tid & 3, lr = tid >> 2;                  // local row: model = lr / 32
         const int qq = lr & (kPairsPerCta - 1);
@@ -1402,6 +1457,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
                 float4 t[4];
                 if (prm.xlocal) {
                     if (xp_take4(pr, prm.part_seg_stride, 4 * l4, prm.nparts, t)) atomicOr(&prm.st_ws[p], ST_EXCHANGE);
+                } else if (prm.lt_words) {
+                    s2_late = lt_take4(prm.lt_words, 2ll * prm.P * NK, grow, 4 * l4, prm.nparts, t);
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -1457,7 +1514,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2202);
     // ---- ell per row (thread = local row), then terms per pair
-    uint32_t st = 0;
+    uint32_t st = s2_late ? ST_EXCHANGE : 0u;
     if (row_thread) {
         const int j = lr_q - (lr_q / K) * K;
         const bool valid = lr_kn >= 0 && lr_kn <= K && j < lr_kn;
@@ -1476,14 +1533,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
             ell = __dmul_rn(__dsub_rn(__dsub_rn((double)x, (double)m.x), (double)log2f(m.y)), kLn2);
         }
         ell_s[tid] = ell;
+        // with S3 in the chunk these output stores go after the cluster barrier's arrive (a
+        // release would wait for them)
         float *outp = lr_model == 0 ? prm.logp_tok : prm.logq_tok;
-        if (outp) outp[lr_pn * K + j] = (float)ell;
+        if (outp && !s3_local) outp[lr_pn * K + j] = (float)ell;
     }
     __syncthreads();
     if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2203);
     if (tid < nq) {
         const int qq = q0 + tid, j = qq - (qq / K) * K;
-        const int kn = drafted_len(prm, (int64_t)p * N + qq / K);
+        const int kn = kn_t;
         double term = 0.0;
         if (kn >= 0 && kn <= K && j < kn) {
             const double lp = ell_s[tid], lq = ell_s[kPairsPerCta + tid];
@@ -1509,8 +1568,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
         if (tid < np_chunk) {
             const int n = q0 / K + tid;
-            const int64_t pn = (int64_t)p * N + n;
-            int kn = drafted_len(prm, pn);
+            int kn = kn3;
             uint32_t st3 = 0;
             bool bad = false;
             if (kn < 0 || kn > K) {
@@ -1521,15 +1579,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
             double delta = 0.0;
             for (int j = 0; j < kn; ++j) delta = __dadd_rn(delta, term_s[tid * K + j]);
             if (isnan(delta)) bad = true;
-            const float prev = prm.logw_prev ? prm.logw_prev[pn] : (float)(-log((double)N));
+            const float prev = prev3;
             if (isnan(prev) || prev == INFINITY) {
                 st3 |= ST_NONFINITE;
                 bad = true;
             }
             const float lam = bad ? -INFINITY : (float)__dadd_rn((double)prev, delta);
             st_cluster_f32(&sh.lam[n], 0u, lam);
-            if (prm.logw_pre) prm.logw_pre[pn] = lam;
-            if (!resample_mode) prm.logw_out[pn] = lam;
+            prev3 = lam;                                        // stored after the arrive
             if (st3) atomicOr(&s_cst, st3);
         }
         __syncthreads();
@@ -1548,7 +1605,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
         // acquire at cluster scope, covering the global terms and flags) replaces the counter,
         // and cluster rank 0 finishes the prompt
         if (tid == 0 && blockIdx.x == 0) SMCSD_CLK_AT(2205);
-        asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+        asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+        if (s3_local) {
+            // this chunk's outputs, after the arrive: nothing in the cluster reads them
+            if (row_thread) {
+                float *outp = lr_model == 0 ? prm.logp_tok : prm.logq_tok;
+                if (outp) outp[lr_pn * K + (lr_q - (lr_q / K) * K)] = (float)ell_s[tid];
+            }
+            if (tid < nq / K) {
+                const int64_t pn = (int64_t)p * N + q0 / K + tid;
+                if (prm.logw_pre) prm.logw_pre[pn] = prev3;
+                if (!resample_mode) prm.logw_out[pn] = prev3;
+            }
+        }
+        asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
         if (tid == 0) {
             unsigned r;
             asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

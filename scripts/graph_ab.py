@@ -10,10 +10,13 @@ import synth
 
 dev = torch.device("cuda")
 name = os.path.basename(smc.lib_path)
+if os.environ.get("SMCSD_POLL") is not None:                  # polling tail on / off
+    smc.smcsd_set_poll_tail(os.environ["SMCSD_POLL"] == "1")
+    name += " poll=" + os.environ["SMCSD_POLL"]
 
 
-def case(label, N, ring_n=6, reps=20):
-    ring = [synth.lm_logits(1, N, 8, 128256, device=dev, seed=10 + r) for r in range(ring_n)]
+def case(label, N, ring_n=6, reps=20, P=1):
+    ring = [synth.lm_logits(P, N, 8, 128256, device=dev, seed=10 + r) for r in range(ring_n)]
     ws, out = smc.Workspace(dev), smc.Outputs()
     call = lambda i: smc.smcsd_step(*ring[i % ring_n], V=128256, step=i, out=out, fields=(), workspace=ws)
     for i in range(3):
@@ -55,3 +58,5 @@ def case(label, N, ring_n=6, reps=20):
 
 case("cfg2", 16)
 case("N64", 64, ring_n=3)
+if os.environ.get("CFG4"):
+    case("cfg4", 32, ring_n=2, reps=5, P=64)
