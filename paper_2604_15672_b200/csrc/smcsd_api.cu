@@ -146,22 +146,32 @@ smcsd_rc launch_pdl(void (*kernel)(KArgs...), unsigned grid, size_t smem, cudaSt
 }
 
 // K1 persistent grid: SMs x resident CTAs (shared-memory ring), capped by the work items.
+// Resident CTAs of K1 variant <DT, PW, XP> on the current device (SMs x CTAs per SM; cached,
+// with the kernel's shared-memory attributes set on first use), or 0 on a CUDA error.
 template <int DT, int PW, bool XP = false>
-smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
+int k1_ctas() {
     static int ctas[64] = {0};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
-    const size_t smem = rowstats_smem_bytes<DT, XP>();
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 0;
     if (ctas[dev] == 0) {
+        const size_t smem = rowstats_smem_bytes<DT, XP>();
         int occ = 0, sms = 0;
         if (cudaFuncSetAttribute(k_rowstats<DT, PW, XP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
             cudaFuncSetAttribute(k_rowstats<DT, PW, XP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rowstats<DT, PW, XP>, kK1Threads, smem) != cudaSuccess ||
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || occ < 1)
-            return SMCSD_ECUDA;
+            return 0;
         ctas[dev] = occ * sms;
     }
-    const int64_t grid = items < ctas[dev] ? items : ctas[dev];
+    return ctas[dev];
+}
+
+template <int DT, int PW, bool XP = false>
+smcsd_rc launch_rowstats_dt(const Params &prm, int64_t items, cudaStream_t st) {
+    const int ctas = k1_ctas<DT, PW, XP>();
+    if (ctas == 0) return SMCSD_ECUDA;
+    const size_t smem = rowstats_smem_bytes<DT, XP>();
+    const int64_t grid = items < ctas ? items : ctas;
     // latency-bound streams (<= kLateClaimItemsPerCta items per CTA) claim items late
     // (profiles/r02v_ab_late_claim.txt: cfg2 -0.3 us; long streams +1-3 % with it, so not there)
     Params p2 = prm;
@@ -231,8 +241,9 @@ TailMode tail_mode(Params &prm, void *ws, const WsLayout &L) {
     if (common && g_latency_tail && prm.N <= kLtMaxN && 2 * prm.N * prm.K <= kLtMaxRows &&
         prm.nseg <= kLtMaxParts && prm.P <= kLtMaxP)
         m = TAIL_LT;
-    else if (common && g_poll_tail && prm.nseg <= 16 && prm.N <= kTailMaxN)
-        m = TAIL_POLL;
+    else if (common && g_poll_tail && prm.nseg <= 16 && prm.N <= kTailMaxN &&
+             prm.main_items <= kLateClaimItemsPerCta * (int64_t)(prm.dtype == SMCSD_BF16 ? k1_ctas<1, 0>() : k1_ctas<0, 0>()))
+        m = TAIL_POLL;                   // latency-bound steps only (cfg4-sized streams: +10 us)
     if (m != TAIL_WAIT) prm.lt_words = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + L.words);
     return m;
 }

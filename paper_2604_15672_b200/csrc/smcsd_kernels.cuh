@@ -218,6 +218,9 @@ __device__ __forceinline__ float load_x(const Params &prm, int model, int64_t pn
 // with s2 = sum 2^(alpha (t - m)) for PowerSMC (PW != 0), 0 otherwise.  PW = -1: general alpha,
 // a second ex2 per element; PW = k in 1..4: alpha == k, 2^(k t') = (2^t')^k by k-1 multiplies of
 // the ex2 already taken for s (no second MUFU op; keeps the power sum at the HBM roofline).
+#ifndef SMCSD_K1_POLY_K
+#define SMCSD_K1_POLY_K 4             // plain exp-sum: all on MUFU (see reduce_item)
+#endif
 #ifndef SMCSD_POW_POLY_K
 #define SMCSD_POW_POLY_K 2            // pairs k >= this (of 4 per 16-byte vector) on the FMA pipe
 #endif
@@ -276,7 +279,12 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
         for (int i = 0; i < T::kLoads; ++i) {
             const uint32_t w4[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
 #pragma unroll
-            for (int k = 0; k < 4; ++k) asm("max.bf16x2 %0, %0, %1;" : "+r"(acc) : "r"(w4[k]));
+            for (int k = 0; k < 4; ++k) {
+                if (SMCSD_K1_POLY_K < 4 && PW == 0)             // the polynomial does not carry NaN
+                    asm("max.NaN.bf16x2 %0, %0, %1;" : "+r"(acc) : "r"(w4[k]));
+                else
+                    asm("max.bf16x2 %0, %0, %1;" : "+r"(acc) : "r"(w4[k]));
+            }
         }
         mt = fmaxf(bf16lo(acc), bf16hi(acc));
     } else {
@@ -310,7 +318,10 @@ __device__ __forceinline__ void reduce_item(uint4 (&v)[ItemTraits<DT>::kLoads], 
                 continue;
             }
             const float2 t = ffma2(z, cc, mo);
-            const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+            // (A/B option SMCSD_K1_POLY_K < 4: pairs k >= it of each bf16 vector on the FMA-pipe
+            // polynomial instead of MUFU -- slower burst and sustained, profiles/r02c_ab_k1_poly_sustained.txt)
+            const float2 e = PW == 0 && DT == 1 && k >= SMCSD_K1_POLY_K ? ex2_poly2(t)
+                                                                        : make_float2(ex2_approx(t.x), ex2_approx(t.y));
             a = fadd2(a, e);
             if (PW) a2 = pow_acc<PW>(a2, e, t, alpha, PW == -1 && DT == 1 && k >= SMCSD_POW_POLY_K);
         }

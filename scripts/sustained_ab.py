@@ -12,6 +12,8 @@ import synth
 pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
 dev = torch.device("cuda")
+if os.environ.get("SMCSD_POLL") is not None:                  # polling tail on / off
+    smc.smcsd_set_poll_tail(os.environ["SMCSD_POLL"] == "1")
 P, N, K, V = 64, 32, 8, 128256
 lp, lq, tok = synth.lm_logits(P, N, K, V, device=dev, seed=4)
 ws, out = smc.Workspace(dev), smc.Outputs()
@@ -44,6 +46,6 @@ b.record()
 torch.cuda.synchronize()
 sus = a.elapsed_time(b) / n * 1e3
 byts = P * 2 * N * K * V * 2
-name = os.path.basename(smc.lib_path)
+name = os.path.basename(smc.lib_path) + (" poll=" + os.environ["SMCSD_POLL"] if os.environ.get("SMCSD_POLL") else "")
 print(f"{name:40s} burst {burst:7.1f} us ({byts / burst / 1e3 / 6451.5:.3f})  sustained {sus:7.1f} us "
       f"({byts / sus / 1e3 / 6451.5:.3f})  sm {statistics.median(clk):.0f} MHz  {statistics.median(pw):.0f} W", flush=True)
