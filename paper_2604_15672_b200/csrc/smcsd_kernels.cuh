@@ -1654,14 +1654,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);
     if (s3_local) {
-        // S3 ran in the chunk CTAs: lam' is in sh.lam, the chunks' status bits in s_flags
-        if (tid == 0) {
+        // S3 ran in the chunk CTAs: lam' is in sh.lam (visible after the cluster barrier), the
+        // chunks' status bits in s_flags.  With N <= 32 warp 2 merges the bits while warps 0-1
+        // run S4-S7 (the barrier after S4-S7 orders sh.st before the status write).
+        if (tid == 64) {
             uint32_t f = 0;
             for (int r = 0; r < per_prompt; ++r) f |= s_flags[r];
             sh.st |= f;
-            prm.prompt_ctr[p] = 0u;
         }
-        __syncthreads();
+        if (N > 32) __syncthreads();
     } else {
     // ---- S3: lam' = fl32(prev + sum_{j<k_n} term_j) in j order
     const double *terms = prm.ell_ws + (int64_t)p * NK;
