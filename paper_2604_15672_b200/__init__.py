@@ -27,7 +27,7 @@ __all__ = [
     "smcsd_ipc_handle_bytes", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close", "smcsd_tp_step",
     "ST_EXCHANGE", "ST_BAD_INDEX", "ST_OUT_OF_PAGES", "smcsd_kv_append_paged", "kv_pool",
     "paged_pool_geometry", "AppendOutputs", "smcsd_kv_append_workspace_bytes",
-    "smcsd_set_latency_tail", "smcsd_set_poll_tail",
+    "smcsd_set_latency_tail", "smcsd_set_poll_tail", "smcsd_set_small_tail",
 ]
 
 SMCSD_F32, SMCSD_BF16 = 0, 1
@@ -112,6 +112,8 @@ def _load():
                  "smcsd_tp_exchange_init", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close",
                  "smcsd_tp_step"):
         getattr(L, name).restype = i32
+    L.smcsd_set_small_tail.argtypes = [i32]
+    L.smcsd_set_small_tail.restype = i32
     L.smcsd_set_poll_tail.argtypes = [i32]
     L.smcsd_set_poll_tail.restype = i32
     L.smcsd_set_latency_tail.argtypes = [i32]
@@ -204,6 +206,12 @@ def _empty(shape, dtype, device):
 
 def smcsd_version() -> str:
     return _lib.smcsd_version().decode()
+
+
+def smcsd_set_small_tail(enable: bool) -> bool:
+    """Process-wide switch for the small (K1-resident) polling tail (include/smcsd.h); returns
+    the previous setting."""
+    return bool(_lib.smcsd_set_small_tail(1 if enable else 0))
 
 
 def smcsd_set_poll_tail(enable: bool) -> bool:

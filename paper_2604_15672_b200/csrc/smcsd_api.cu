@@ -12,6 +12,7 @@
 #include "smcsd_kernels.cuh"
 #include "smcsd_paged.cuh"
 #include "smcsd_lt.cuh"
+#include "smcsd_tail_small.cuh"
 
 using namespace smcsd;
 
@@ -197,9 +198,49 @@ smcsd_rc ensure_tail_attrs() {
     return SMCSD_OK;
 }
 
+// Polling tail, N <= 32, whole particles per 16-pair CTA, <= 16 CTAs per prompt, no bonus rows:
+// k_tail_small (smcsd_tail_small.cuh), resident beside K1 from the start of its stream.
+#ifndef SMCSD_NO_TAIL_SMALL
+int g_tail_small = 1;
+#else
+int g_tail_small = 0;
+#endif
+
+smcsd_rc launch_tail_small(const Params &prm, int resample_mode, int chunks, cudaStream_t st) {
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
+    if (!attr_set[dev]) {
+        // the SM configuration K1's CTAs run under must admit these CTAs beside them
+        if (cudaFuncSetAttribute(k_tail_small, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tail_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+            return SMCSD_ECUDA;
+        attr_set[dev] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(prm.P * chunks));
+    cfg.blockDim = dim3(kTsThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (unsigned)chunks;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, k_tail_small, prm, resample_mode, chunks) == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
+}
+
 smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     if (ensure_tail_attrs() != SMCSD_OK) return SMCSD_ECUDA;
     if (prm.N > kTailMaxN) return launch_pdl(k_tail_large, (unsigned)prm.P, kTailStageBytes, st, prm);
+    if (g_tail_small && prm.lt_words && !prm.bonus_tok && prm.x_from_logits && prm.N <= 32 &&
+        kTsPairs % prm.K == 0 && prm.nseg <= 16) {
+        const int cs = (int)cdiv((int64_t)prm.N * prm.K, kTsPairs);
+        if (cs <= 16 && (int64_t)prm.P * cs < (1ll << 31)) return launch_tail_small(prm, resample_mode, cs, st);
+    }
     const int chunks = (int)cdiv((int64_t)prm.N * prm.K, kPairsPerCta);
     const int bonus_ctas = prm.bonus_tok ? prm.N : 0;
     const int64_t grid = (int64_t)prm.P * chunks + (int64_t)prm.P * bonus_ctas;
@@ -822,6 +863,12 @@ const char *smcsd_strerror(smcsd_rc rc) {
         case SMCSD_ENOSYS: return "not implemented in this build";
     }
     return "unknown smcsd_rc";
+}
+
+int smcsd_set_small_tail(int enable) {
+    const int prev = g_tail_small;
+    g_tail_small = enable != 0;
+    return prev;
 }
 
 int smcsd_set_poll_tail(int enable) {

@@ -10,6 +10,9 @@ import synth
 
 dev = torch.device("cuda")
 name = os.path.basename(smc.lib_path)
+if os.environ.get("SMCSD_SMALL") is not None:                 # small (K1-resident) tail on / off
+    smc.smcsd_set_small_tail(os.environ["SMCSD_SMALL"] == "1")
+    name += " small=" + os.environ["SMCSD_SMALL"]
 if os.environ.get("SMCSD_POLL") is not None:                  # polling tail on / off
     smc.smcsd_set_poll_tail(os.environ["SMCSD_POLL"] == "1")
     name += " poll=" + os.environ["SMCSD_POLL"]

@@ -17,6 +17,8 @@ P, N, K, V = int(os.environ.get("P", 1)), int(os.environ.get("N", 16)), 8, 12825
 dev = torch.device("cuda")
 ring = [synth.lm_logits(P, N, K, V, device=dev, seed=100 + r) for r in range(6)]
 lib = ctypes.CDLL(smc.lib_path)
+if os.environ.get("SMCSD_SMALL") is not None:
+    smc.smcsd_set_small_tail(os.environ["SMCSD_SMALL"] == "1")
 if os.environ.get("SMCSD_LT"):
     smc.smcsd_set_latency_tail(True)
 buf = (ctypes.c_ulonglong * 4096)()
