@@ -1392,7 +1392,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     // other CTAs have long arrived by then, so the wait does not stall)
     if (s3_local) asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
     // N <= 32: this lane's uniform for warp_tail (weight-independent, drawn before the wait)
-    const double u_lane = (N <= 32 && resample_mode && tid < 32) ? tail_uniform(prm, p, tid) : 0.0;
+    const double u_lane = (N <= 64 && resample_mode && tid < 32) ? tail_uniform(prm, p, tid) : 0.0;
+    const double u_lane2 = (N > 32 && N <= 64 && resample_mode && tid < 32) ? tail_uniform(prm, p, tid + 32) : 0.0;
     int lr_model = 0, lr_q = 0;
     int64_t lr_pn = 0;
     float prev3 = 0.0f;                                         // S3 in the chunk: lam_prev, then lam'
@@ -1655,14 +1656,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);
     if (s3_local) {
         // S3 ran in the chunk CTAs: lam' is in sh.lam (visible after the cluster barrier), the
-        // chunks' status bits in s_flags.  With N <= 32 warp 2 merges the bits while warps 0-1
+        // chunks' status bits in s_flags.  With N <= 64 warp 2 merges the bits while warps 0-1
         // run S4-S7 (the barrier after S4-S7 orders sh.st before the status write).
         if (tid == 64) {
             uint32_t f = 0;
             for (int r = 0; r < per_prompt; ++r) f |= s_flags[r];
             sh.st |= f;
         }
-        if (N > 32) __syncthreads();
+        if (N > 64) __syncthreads();
     } else {
     // ---- S3: lam' = fl32(prev + sum_{j<k_n} term_j) in j order
     const double *terms = prm.ell_ws + (int64_t)p * NK;
@@ -1707,8 +1708,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
     __syncthreads();
     }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2051);
-    if (N <= 32) {
-        if (tid < 64) warp_tail(tid >> 5, p, resample_mode, 0, sh.lam[tid & 31], u_lane, sh.reset, wts);
+    if (N <= 64) {
+        if (tid < 64) {
+            if (N <= 32) warp_tail<1>(tid >> 5, p, resample_mode, 0, sh.lam, u_lane, 0.0, sh.reset, wts);
+            else warp_tail<2>(tid >> 5, p, resample_mode, 0, sh.lam, u_lane, u_lane2, sh.reset, wts);
+        }
     } else {
         normalise_resample(prm, p, resample_mode != 0, sh);
     }

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kLtThreads, 8) k_lt(const __grid_constant__ Pa
     const float reset = (float)(-log((double)N));
 #ifdef SMCSD_LT_DRY
     __syncthreads();
-    if (tid < 64) warp_tail(tid >> 5, p, 1, 1, 0.0f, u, reset, ls.w);   // instruction warm-up, no stores
+    if (tid < 64) warp_tail<1>(tid >> 5, p, 1, 1, ls.lam, u, 0.0, reset, ls.w);   // instruction warm-up, no stores
 #endif
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2401);                // inputs (+ warm-up) done
 
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kLtThreads, 8) k_lt(const __grid_constant__ Pa
     if (st) atomicOr(&ls.st, st);
     __syncthreads();
     if (tid == 0 && p == 0) { SMCSD_TRACE_AT(2402); SMCSD_CLK_AT(2494); }   // S2 + S3 done
-    if (tid < 64) warp_tail(tid >> 5, p, resample_mode, 0, ls.lam[lane], u, reset, ls.w);
+    if (tid < 64) warp_tail<1>(tid >> 5, p, resample_mode, 0, ls.lam, u, 0.0, reset, ls.w);
     __syncthreads();
     if (tid == 0) prm.status[p] = ls.st | ls.w.st;
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2403);                // S4-S7 done

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
     uint32_t f = 0;
     if (tid == 64)
         for (int r = 0; r < chunks; ++r) f |= s_flags[r];
-    if (tid < 64) warp_tail(tid >> 5, p, resample_mode, 0, s_lam[lane], u, reset, wts);
+    if (tid < 64) warp_tail<1>(tid >> 5, p, resample_mode, 0, s_lam, u, 0.0, reset, wts);
     __syncthreads();
     if (tid == 64) prm.status[p] = f | wts.st;
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);               // S4-S7 done

@@ -1,10 +1,11 @@
-// smcsd_warp_tail.cuh -- S4-S7 of one prompt with N <= 32 particles as two warp-synchronous
-// routines, lane n = particle n (the small-N tail of k_tail and of the latency tail k_lt).
+// smcsd_warp_tail.cuh -- S4-S7 of one prompt with N <= 64 particles as two warp-synchronous
+// routines, lane l = particles l (and l + 32) (the small-N tail of k_tail, k_tail_small, k_lt).
 //
 // The general S4-S7 (normalise_resample: one lane runs the prefix, a binary search per
 // particle, shared-memory atomics for the offspring, loops per lane) is a long chain of
-// dependent steps; with N <= 32 every per-particle quantity lives in one register of one lane
-// and the tail becomes a short chain with its off-path outputs on a second warp:
+// dependent steps; with N <= 64 every per-particle quantity lives in a register of one lane (two
+// particles per lane above 32) and the tail becomes a short chain with its off-path outputs on a
+// second warp:
 //   role 0 (warp 0): S5-S7 -- M, e, the prefix P_m, C_m = P_m / S, a_n, ties, offspring, the
 //                    in-place slot plan, S7 writes;
 //   role 1 (warp 1): the S4 outputs -- ESS, lse, normalised weights (and the degenerate flag),
@@ -36,10 +37,10 @@ struct WtArgs {
 
 struct WtSmem {
     WtArgs a;
-    alignas(16) double eb[2][32];   // e of each role (16-byte broadcast reads), then C (role 0)
-    alignas(16) int ib[32];         // a_n
-    int ex[32];                // source of the i-th extra copy
-    uint32_t st;               // ST_DEGENERATE (role 1); the caller ORs it into the status
+    alignas(16) double eb[2][64];   // e of each role (16-byte broadcast reads), then C (role 0)
+    alignas(16) int ib[64];         // a_n
+    int ex[64];                     // source of the i-th extra copy
+    uint32_t st;                    // ST_DEGENERATE (role 1); the caller ORs it into the status
 };
 
 __device__ __forceinline__ int wt_key(float f) {              // order-preserving float -> int
@@ -48,58 +49,53 @@ __device__ __forceinline__ int wt_key(float f) {              // order-preservin
 }
 __device__ __forceinline__ float wt_unkey(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
 
-// Every lane: the sequential sums over e_0 .. e_{N-1} (zeros beyond N) read from eb, and
-// P_lane.  Broadcast 16-byte shared loads, 8 particles per step.
-__device__ __forceinline__ void wt_prefix(const double *eb, int N, int lane, double &S, double &sq, double &Pm) {
-    const int N8 = (N + 7) & ~7;
-    double acc = 0.0, q = 0.0, pm = 0.0;
-    for (int m0 = 0; m0 < N8; m0 += 8) {
-        double2 v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = reinterpret_cast<const double2 *>(eb)[(m0 >> 1) + k];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const double em = (k & 1) ? v[k >> 1].y : v[k >> 1].x;
-            acc = __dadd_rn(acc, em);
-            q = __dadd_rn(q, __dmul_rn(em, em));
-            pm = m0 + k == lane ? acc : pm;
-        }
-    }
-    S = acc;
-    sq = q;
-    Pm = pm;
-}
-
-// role 0 / role 1 of S4-S7 for prompt p (see the file comment).  lam: this lane's lam' (any
-// value on lanes >= N); u: this lane's uniform (role 0); reset = fl32(-ln N).  dry != 0 runs the
-// same instructions with every global store off (instruction warm-up).  Both roles must be
-// called (by two different warps); the caller synchronises them before reading ws.st.
-__device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int dry, float lam, double u,
-                                       float reset, WtSmem &ws) {
+// role 0 / role 1 of S4-S7 for prompt p (see the file comment), H particles per lane: lane l
+// holds particles l and l + 32 (H = 2, N <= 64) or l (H = 1, N <= 32).  lam: the prompt's lam'
+// in shared memory (entries >= N are not read); u0 / u1: the uniforms of this lane's particles
+// (role 0); reset = fl32(-ln N).  dry != 0 runs the same instructions with every global store
+// off (instruction warm-up).  Both roles must be called (by two different warps); the caller
+// synchronises them before reading ws.st.
+template <int H>
+__device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int dry, const float *lam_s,
+                                       double u0, double u1, float reset, WtSmem &ws) {
     const unsigned FULL = 0xffffffffu;
     const WtArgs A = ws.a;                                      // registers from here on
     const int N = A.N, lane = threadIdx.x & 31;
-    const bool act = lane < N, out = !dry;
-    const int64_t pn = (int64_t)p * N + lane;
+    const bool out = !dry;
+    bool act[H];
+    float lam[H];
+    int64_t pn[H];
+    const double u[2] = {u0, u1};
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        act[h] = lane + 32 * h < N;
+        lam[h] = act[h] ? (dry ? 0.0f : lam_s[lane + 32 * h]) : -INFINITY;
+        pn[h] = (int64_t)p * N + lane + 32 * h;
+    }
     if (role == 0 && !resample_mode) return;
     if (role == 0) SMCSD_PHASE(0);
     // ---- S4: M = max lam (order-free: one warp reduction on order-preserving keys)
-    const float Mf = wt_unkey(__reduce_max_sync(FULL, wt_key(act ? lam : -INFINITY)));
+    int key = wt_key(lam[0]);
+    if (H == 2) key = max(key, wt_key(lam[H - 1]));
+    const float Mf = wt_unkey(__reduce_max_sync(FULL, key));
     if (Mf == -INFINITY) {                                      // degenerate prompt
-        if (role == 0) {
-            if (act && out) {
-                A.ancestors[pn] = lane;
-                if (A.offspring) A.offspring[pn] = 1;
-                if (A.slot_src) A.slot_src[pn] = lane;
-                A.logw_out[pn] = lam;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            if (!act[h] || !out) continue;
+            if (role == 0) {
+                A.ancestors[pn[h]] = lane + 32 * h;
+                if (A.offspring) A.offspring[pn[h]] = 1;
+                if (A.slot_src) A.slot_src[pn[h]] = lane + 32 * h;
+                A.logw_out[pn[h]] = lam[h];
+            } else if (A.wnorm) {
+                A.wnorm[pn[h]] = 0.0f;
             }
-            if (lane == 0 && out) {
+        }
+        if (lane == 0 && out) {
+            if (role == 0) {
                 A.resampled[p] = 0;
                 if (A.n_ties) A.n_ties[p] = 0;
-            }
-        } else {
-            if (act && out && A.wnorm) A.wnorm[pn] = 0.0f;
-            if (lane == 0 && out) {
+            } else {
                 ws.st |= ST_DEGENERATE;
                 if (A.lse) A.lse[p] = -INFINITY;
                 if (A.ess) A.ess[p] = 0.0;
@@ -108,14 +104,43 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
         return;
     }
     const double M = (double)Mf;
-    // (lanes >= N take exp(0) and their divisions use S / S, so no lane sends the fp64
+    // (inactive particles take exp(0) and their divisions use S / S, so no lane sends the fp64
     // routines down their special-operand slow paths)
-    const double e = exp(act ? __dsub_rn((double)lam, M) : 0.0);
+    double e[H];
     double *eb = ws.eb[role];
-    eb[lane] = act ? e : 0.0;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        e[h] = exp(act[h] ? __dsub_rn((double)lam[h], M) : 0.0);
+        eb[lane + 32 * h] = act[h] ? e[h] : 0.0;
+    }
+    if (H == 1) eb[lane + 32] = 0.0;                            // (N8 may reach past 32: never with H = 1)
     __syncwarp();
-    double S, sq, Pm;
-    wt_prefix(eb, N, lane, S, sq, Pm);
+    // sequential fp64 sums over e_0 .. e_{N-1} in particle order (reading G6), run by every
+    // lane from 16-byte broadcast shared loads; lane l keeps P_l (and P_{l+32})
+    const int N8 = (N + 7) & ~7;
+    double S, sq, Pm[H];
+    {
+        double acc = 0.0, q = 0.0, pm[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) pm[h] = 0.0;
+        for (int m0 = 0; m0 < N8; m0 += 8) {
+            double2 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k] = reinterpret_cast<const double2 *>(eb)[(m0 >> 1) + k];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double em = (k & 1) ? v[k >> 1].y : v[k >> 1].x;
+                acc = __dadd_rn(acc, em);
+                q = __dadd_rn(q, __dmul_rn(em, em));
+#pragma unroll
+                for (int h = 0; h < H; ++h) pm[h] = m0 + k == lane + 32 * h ? acc : pm[h];
+            }
+        }
+        S = acc;
+        sq = q;
+#pragma unroll
+        for (int h = 0; h < H; ++h) Pm[h] = pm[h];
+    }
     if (role == 1) {
         // ---- S4 outputs, off the ancestors' path
         if (A.ess || dry) {
@@ -123,8 +148,11 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
             if (lane == 0 && out && A.ess) A.ess[p] = ess;
         }
         if (A.wnorm || dry) {
-            const float wn = (float)__ddiv_rn(e, act ? S : e);
-            if (act && out) A.wnorm[pn] = wn;
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const float wn = (float)__ddiv_rn(e[h], act[h] ? S : e[h]);
+                if (act[h] && out) A.wnorm[pn[h]] = wn;
+            }
         }
         if (A.lse || dry) {
             const double l = __dadd_rn(M, log(S));
@@ -138,11 +166,14 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
     // always resamples and the division is skipped)
     const bool do_res = dry || A.eta == (double)INFINITY || __ddiv_rn(__dmul_rn(S, S), sq) < A.eta;
     if (!do_res) {
-        if (act && out) {
-            A.ancestors[pn] = lane;
-            if (A.offspring) A.offspring[pn] = 1;
-            if (A.slot_src) A.slot_src[pn] = lane;
-            A.logw_out[pn] = lam;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            if (act[h] && out) {
+                A.ancestors[pn[h]] = lane + 32 * h;
+                if (A.offspring) A.offspring[pn[h]] = 1;
+                if (A.slot_src) A.slot_src[pn[h]] = lane + 32 * h;
+                A.logw_out[pn[h]] = lam[h];
+            }
         }
         if (lane == 0 && out) {
             A.resampled[p] = 0;
@@ -152,71 +183,137 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
         return;
     }
     // ---- S6: C_m = P_m / S; a_n = #{m : C_m <= u_n}; ties |u_n - C_m| <= 2^-40
-    const double Cq = __ddiv_rn(act ? Pm : S, S);
+    double Cq[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) Cq[h] = __ddiv_rn(act[h] ? Pm[h] : S, S);
     __syncwarp();                                               // every lane is done with e
-    eb[lane] = act ? Cq : (double)INFINITY;                    // +inf never counts
+#pragma unroll
+    for (int h = 0; h < H; ++h) eb[lane + 32 * h] = act[h] ? Cq[h] : (double)INFINITY;   // +inf never counts
+    if (H == 1) eb[lane + 32] = (double)INFINITY;
     __syncwarp();
     if (role == 0) SMCSD_PHASE(2);
     const double tie = 9.094947017729282379150390625e-13;      // 2^-40
-    const int N8 = (N + 7) & ~7;
-    int a = 0, ties = 0;
-    for (int m0 = 0; m0 < N8; m0 += 8) {
-        double2 v[4];
+    int a[H], o[H], ties = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = reinterpret_cast<const double2 *>(eb)[(m0 >> 1) + k];
+    for (int h = 0; h < H; ++h) a[h] = 0;
+    if (H == 1) {
+        // N <= 32: every lane compares its u with all C (broadcast 16-byte reads)
+        for (int m0 = 0; m0 < N8; m0 += 8) {
+            double2 v[4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const double Cm = (k & 1) ? v[k >> 1].y : v[k >> 1].x;
-            a += Cm <= u;
-            ties += fabs(__dsub_rn(u, Cm)) <= tie;
+            for (int k = 0; k < 4; ++k) v[k] = reinterpret_cast<const double2 *>(eb)[(m0 >> 1) + k];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const double Cm = (k & 1) ? v[k >> 1].y : v[k >> 1].x;
+                a[0] += Cm <= u[0];
+                ties += act[0] && fabs(__dsub_rn(u[0], Cm)) <= tie;
+            }
+        }
+    } else {
+        // 32 < N <= 64: binary search of C, then the tie run around the boundary (an O(log N)
+        // chain instead of 2 x N broadcast compares per lane)
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            int lo = 0, hi = N;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (eb[mid] <= u[h]) lo = mid + 1; else hi = mid;
+            }
+            a[h] = lo;
+            if (act[h]) {
+                for (int m = lo - 1; m >= 0 && fabs(__dsub_rn(u[h], eb[m])) <= tie; --m) ++ties;
+                for (int m = lo; m < N && fabs(__dsub_rn(u[h], eb[m])) <= tie; ++m) ++ties;
+            }
         }
     }
-    a = act ? min(a, N - 1) : -1;                               // a < N always (C_{N-1} = 1 > u)
-    ties = act ? ties : 0;
-    ws.ib[lane] = a;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        a[h] = act[h] ? min(a[h], N - 1) : -1;                  // a < N always (C_{N-1} = 1 > u)
+        if (H == 1) ws.ib[lane + 32 * h] = a[h];
+        else ws.ib[lane + 32 * h] = 0;
+        o[h] = 0;
+    }
+    if (H == 1) ws.ib[lane + 32] = -1;
     __syncwarp();
     if (role == 0) SMCSD_PHASE(3);
-    // offspring o_m = #{n : a_n = m} (a = -1 beyond N never matches)
-    int o = 0;
-    for (int n0 = 0; n0 < N8; n0 += 8) {
-        const int4 v0 = reinterpret_cast<const int4 *>(ws.ib)[n0 >> 2];
-        const int4 v1 = reinterpret_cast<const int4 *>(ws.ib)[(n0 >> 2) + 1];
-        o += (v0.x == lane) + (v0.y == lane) + (v0.z == lane) + (v0.w == lane) +
-             (v1.x == lane) + (v1.y == lane) + (v1.z == lane) + (v1.w == lane);
+    // offspring o_m = #{n : a_n = m}
+    if (H == 1) {
+        // broadcast reads of a (a = -1 beyond N never matches)
+        for (int n0 = 0; n0 < N8; n0 += 8) {
+            const int4 v0 = reinterpret_cast<const int4 *>(ws.ib)[n0 >> 2];
+            const int4 v1 = reinterpret_cast<const int4 *>(ws.ib)[(n0 >> 2) + 1];
+            o[0] += (v0.x == lane) + (v0.y == lane) + (v0.z == lane) + (v0.w == lane) +
+                    (v1.x == lane) + (v1.y == lane) + (v1.z == lane) + (v1.w == lane);
+        }
+    } else {
+        // shared-memory counts
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+            if (act[h]) atomicAdd(&ws.ib[a[h]], 1);
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < H; ++h) o[h] = ws.ib[lane + 32 * h];
     }
-    o = act ? o : 0;
-    // ---- in-place slot plan (G14)
+    // ---- in-place slot plan (G14): ranks over the particle order l, then l + 32
     const unsigned lt_mask = (1u << lane) - 1u;
-    const bool dead = act && o == 0;
-    const int d_rank = __popc(__ballot_sync(FULL, dead) & lt_mask);
+    bool dead[H];
+    int d_rank[H];
+    {
+        int base = 0;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            o[h] = act[h] ? o[h] : 0;
+            dead[h] = act[h] && o[h] == 0;
+            const unsigned b = __ballot_sync(FULL, dead[h]);
+            d_rank[h] = base + __popc(b & lt_mask);
+            base += __popc(b);
+        }
+    }
     if (A.scheme == 0) {
         // systematic: a is nondecreasing in n, so the copies of m are consecutive particles and
         // every particle after the first of its run is an extra copy -- the extras in particle
         // order are the extras in ascending source order
-        const int ap = __shfl_up_sync(FULL, a, 1);
-        const bool isx = act && lane > 0 && a == ap;
-        const int xr = __popc(__ballot_sync(FULL, isx) & lt_mask);
-        if (isx) ws.ex[xr] = a;
+        int base = 0;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            int ap = __shfl_up_sync(FULL, a[h], 1);
+            if (h == 1) {
+                const int last0 = __shfl_sync(FULL, a[0], 31);
+                if (lane == 0) ap = last0;
+            }
+            const bool isx = act[h] && (lane > 0 || h > 0) && a[h] == ap;
+            const unsigned b = __ballot_sync(FULL, isx);
+            if (isx) ws.ex[base + __popc(b & lt_mask)] = a[h];
+            base += __popc(b);
+        }
     } else {
         // multinomial: scan of the extra counts, source m written o_m - 1 times
-        const int extra = o > 1 ? o - 1 : 0;
-        int xx = extra;
+        int base = 0;
 #pragma unroll
-        for (int s = 1; s < 32; s <<= 1) {
-            const int xv = __shfl_up_sync(FULL, xx, s);
-            if (lane >= s) xx += xv;
+        for (int h = 0; h < H; ++h) {
+            const int extra = o[h] > 1 ? o[h] - 1 : 0;
+            int xx = extra;
+#pragma unroll
+            for (int s = 1; s < 32; s <<= 1) {
+                const int xv = __shfl_up_sync(FULL, xx, s);
+                if (lane >= s) xx += xv;
+            }
+            for (int c = 0, x_pos = base + xx - extra; c < extra; ++c) ws.ex[x_pos + c] = lane + 32 * h;
+            base += __shfl_sync(FULL, xx, 31);
         }
-        for (int c = 0, x_pos = xx - extra; c < extra; ++c) ws.ex[x_pos + c] = lane;
     }
     __syncwarp();
-    const int slot = dead ? ws.ex[d_rank] : lane;
     ties = __reduce_add_sync(FULL, ties);
     if (role == 0) SMCSD_PHASE(4);
-    if (act && out) {                                           // S7
-        A.ancestors[pn] = a;
-        if (A.offspring) A.offspring[pn] = o;
-        if (A.slot_src) A.slot_src[pn] = slot;
-        A.logw_out[pn] = reset;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        const int slot = dead[h] ? ws.ex[d_rank[h]] : lane + 32 * h;
+        if (act[h] && out) {                                    // S7
+            A.ancestors[pn[h]] = a[h];
+            if (A.offspring) A.offspring[pn[h]] = o[h];
+            if (A.slot_src) A.slot_src[pn[h]] = slot;
+            A.logw_out[pn[h]] = reset;
+        }
     }
     if (lane == 0 && out) {
         A.resampled[p] = 1;

@@ -8,6 +8,7 @@ using namespace smcsd;
 __global__ void k(int N, float *logw, double *lse, double *ess, float *wnorm, int32_t *anc, int32_t *off,
                   int32_t *slot, int32_t *ties, uint8_t *res, long long *out) {
     __shared__ WtSmem ls;
+    __shared__ float lam_s[64];
     const int lane = threadIdx.x & 31;
     if (lane == 0) {
         ls.st = 0;
@@ -18,7 +19,9 @@ __global__ void k(int N, float *logw, double *lse, double *ess, float *wnorm, in
     const float lam = lane < N ? -0.1f * lane + 0.05f * (lane % 3) : -INFINITY;
     for (int r = 0; r < 4; ++r) {
         const long long t0 = clock64();
-        warp_tail(threadIdx.x >> 5, 0, 1, 0, lam, u, -2.77f, ls);
+        lam_s[lane] = lam;
+        __syncthreads();
+        warp_tail<1>(threadIdx.x >> 5, 0, 1, 0, lam_s, u, 0.0, -2.77f, ls);
         __syncthreads();
         const long long t1 = clock64();
         if (threadIdx.x == 0) {

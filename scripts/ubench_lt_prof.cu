@@ -6,17 +6,20 @@ using namespace smcsd;
 
 __global__ void k(int N, int reps, float *logw, double *lse, double *ess, float *wnorm, int32_t *anc,
                   int32_t *off, int32_t *slot, int32_t *ties, uint8_t *res) {
-    __shared__ LtSmem ls;
+    __shared__ WtSmem ls;
+    __shared__ float lam_s[64];
     const int lane = threadIdx.x;
     if (lane == 0) {
         ls.st = 0;
-        ls.a = LtArgs{logw, wnorm, lse, ess, anc, off, slot, ties, res, (double)INFINITY, N};
+        ls.a = WtArgs{logw, wnorm, lse, ess, anc, off, slot, ties, res, (double)INFINITY, N, 0};
     }
     __syncwarp();
     const double u = (lane + 0.37) / N;
     float lam = lane < N ? -0.1f * lane + 0.05f * (lane % 3) : -INFINITY;
     for (int r = 0; r < reps; ++r) {
-        lt_finish(0, 1, r != reps - 1, lam, u, -2.77f, ls);
+        lam_s[lane] = lam;
+        __syncwarp();
+        warp_tail<1>(0, 0, 1, r != reps - 1, lam_s, u, 0.0, -2.77f, ls);
         lam += 1e-7f;
     }
 }

@@ -316,22 +316,27 @@ def test_systematic_unbiased_sweep(smc):
     assert np.max(np.abs(mean - N * wbar)) <= 2.0 / M + 1e-6
 
 
-def test_step_staged_parity(smc, orc):
-    # fused S1-S7: logw_pre feeds the oracle's S4-S7 -> bit-exact ancestry (staged protocol)
-    P, N, K, V = 4, 32, 8, 40000
-    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=21)
+@pytest.mark.parametrize("N,scheme,eta", [(32, 0, math.inf), (33, 0, math.inf), (48, 1, math.inf),
+                                           (64, 0, math.inf), (64, 1, None), (65, 0, math.inf)])
+def test_step_staged_parity(smc, orc, N, scheme, eta):
+    # fused S1-S7: logw_pre feeds the oracle's S4-S7 -> bit-exact ancestry (staged protocol);
+    # N <= 32 / <= 64 / > 64 are the three S4-S7 routines (warp_tail<1>, warp_tail<2>, one lane)
+    P, K, V = 4, 8, 40000
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=21 + N)
     dev = torch.device("cuda")
     prev = synth.uniform_prior(P, N)
+    prev[1, ::3] = -math.inf                                  # zero-weight particles
+    eta_v = N / 2 if eta is None else eta
     out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, logw_prev=prev.to(dev),
-                         eta=math.inf, seed=123, step=9, prompt_base=40)
+                         eta=eta, scheme=scheme, seed=123, step=9, prompt_base=40)
     torch.cuda.synchronize()
     ref_w = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, logw_prev=prev.numpy())
     assert max_abs(np_(out.logw_pre), ref_w["logw"]) <= TOL_LOGW
-    staged = orc.resample(np_(out.logw_pre), eta=math.inf, seed=123, step=9, prompt_base=40)
+    staged = orc.resample(np_(out.logw_pre), eta=eta_v, scheme=scheme, seed=123, step=9, prompt_base=40)
     _assert_resample_equal(out, staged)
     # determinism: a second run is bitwise identical
     out2 = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, logw_prev=prev.to(dev),
-                          eta=math.inf, seed=123, step=9, prompt_base=40)
+                          eta=eta, scheme=scheme, seed=123, step=9, prompt_base=40)
     for f in ("logw", "logw_pre", "ancestors", "slot_src", "ess", "lse", "logp_tok"):
         assert torch.equal(getattr(out, f), getattr(out2, f)), f
 

@@ -1,7 +1,11 @@
-"""GPU: the latency tail (smcsd_lt.cuh, smcsd_set_latency_tail) -- S2-S7 in a kernel that runs
-beside K1 and polls K1's {m, s} words -- against the two-kernel path (bit-identical outputs) and
-against the CPU oracle (staged protocol: the oracle's S4-S7 from the GPU's logw_pre gives the same
-ancestry).  Also the word array is left zero (the next call depends on it)."""
+"""GPU: the tail variants of smcsd_step / smcsd_weights against each other (bit-identical outputs)
+and against the CPU oracle (staged protocol: the oracle's S4-S7 from the GPU's logw_pre gives the
+same ancestry):
+  * the small polling cluster tail k_tail_small (smcsd_tail_small.cuh, default for small steps),
+  * the 256-thread polling tail (smcsd_set_small_tail(0)),
+  * the wait-for-K1 tail (smcsd_set_poll_tail(0)),
+  * the experimental latency tail k_lt (smcsd_lt.cuh, smcsd_set_latency_tail(1)).
+Each runs twice on one workspace: the polling tails leave K1's word array zero for the next call."""
 import math
 
 import numpy as np
@@ -21,17 +25,22 @@ FIELDS = ("logw", "logw_pre", "logp_tok", "logq_tok", "lse", "ess", "wnorm", "st
 def smc():
     import paper_2604_15672_b200 as m
     assert torch.cuda.is_available()
-    prev = m.smcsd_set_latency_tail(False)
     yield m
-    m.smcsd_set_latency_tail(prev)
+    _set(m, "small")
 
 
 def _bits(t):
     return t.view(torch.uint8) if t.is_floating_point() else t
 
 
+def _set(smc, variant):
+    smc.smcsd_set_latency_tail(variant == "lt")
+    smc.smcsd_set_poll_tail(variant != "wait")
+    smc.smcsd_set_small_tail(variant not in ("wait", "poll256"))
+
+
 def _run(smc, lt, mode, lp, lq, tok, ws, **kw):
-    smc.smcsd_set_latency_tail(lt)
+    _set(smc, lt if isinstance(lt, str) else ("lt" if lt else "wait"))
     try:
         if mode == "step":
             o = smc.smcsd_step(lp, lq, tok, workspace=ws, **kw)
@@ -40,7 +49,7 @@ def _run(smc, lt, mode, lp, lq, tok, ws, **kw):
             o = smc.smcsd_weights(lp, lq, tok, workspace=ws, **kw)
         torch.cuda.synchronize()
     finally:
-        smc.smcsd_set_latency_tail(False)
+        _set(smc, "small")
     return {f: getattr(o, f).clone() for f in FIELDS if getattr(o, f, None) is not None}
 
 
@@ -53,6 +62,8 @@ def _run(smc, lt, mode, lp, lq, tok, ws, **kw):
     (4, 32, 16, 128256, torch.bfloat16, {"eta": None}),                      # eta = N/2, 1024 rows
     (2, 12, 8, 131072, torch.bfloat16, {}),                                  # 16 full segments
     (5, 8, 16, 32000, torch.bfloat16, {"alpha": 0.7, "inv_temp_p": 1.3}),
+    (2, 32, 2, 60000, torch.bfloat16, {}),                                   # 4 small CTAs, K = 2
+    (1, 3, 5, 9000, torch.float32, {}),                                      # K = 5: no small tail
 ])
 @pytest.mark.parametrize("mode", ["step", "weights"])
 def test_latency_tail_bit_identical(smc, P, N, K, V, dtype, extra, mode):
@@ -66,27 +77,29 @@ def test_latency_tail_bit_identical(smc, P, N, K, V, dtype, extra, mode):
         kw = dict(V=V, n_drafted=ndv, logw_prev=prev, step=3, eta=extra.get("eta", math.inf))
         kw.update({k: v for k, v in extra.items() if k != "eta"})
         ws = smc.Workspace(dev)
-        ref = _run(smc, False, mode, lp, lq, tok, ws, **kw)
-        for rep in range(2):                     # twice on one workspace: the words were re-zeroed
-            got = _run(smc, True, mode, lp, lq, tok, ws, **kw)
-            for f in ref:
-                assert torch.equal(_bits(ref[f]), _bits(got[f])), (f, rep, ndv is not None)
+        ref = _run(smc, "wait", mode, lp, lq, tok, ws, **kw)
+        for variant in ("small", "poll256", "lt"):
+            for rep in range(2):                 # twice on one workspace: the words were re-zeroed
+                got = _run(smc, variant, mode, lp, lq, tok, ws, **kw)
+                for f in ref:
+                    assert torch.equal(_bits(ref[f]), _bits(got[f])), (variant, f, rep, ndv is not None)
 
 
-def test_latency_tail_staged_oracle_parity(smc, orc):
+@pytest.mark.parametrize("variant", ["small", "poll256", "lt"])
+def test_tail_variant_staged_oracle_parity(smc, orc, variant):
     # the GPU's lam' (logw_pre) within 1e-4 of the oracle's, and the oracle's S4-S7 from it gives
     # the GPU's ancestry bit-exactly (reading G7: no ties here)
     P, N, K, V = 2, 16, 8, 128256
     lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.bfloat16, seed=31, bonus=False)
     dev = torch.device("cuda")
     prev = synth.uniform_prior(P, N)
-    smc.smcsd_set_latency_tail(True)
+    _set(smc, variant)
     try:
         out = smc.smcsd_step(lp.to(dev), lq.to(dev), tok.to(dev), V=V, logw_prev=prev.to(dev),
                              eta=math.inf, seed=7, step=4, prompt_base=11)
         torch.cuda.synchronize()
     finally:
-        smc.smcsd_set_latency_tail(False)
+        _set(smc, "small")
     ref_w = orc.weights(to_host(lp), to_host(lq), tok.numpy(), V=V, logw_prev=prev.numpy())
     assert max_abs(np_(out.logw_pre), ref_w["logw"]) <= 1e-4
     staged = orc.resample(np_(out.logw_pre), eta=math.inf, seed=7, step=4, prompt_base=11)
