@@ -198,7 +198,7 @@ smcsd_rc ensure_tail_attrs() {
     return SMCSD_OK;
 }
 
-// Polling tail, N <= 32, whole particles per 16-pair CTA, <= 16 CTAs per prompt, no bonus rows:
+// Polling tail, N <= 32, N K <= 256 pairs (<= 16 CTAs of 16 pairs per prompt), no bonus rows:
 // k_tail_small (smcsd_tail_small.cuh), resident beside K1 from the start of its stream.
 #ifndef SMCSD_NO_TAIL_SMALL
 int g_tail_small = 1;
@@ -236,10 +236,9 @@ smcsd_rc launch_tail_small(const Params &prm, int resample_mode, int chunks, cud
 smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     if (ensure_tail_attrs() != SMCSD_OK) return SMCSD_ECUDA;
     if (prm.N > kTailMaxN) return launch_pdl(k_tail_large, (unsigned)prm.P, kTailStageBytes, st, prm);
-    if (g_tail_small && prm.lt_words && !prm.bonus_tok && prm.x_from_logits && prm.N <= 32 &&
-        kTsPairs % prm.K == 0 && prm.nseg <= 16) {
+    if (g_tail_small && prm.lt_words && !prm.bonus_tok && prm.x_from_logits && prm.N <= 32 && prm.nseg <= 16) {
         const int cs = (int)cdiv((int64_t)prm.N * prm.K, kTsPairs);
-        if (cs <= 16 && (int64_t)prm.P * cs < (1ll << 31)) return launch_tail_small(prm, resample_mode, cs, st);
+        if (cs <= kTsMaxChunks && (int64_t)prm.P * cs < (1ll << 31)) return launch_tail_small(prm, resample_mode, cs, st);
     }
     const int chunks = (int)cdiv((int64_t)prm.N * prm.K, kPairsPerCta);
     const int bonus_ctas = prm.bonus_tok ? prm.N : 0;

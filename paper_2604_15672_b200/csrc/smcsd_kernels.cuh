@@ -147,6 +147,11 @@ __device__ __forceinline__ void st_cluster_f32(float *local, unsigned rank, floa
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(r), "f"(v) : "memory");
 }
+__device__ __forceinline__ void st_cluster_f64(double *local, unsigned rank, double v) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(local), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(r), "d"(v) : "memory");
+}
 __device__ __forceinline__ void st_cluster_u32(uint32_t *local, unsigned rank, uint32_t v) {
     uint32_t a = (uint32_t)__cvta_generic_to_shared(local), r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));

@@ -5,8 +5,9 @@
 // next to K1's six 288-thread CTAs per SM, so they start only as K1's CTAs exit and run their
 // one-shot code cold after K1's last item.  k_tail_small is the same computation in CTAs that
 // fit in what K1 leaves free on an SM (128 threads at <= 64 registers: one warp per SM
-// sub-partition; ~2 KB of shared memory): 16 (particle, position) pairs per CTA, a prompt's
-// CTAs one thread-block cluster (<= 16).  K1 launches it at once (polling tail), so its CTAs
+// sub-partition; ~4.6 KB of shared memory): 16 (particle, position) pairs per CTA, a prompt's
+// CTAs one thread-block cluster (<= 16).  S3 runs in the chunk CTAs when K divides 16, else in
+// the finisher from the terms the chunks push to it.  K1 launches it at once (polling tail), so its CTAs
 // are resident from the start of K1's stream: they read their inputs and poll K1's {m, s}
 // words while K1 runs, and the finishing CTA runs S4-S7 (warp_tail) once every chunk has
 // pushed its lam' over DSMEM.
@@ -22,13 +23,16 @@ namespace smcsd {
 
 constexpr int kTsThreads = 128;
 constexpr int kTsPairs = 16;                  // (particle, position) pairs per CTA: 32 rows x 4 lanes
+constexpr int kTsMaxChunks = 16;              // CTAs per prompt (one cluster, non-portable size)
+constexpr int kTsMaxPairs = kTsPairs * kTsMaxChunks;
 
-// grid = P x chunks (cluster = chunks <= 16, K divides kTsPairs), block = kTsThreads.
+// grid = P x chunks (cluster = chunks <= 16, N <= 32), block = kTsThreads.
 __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_constant__ Params prm, int resample_mode,
                                                            int chunks) {
     __shared__ float4 rs[2 * kTsPairs];
     __shared__ double term_s[kTsPairs];
     __shared__ float s_lam[32];                                 // finisher: every particle's lam'
+    __shared__ double s_term[kTsMaxPairs];                      // finisher (S3 there): every pair's term
     __shared__ uint32_t s_flags[16];                            // finisher: every chunk's status bits
     __shared__ __align__(16) WtSmem wts;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -64,6 +68,16 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
             xq = load_x(prm, 1, pn, j, d);
         }
         if (j == 0) prev = prm.logw_prev ? prm.logw_prev[pn] : (float)(-log((double)N));
+    }
+    // S3 runs in the chunk when whole particles fit in it (K divides 16); otherwise the chunks
+    // push their terms to the finisher, whose warp 0 (lane n = particle n) sums them
+    const bool s3_fin = (kTsPairs % K) != 0;                    // uniform
+    int kn_f = 0;
+    float prev_f = 0.0f;
+    if (s3_fin && crank == fin && tid < N) {
+        const int64_t pf = (int64_t)p * N + tid;
+        kn_f = drafted_len(prm, pf);
+        prev_f = prm.logw_prev ? prm.logw_prev[pf] : (float)(-log((double)N));
     }
     double u = 0.0;
     float reset = 0.0f;
@@ -140,10 +154,11 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
                     term = __dsub_rn(__dmul_rn(prm.alpha, ellp), ellq);
                 }
             }
-            term_s[tid] = term;
+            if (s3_fin) st_cluster_f64(&s_term[q0 + tid], fin, term);
+            else term_s[tid] = term;
         }
         __syncwarp();
-        if (tid < nq && j == 0) {
+        if (!s3_fin && tid < nq && j == 0) {
             // S3: lam' = fl32(prev + sum_{j < k_n} term_j) in j order
             int kk = kn;
             bool bad = false;
@@ -171,7 +186,7 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
     if (tid < nq) {
         if (prm.logp_tok) prm.logp_tok[pn * K + j] = (float)ellp;
         if (prm.logq_tok) prm.logq_tok[pn * K + j] = (float)ellq;
-        if (j == 0) {
+        if (j == 0 && !s3_fin) {
             if (prm.logw_pre) prm.logw_pre[pn] = lam;
             if (!resample_mode) prm.logw_out[pn] = lam;
         }
@@ -186,6 +201,36 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
     uint32_t f = 0;
     if (tid == 64)
         for (int r = 0; r < chunks; ++r) f |= s_flags[r];
+    if (s3_fin) {
+        // S3 here: lam'_n = fl32(prev_n + sum_{j < k_n} term_{nK + j}) in j order
+        if (tid < 32) {
+            uint32_t st3 = 0;
+            if (tid < N) {
+                int kk = kn_f;
+                bool bad = false;
+                if (kk < 0 || kk > K) {
+                    st3 |= ST_BAD_TOKEN;
+                    bad = true;
+                    kk = 0;
+                }
+                double delta = 0.0;
+                for (int jj = 0; jj < kk; ++jj) delta = __dadd_rn(delta, s_term[tid * K + jj]);
+                if (isnan(delta)) bad = true;
+                if (isnan(prev_f) || prev_f == INFINITY) {
+                    st3 |= ST_NONFINITE;
+                    bad = true;
+                }
+                const float lm = bad ? -INFINITY : (float)__dadd_rn((double)prev_f, delta);
+                s_lam[tid] = lm;
+                const int64_t pf = (int64_t)p * N + tid;
+                if (prm.logw_pre) prm.logw_pre[pf] = lm;
+                if (!resample_mode) prm.logw_out[pf] = lm;
+            }
+            st3 = __reduce_or_sync(0xffffffffu, st3);
+            if (tid == 0 && st3) wts.st |= st3;                 // (role 1 sets only ST_DEGENERATE, later)
+        }
+        if (tid < 64) asm volatile("bar.sync 1, 64;" ::: "memory");     // s_lam for warp 1
+    }
     if (tid < 64) warp_tail<1>(tid >> 5, p, resample_mode, 0, s_lam, u, 0.0, reset, wts);
     __syncthreads();
     if (tid == 64) prm.status[p] = f | wts.st;

@@ -63,7 +63,9 @@ def _run(smc, lt, mode, lp, lq, tok, ws, **kw):
     (2, 12, 8, 131072, torch.bfloat16, {}),                                  # 16 full segments
     (5, 8, 16, 32000, torch.bfloat16, {"alpha": 0.7, "inv_temp_p": 1.3}),
     (2, 32, 2, 60000, torch.bfloat16, {}),                                   # 4 small CTAs, K = 2
-    (1, 3, 5, 9000, torch.float32, {}),                                      # K = 5: no small tail
+    (1, 3, 5, 9000, torch.float32, {}),                                      # K = 5: S3 in the finisher
+    (2, 6, 12, 30000, torch.bfloat16, {}),                                   # K = 12: S3 in the finisher
+    (1, 8, 32, 50000, torch.bfloat16, {"scheme": 1}),                        # K = 32: 16 small CTAs
 ])
 @pytest.mark.parametrize("mode", ["step", "weights"])
 def test_latency_tail_bit_identical(smc, P, N, K, V, dtype, extra, mode):
