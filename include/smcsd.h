@@ -387,17 +387,6 @@ SMCSD_API int smcsd_set_poll_tail(int enable);
  * 256-thread tail for them.  Returns the previous setting. */
 SMCSD_API int smcsd_set_small_tail(int enable);
 
-/* Latency tail switch (process-wide; default 0 = off, experimental).  With it on, smcsd_step and smcsd_weights
- * run S2-S7 of small calls (N <= 32, 2*N*K <= 1024, ceil(V / 8192) <= 32, P <= 148, no bonus
- * token) in a kernel that runs beside K1 and polls K1's per-segment {m, s} words instead of
- * waiting for K1's grid to complete (paper_2604_15672_b200/csrc/smcsd_lt.cuh); the results are
- * bit-identical to the two-kernel path, which every other call takes.  0 forces the two-kernel
- * path (A/B timing, tests).  The LT words live in the workspace and are zero between calls (the
- * latency tail clears them); after a call that returned an error, re-initialise the workspace
- * (smcsd_workspace_init).  Not synchronised with calls in flight on other host threads: set it
- * before issuing work.  Returns the previous setting. */
-SMCSD_API int smcsd_set_latency_tail(int enable);
-
 /* Human-readable name of a return code (static storage). */
 SMCSD_API const char *smcsd_strerror(smcsd_rc rc);
 

@@ -27,7 +27,7 @@ __all__ = [
     "smcsd_ipc_handle_bytes", "smcsd_ipc_export", "smcsd_ipc_open", "smcsd_ipc_close", "smcsd_tp_step",
     "ST_EXCHANGE", "ST_BAD_INDEX", "ST_OUT_OF_PAGES", "smcsd_kv_append_paged", "kv_pool",
     "paged_pool_geometry", "AppendOutputs", "smcsd_kv_append_workspace_bytes",
-    "smcsd_set_latency_tail", "smcsd_set_poll_tail", "smcsd_set_small_tail",
+    "smcsd_set_poll_tail", "smcsd_set_small_tail",
 ]
 
 SMCSD_F32, SMCSD_BF16 = 0, 1
@@ -116,8 +116,6 @@ def _load():
     L.smcsd_set_small_tail.restype = i32
     L.smcsd_set_poll_tail.argtypes = [i32]
     L.smcsd_set_poll_tail.restype = i32
-    L.smcsd_set_latency_tail.argtypes = [i32]
-    L.smcsd_set_latency_tail.restype = i32
     L.smcsd_version.restype = ctypes.c_char_p
     L.smcsd_strerror.restype = ctypes.c_char_p
     L.smcsd_strerror.argtypes = [i32]
@@ -217,12 +215,6 @@ def smcsd_set_small_tail(enable: bool) -> bool:
 def smcsd_set_poll_tail(enable: bool) -> bool:
     """Process-wide switch for the polling tail (include/smcsd.h); returns the previous setting."""
     return bool(_lib.smcsd_set_poll_tail(1 if enable else 0))
-
-
-def smcsd_set_latency_tail(enable: bool) -> bool:
-    """Process-wide switch for the latency tail of small steps (include/smcsd.h); returns the
-    previous setting."""
-    return bool(_lib.smcsd_set_latency_tail(1 if enable else 0))
 
 
 def smcsd_workspace_bytes(P: int, N: int, K: int, v_len: int) -> int:

@@ -11,7 +11,6 @@
 #include "smcsd.h"
 #include "smcsd_kernels.cuh"
 #include "smcsd_paged.cuh"
-#include "smcsd_lt.cuh"
 #include "smcsd_tail_small.cuh"
 
 using namespace smcsd;
@@ -256,51 +255,30 @@ smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     return launch_pdl(k_tail, (unsigned)grid, 0, st, prm, resample_mode, chunks, bonus_ctas, 0);
 }
 
-// The latency tail (smcsd_lt.cuh) replaces K2 for small steps: N <= 32 (lane per particle),
-// 2NK <= 1024 rows and <= 32 segments per row per prompt, one CTA per prompt beside K1, no bonus
-// rows, no exchange.
-int g_latency_tail = 0;                          // smcsd_set_latency_tail (experimental, off)
 #ifndef SMCSD_NO_POLL_TAIL
 int g_poll_tail = 1;                             // smcsd_set_poll_tail
 #else
 int g_poll_tail = 0;
 #endif
 
-// Tail modes of smcsd_step / smcsd_weights.  K1 publishes {m, s} words (prm.lt_words) and
-// launches its dependents at once in both polling modes:
-//   TAIL_LT    -- k_lt (smcsd_lt.cuh), experimental, smcsd_set_latency_tail;
-//   TAIL_POLL  -- k_tail polls the words instead of waiting for K1's grid (no bonus rows, at
-//                 most 16 segments per row: one word per lane per part group);
+// Tail modes of smcsd_step / smcsd_weights:
+//   TAIL_POLL  -- K1 publishes {m, s} words (prm.lt_words) and launches its dependents at once;
+//                 the tail (k_tail_small when it applies, else k_tail) polls the words instead
+//                 of waiting for K1's grid (no bonus rows, at most 16 segments per row);
 //   TAIL_WAIT  -- k_tail behind griddepcontrol.wait on K1's float4 partials (every other call).
-enum TailMode { TAIL_WAIT = 0, TAIL_POLL = 1, TAIL_LT = 2 };
+enum TailMode { TAIL_WAIT = 0, TAIL_POLL = 1 };
 
 TailMode tail_mode(Params &prm, void *ws, const WsLayout &L) {
     prm.lt_words = nullptr;
     const bool common = !prm.bonus_tok && !prm.xpeer && prm.x_from_logits && prm.n_models == 2;
     TailMode m = TAIL_WAIT;
-    if (common && g_latency_tail && prm.N <= kLtMaxN && 2 * prm.N * prm.K <= kLtMaxRows &&
-        prm.nseg <= kLtMaxParts && prm.P <= kLtMaxP)
-        m = TAIL_LT;
-    else if (common && g_poll_tail && prm.nseg <= 16 && prm.N <= kTailMaxN &&
+    if (common && g_poll_tail && prm.nseg <= 16 && prm.N <= kTailMaxN &&
              prm.main_items <= kLateClaimItemsPerCta * (int64_t)(prm.dtype == SMCSD_BF16 ? k1_ctas<1, 0>() : k1_ctas<0, 0>()))
         m = TAIL_POLL;                   // latency-bound steps only (cfg4-sized streams: +10 us)
     if (m != TAIL_WAIT) prm.lt_words = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + L.words);
     return m;
 }
 
-smcsd_rc launch_lt(const Params &prm, int resample_mode, cudaStream_t st) {
-    static bool attr_set[64] = {false};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
-    if (!attr_set[dev]) {
-        // the same shared-memory carveout as K1, so that the SM configuration K1's CTAs run
-        // under admits this CTA beside them
-        if (cudaFuncSetAttribute(k_lt, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
-            return SMCSD_ECUDA;
-        attr_set[dev] = true;
-    }
-    return launch_pdl_b(k_lt, (unsigned)prm.P, 0, st, (unsigned)kLtThreads, prm, resample_mode);
-}
 
 template <int PW>
 smcsd_rc launch_rowstats_pw(const Params &prm, int dtype, int64_t items, cudaStream_t st) {
@@ -410,7 +388,8 @@ smcsd_rc smcsd_weights(const void *logits_p, int64_t ld_p, int rows_per_particle
     const TailMode tm = tail_mode(prm, workspace, L);
     rc = launch_rowstats(prm, dtype, items, st);
     if (rc != SMCSD_OK) return rc;
-    return tm == TAIL_LT ? launch_lt(prm, 0, st) : launch_tail(prm, 0, st);
+    (void)tm;
+    return launch_tail(prm, 0, st);
 }
 
 smcsd_rc smcsd_resample(const float *logw, int P, int N, int64_t prompt_base, float eta,
@@ -478,7 +457,8 @@ smcsd_rc smcsd_step(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
     const TailMode tm = tail_mode(prm, workspace, L);
     rc = launch_rowstats(prm, dtype, prm.main_items + prm.bonus_items, st);
     if (rc != SMCSD_OK) return rc;
-    return tm == TAIL_LT ? launch_lt(prm, 1, st) : launch_tail(prm, 1, st);
+    (void)tm;
+    return launch_tail(prm, 1, st);
 }
 
 smcsd_rc smcsd_weights_partial(const void *logits_p, int64_t ld_p, int rows_per_particle_p,
@@ -876,11 +856,6 @@ int smcsd_set_poll_tail(int enable) {
     return prev;
 }
 
-int smcsd_set_latency_tail(int enable) {
-    const int prev = g_latency_tail;
-    g_latency_tail = enable != 0;
-    return prev;
-}
 
 const char *smcsd_version(void) { return "smcsd 0.1 sm_100a"; }
 

@@ -81,7 +81,7 @@ struct Params {
     int nparts;
     // ---- workspace
     float4 *part_ws;                            // [P*2*N*K*nseg]
-    unsigned long long *lt_words;               // LT (smcsd_lt.cuh): [P*2*N*K*nseg] {m, s} words
+    unsigned long long *lt_words;               // polling tails: [nseg][P*2*N*K] {m, s} words
                                                 // K1 publishes, zero between steps; or null
     double *ell_ws;                             // [P*2*N*K]
     float *lam_ws;                              // [P*N]   (N > kTailMaxN path)
@@ -501,9 +501,9 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
     uint32_t *xep = reinterpret_cast<uint32_t *>(xdst + kXMaxG);     // S10: this launch's epoch
     __syncthreads();
     if (!XP && PW == 0 && prm.lt_words) {
-        // LT mode: the latency tail runs beside this grid (it polls lt_words), so let it launch
-        // now -- after the wait, so that it too sees the predecessor's outputs.  Every thread
-        // (the consumers would wait for the producer's first copy anyway).
+        // Polling tail: the tail polls lt_words (k_tail_small even runs beside this grid), so let
+        // it launch now -- after the wait, so that it too sees the predecessor's outputs.  Every
+        // thread (the consumers would wait for the producer's first copy anyway).
         pdl_wait();
         pdl_trigger();
     }
@@ -654,9 +654,9 @@ __global__ void __launch_bounds__(kK1Threads, k1_min_blocks<DT, PW>()) k_rowstat
                     }
                     if (lane == 0) done[s] = 0;
                 } else if (lane == 0) {
-                    if (PW == 0 && prm.lt_words) {            // LT: data and flag in one word,
-                        // segment-major ([seg][row]) so that the latency tail's row-per-thread
-                        // reads are coalesced
+                    if (PW == 0 && prm.lt_words) {            // polling tail: data and flag in
+                        // one word, segment-major ([seg][row]): the tail's lanes that take part
+                        // k of consecutive rows read consecutive words
                         const unsigned row = fastdiv((unsigned)m.item, prm.mg_nseg, prm.sh_nseg);
                         const unsigned sg = (unsigned)m.item - row * (unsigned)prm.nseg;
                         st_relaxed_gpu_b64(prm.lt_words + (size_t)sg * (unsigned)(2 * prm.P * prm.N * prm.K) + row,

@@ -1,5 +1,5 @@
 // smcsd_warp_tail.cuh -- S4-S7 of one prompt with N <= 64 particles as two warp-synchronous
-// routines, lane l = particles l (and l + 32) (the small-N tail of k_tail, k_tail_small, k_lt).
+// routines, lane l = particles l (and l + 32) (the small-N tail of k_tail and k_tail_small).
 //
 // The general S4-S7 (normalise_resample: one lane runs the prefix, a binary search per
 // particle, shared-memory atomics for the offspring, loops per lane) is a long chain of

@@ -19,10 +19,10 @@ for (P, N, K, V, dt) in ((1, 4, 4, 1000, torch.float32), (2, 16, 8, 20001, torch
     smc.smcsd_set_poll_tail(False)                                   # wait-for-K1 tail
     smc.smcsd_step(lp, lq, tok, V=V, n_drafted=ndr, step=2, eta=N / 2)
     smc.smcsd_set_poll_tail(True)
-    smc.smcsd_set_latency_tail(True)                                 # experimental latency tail
+    smc.smcsd_set_small_tail(False)                                  # 256-thread polling tail
     smc.smcsd_step(lp, lq, tok, V=V, n_drafted=ndr, step=2, eta=math.inf)
     smc.smcsd_weights(lp, lq, tok, V=V)
-    smc.smcsd_set_latency_tail(False)
+    smc.smcsd_set_small_tail(True)
     w = smc.smcsd_weights(lp, lq, tok, V=V, alpha=2.0)
     part = smc.smcsd_weights_partial(lp, lq, tok, v_begin=0, v_len=V)
     smc.smcsd_weights_combine(part.unsqueeze(0).contiguous(), tok, V=V)

@@ -19,8 +19,6 @@ ring = [synth.lm_logits(P, N, K, V, device=dev, seed=100 + r) for r in range(6)]
 lib = ctypes.CDLL(smc.lib_path)
 if os.environ.get("SMCSD_SMALL") is not None:
     smc.smcsd_set_small_tail(os.environ["SMCSD_SMALL"] == "1")
-if os.environ.get("SMCSD_LT"):
-    smc.smcsd_set_latency_tail(True)
 buf = (ctypes.c_ulonglong * 4096)()
 flush = torch.ones(64 << 20, dtype=torch.float32, device=dev)
 TP = os.environ.get("TP")            # fused-exchange smcsd_tp_step at G = 1 instead of smcsd_step

@@ -33,7 +33,7 @@ def lib():
 
 def test_every_declared_symbol_is_exported(lib):
     names = _declared()
-    assert len(names) == 27, names
+    assert len(names) == 26, names
     for n in names:
         assert hasattr(lib, n), n
 

@@ -3,8 +3,7 @@ and against the CPU oracle (staged protocol: the oracle's S4-S7 from the GPU's l
 same ancestry):
   * the small polling cluster tail k_tail_small (smcsd_tail_small.cuh, default for small steps),
   * the 256-thread polling tail (smcsd_set_small_tail(0)),
-  * the wait-for-K1 tail (smcsd_set_poll_tail(0)),
-  * the experimental latency tail k_lt (smcsd_lt.cuh, smcsd_set_latency_tail(1)).
+  * the wait-for-K1 tail (smcsd_set_poll_tail(0)).
 Each runs twice on one workspace: the polling tails leave K1's word array zero for the next call."""
 import math
 
@@ -34,13 +33,12 @@ def _bits(t):
 
 
 def _set(smc, variant):
-    smc.smcsd_set_latency_tail(variant == "lt")
     smc.smcsd_set_poll_tail(variant != "wait")
     smc.smcsd_set_small_tail(variant not in ("wait", "poll256"))
 
 
 def _run(smc, lt, mode, lp, lq, tok, ws, **kw):
-    _set(smc, lt if isinstance(lt, str) else ("lt" if lt else "wait"))
+    _set(smc, lt)
     try:
         if mode == "step":
             o = smc.smcsd_step(lp, lq, tok, workspace=ws, **kw)
@@ -68,7 +66,7 @@ def _run(smc, lt, mode, lp, lq, tok, ws, **kw):
     (1, 8, 32, 50000, torch.bfloat16, {"scheme": 1}),                        # K = 32: 16 small CTAs
 ])
 @pytest.mark.parametrize("mode", ["step", "weights"])
-def test_latency_tail_bit_identical(smc, P, N, K, V, dtype, extra, mode):
+def test_tail_variants_bit_identical(smc, P, N, K, V, dtype, extra, mode):
     dev = torch.device("cuda")
     lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=dtype, seed=900 + N + V, bonus=False)
     lp, lq, tok = lp.to(dev), lq.to(dev), tok.to(dev)
@@ -80,14 +78,14 @@ def test_latency_tail_bit_identical(smc, P, N, K, V, dtype, extra, mode):
         kw.update({k: v for k, v in extra.items() if k != "eta"})
         ws = smc.Workspace(dev)
         ref = _run(smc, "wait", mode, lp, lq, tok, ws, **kw)
-        for variant in ("small", "poll256", "lt"):
+        for variant in ("small", "poll256"):
             for rep in range(2):                 # twice on one workspace: the words were re-zeroed
                 got = _run(smc, variant, mode, lp, lq, tok, ws, **kw)
                 for f in ref:
                     assert torch.equal(_bits(ref[f]), _bits(got[f])), (variant, f, rep, ndv is not None)
 
 
-@pytest.mark.parametrize("variant", ["small", "poll256", "lt"])
+@pytest.mark.parametrize("variant", ["small", "poll256", "wait"])
 def test_tail_variant_staged_oracle_parity(smc, orc, variant):
     # the GPU's lam' (logw_pre) within 1e-4 of the oracle's, and the oracle's S4-S7 from it gives
     # the GPU's ancestry bit-exactly (reading G7: no ties here)
