@@ -196,17 +196,25 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
     int a[H], o[H], ties = 0;
 #pragma unroll
     for (int h = 0; h < H; ++h) a[h] = 0;
+    // outputs nobody asked for are not computed: the tie count without n_ties, the offspring and
+    // the slot plan without offspring / slot_src (uniform)
+    const bool need_ties = A.n_ties != nullptr || dry, need_plan = A.offspring != nullptr || A.slot_src != nullptr || dry;
     if (H == 1) {
         // N <= 32: every lane compares its u with all C (broadcast 16-byte reads)
         for (int m0 = 0; m0 < N8; m0 += 8) {
             double2 v[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) v[k] = reinterpret_cast<const double2 *>(eb)[(m0 >> 1) + k];
+            if (need_ties) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const double Cm = (k & 1) ? v[k >> 1].y : v[k >> 1].x;
-                a[0] += Cm <= u[0];
-                ties += act[0] && fabs(__dsub_rn(u[0], Cm)) <= tie;
+                for (int k = 0; k < 8; ++k) {
+                    const double Cm = (k & 1) ? v[k >> 1].y : v[k >> 1].x;
+                    a[0] += Cm <= u[0];
+                    ties += act[0] && fabs(__dsub_rn(u[0], Cm)) <= tie;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) a[0] += ((k & 1) ? v[k >> 1].y : v[k >> 1].x) <= u[0];
             }
         }
     } else {
@@ -220,7 +228,7 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
                 if (eb[mid] <= u[h]) lo = mid + 1; else hi = mid;
             }
             a[h] = lo;
-            if (act[h]) {
+            if (act[h] && need_ties) {
                 for (int m = lo - 1; m >= 0 && fabs(__dsub_rn(u[h], eb[m])) <= tie; --m) ++ties;
                 for (int m = lo; m < N && fabs(__dsub_rn(u[h], eb[m])) <= tie; ++m) ++ties;
             }
@@ -236,6 +244,22 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
     if (H == 1) ws.ib[lane + 32] = -1;
     __syncwarp();
     if (role == 0) SMCSD_PHASE(3);
+    if (!need_plan) {
+        ties = __reduce_add_sync(FULL, ties);
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            if (act[h] && out) {                                // S7
+                A.ancestors[pn[h]] = a[h];
+                A.logw_out[pn[h]] = reset;
+            }
+        }
+        if (lane == 0 && out) {
+            A.resampled[p] = 1;
+            if (A.n_ties) A.n_ties[p] = ties;
+        }
+        __syncwarp();
+        return;
+    }
     // offspring o_m = #{n : a_n = m}
     if (H == 1) {
         // broadcast reads of a (a = -1 beyond N never matches)
