@@ -198,6 +198,11 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
         return;
     }
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2050);               // finisher past the barrier
+#ifndef SMCSD_TS_LATE_TRIGGER
+    // The next kernel (the next step's K1, or the KV reindex) may launch now: its CTAs set up
+    // beside this one while S4-S7 runs, and its griddepcontrol.wait still waits for this grid.
+    pdl_trigger();
+#endif
     uint32_t f = 0;
     if (tid == 64)
         for (int r = 0; r < chunks; ++r) f |= s_flags[r];
