@@ -197,7 +197,7 @@ smcsd_rc ensure_tail_attrs() {
     return SMCSD_OK;
 }
 
-// Polling tail, N <= 32, N K <= 256 pairs (<= 16 CTAs of 16 pairs per prompt), no bonus rows:
+// Polling tail, N <= 64, N K <= 512 pairs (<= 16 CTAs of 16 or 32 pairs per prompt), no bonus rows:
 // k_tail_small (smcsd_tail_small.cuh), resident beside K1 from the start of its stream.
 #ifndef SMCSD_NO_TAIL_SMALL
 int g_tail_small = 1;
@@ -211,9 +211,10 @@ smcsd_rc launch_tail_small(const Params &prm, int resample_mode, int chunks, cud
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
     if (!attr_set[dev]) {
         // the SM configuration K1's CTAs run under must admit these CTAs beside them
-        if (cudaFuncSetAttribute(k_tail_small, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tail_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
-            return SMCSD_ECUDA;
+        for (auto *k : {k_tail_small<4, 1>, k_tail_small<4, 2>, k_tail_small<2, 1>, k_tail_small<2, 2>})
+            if (cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess ||
+                cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+                return SMCSD_ECUDA;
         attr_set[dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
@@ -229,14 +230,19 @@ smcsd_rc launch_tail_small(const Params &prm, int resample_mode, int chunks, cud
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, k_tail_small, prm, resample_mode, chunks) == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
+    const int64_t nk = (int64_t)prm.N * prm.K;
+    const bool l4 = nk <= 16ll * kTsMaxChunks, h1 = prm.N <= 32;
+    auto *k = l4 ? (h1 ? k_tail_small<4, 1> : k_tail_small<4, 2>) : (h1 ? k_tail_small<2, 1> : k_tail_small<2, 2>);
+    return cudaLaunchKernelEx(&cfg, k, prm, resample_mode, chunks) == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
 }
 
 smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {
     if (ensure_tail_attrs() != SMCSD_OK) return SMCSD_ECUDA;
     if (prm.N > kTailMaxN) return launch_pdl(k_tail_large, (unsigned)prm.P, kTailStageBytes, st, prm);
-    if (g_tail_small && prm.lt_words && !prm.bonus_tok && prm.x_from_logits && prm.N <= 32 && prm.nseg <= 16) {
-        const int cs = (int)cdiv((int64_t)prm.N * prm.K, kTsPairs);
+    if (g_tail_small && prm.lt_words && !prm.bonus_tok && prm.x_from_logits && prm.N <= kTsMaxN && prm.nseg <= 16) {
+        // 16 pairs per CTA (4 lanes per row) up to N K = 256, else 32 (2 lanes per row)
+        const int64_t nk = (int64_t)prm.N * prm.K;
+        const int cs = (int)cdiv(nk, nk <= 16ll * kTsMaxChunks ? 16 : 32);
         if (cs <= kTsMaxChunks && (int64_t)prm.P * cs < (1ll << 31)) return launch_tail_small(prm, resample_mode, cs, st);
     }
     const int chunks = (int)cdiv((int64_t)prm.N * prm.K, kPairsPerCta);

@@ -1059,37 +1059,40 @@ __device__ __forceinline__ float4 xp_decode(unsigned long long a, unsigned long 
     return make_float4(__uint_as_float((uint32_t)a), __uint_as_float((uint32_t)(a >> 32)),
                        __uint_as_float((uint32_t)b), 0.0f);
 }
-// Polling tail (prm.lt_words): parts pi0 .. pi0+3 of global row g from K1's segment-major
-// {m, s} words (nonzero once written; zeroed here for the next step).  Returns true on timeout
-// (the missing parts become neutral {-inf, 0}).
-__device__ __forceinline__ bool lt_take4(unsigned long long *words, int64_t total_rows, int64_t g, int pi0,
-                                         int nparts, float4 (&t)[4]) {
-    unsigned long long a[4];
-    bool nd[4];
+// Polling tail (prm.lt_words): of global row g, the KV groups of 4 parts starting at part
+// pi0 + pstep * v (v < KV) from K1's segment-major {m, s} words (nonzero once written; zeroed here
+// for the next step), all loads in flight at once.  Returns true on timeout (the missing parts
+// become neutral {-inf, 0}).
+template <int KV>
+__device__ __forceinline__ bool lt_take(unsigned long long *words, int64_t total_rows, int64_t g, int pi0, int pstep,
+                                        int nparts, float4 (&t)[4 * KV]) {
+    unsigned long long a[4 * KV];
+    bool nd[4 * KV];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        nd[k] = pi0 + k < nparts;
-        a[k] = nd[k] ? ld_relaxed_gpu_b64(words + (pi0 + k) * total_rows + g) : 0x00000000FF800000ull;
+    for (int i = 0; i < 4 * KV; ++i) {
+        const int pi = pi0 + pstep * (i >> 2) + (i & 3);
+        nd[i] = pi < nparts;
+        a[i] = nd[i] ? ld_relaxed_gpu_b64(words + pi * total_rows + g) : 0x00000000FF800000ull;
     }
     bool late = false;
     uint64_t t0 = 0;
     for (;;) {
         bool all = true;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) all &= a[k] != 0ull;
+        for (int i = 0; i < 4 * KV; ++i) all &= a[i] != 0ull;
         if (all) break;
         const uint64_t now = globaltimer_ns();
         if (t0 == 0) t0 = now;
         else if (now - t0 > kXTimeoutNs) { late = true; break; }
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (a[k] == 0ull) a[k] = ld_relaxed_gpu_b64(words + (pi0 + k) * total_rows + g);
+        for (int i = 0; i < 4 * KV; ++i)
+            if (a[i] == 0ull) a[i] = ld_relaxed_gpu_b64(words + (pi0 + pstep * (i >> 2) + (i & 3)) * total_rows + g);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (a[k] == 0ull) a[k] = 0x00000000FF800000ull;
-        t[k] = make_float4(__uint_as_float((uint32_t)a[k]), __uint_as_float((uint32_t)(a[k] >> 32)), -INFINITY, 0.0f);
-        if (nd[k]) __stcg(words + (pi0 + k) * total_rows + g, 0ull);
+    for (int i = 0; i < 4 * KV; ++i) {
+        if (a[i] == 0ull) a[i] = 0x00000000FF800000ull;
+        t[i] = make_float4(__uint_as_float((uint32_t)a[i]), __uint_as_float((uint32_t)(a[i] >> 32)), -INFINITY, 0.0f);
+        if (nd[i]) __stcg(words + (pi0 + pstep * (i >> 2) + (i & 3)) * total_rows + g, 0ull);
     }
     return late;
 }
@@ -1475,7 +1478,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_tail(const __grid_constant__ Pa
                 if (prm.xlocal) {
                     if (xp_take4(pr, prm.part_seg_stride, 4 * l4, prm.nparts, t)) atomicOr(&prm.st_ws[p], ST_EXCHANGE);
                 } else if (prm.lt_words) {
-                    s2_late = lt_take4(prm.lt_words, 2ll * prm.P * NK, grow, 4 * l4, prm.nparts, t);
+                    s2_late = lt_take<1>(prm.lt_words, 2ll * prm.P * NK, grow, 4 * l4, 0, prm.nparts, t);
                 } else {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {

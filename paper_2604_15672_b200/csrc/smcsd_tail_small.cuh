@@ -5,8 +5,9 @@
 // next to K1's six 288-thread CTAs per SM, so they start only as K1's CTAs exit and run their
 // one-shot code cold after K1's last item.  k_tail_small is the same computation in CTAs that
 // fit in what K1 leaves free on an SM (128 threads at <= 64 registers: one warp per SM
-// sub-partition; ~4.6 KB of shared memory): 16 (particle, position) pairs per CTA, a prompt's
-// CTAs one thread-block cluster (<= 16).  S3 runs in the chunk CTAs when K divides 16, else in
+// sub-partition; ~7 KB of shared memory): 16 (particle, position) pairs per CTA with 4 lanes per
+// row, or 32 with 2 lanes per row for N K up to 512, a prompt's CTAs one thread-block cluster
+// (<= 16), N <= 64.  S3 runs in the chunk CTAs when K divides 16, else in
 // the finisher from the terms the chunks push to it.  K1 launches it at once (polling tail), so its CTAs
 // are resident from the start of K1's stream: they read their inputs and poll K1's {m, s}
 // words while K1 runs, and the finishing CTA runs S4-S7 (warp_tail) once every chunk has
@@ -22,16 +23,22 @@
 namespace smcsd {
 
 constexpr int kTsThreads = 128;
-constexpr int kTsPairs = 16;                  // (particle, position) pairs per CTA: 32 rows x 4 lanes
 constexpr int kTsMaxChunks = 16;              // CTAs per prompt (one cluster, non-portable size)
-constexpr int kTsMaxPairs = kTsPairs * kTsMaxChunks;
+constexpr int kTsMaxPairs = 32 * kTsMaxChunks;
+constexpr int kTsMaxN = 64;                   // warp_tail<2>
 
-// grid = P x chunks (cluster = chunks <= 16, N <= 32), block = kTsThreads.
+// LPR = lanes per row: 4 (16 pairs = 32 rows per CTA, N K <= 256) or 2 (32 pairs = 64 rows per
+// CTA, N K <= 512).  With 2 lanes each lane merges the parts of two of the 4 "virtual" lanes
+// (l and l + 2) and the lanes combine exactly as the 4-lane butterfly does: bit-identical.
+// grid = P x chunks (cluster = chunks <= 16, N <= 64), block = kTsThreads.
+// H = particles per lane in S4-S7: 1 (N <= 32) or 2 (N <= 64), one warp_tail instance per kernel.
+template <int LPR, int H>
 __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_constant__ Params prm, int resample_mode,
                                                            int chunks) {
+    constexpr int kTsPairs = kTsThreads / (2 * LPR);
     __shared__ float4 rs[2 * kTsPairs];
     __shared__ double term_s[kTsPairs];
-    __shared__ float s_lam[32];                                 // finisher: every particle's lam'
+    __shared__ float s_lam[kTsMaxN];                            // finisher: every particle's lam'
     __shared__ double s_term[kTsMaxPairs];                      // finisher (S3 there): every pair's term
     __shared__ uint32_t s_flags[16];                            // finisher: every chunk's status bits
     __shared__ __align__(16) WtSmem wts;
@@ -72,14 +79,21 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
     // S3 runs in the chunk when whole particles fit in it (K divides 16); otherwise the chunks
     // push their terms to the finisher, whose warp 0 (lane n = particle n) sums them
     const bool s3_fin = (kTsPairs % K) != 0;                    // uniform
-    int kn_f = 0;
-    float prev_f = 0.0f;
-    if (s3_fin && crank == fin && tid < N) {
+    int kn_f0 = 0, kn_f1 = 0;
+    float prev_f0 = 0.0f, prev_f1 = 0.0f;
+    if (s3_fin && crank == fin && tid < 32) {
+        const float nl = (float)(-log((double)N));
         const int64_t pf = (int64_t)p * N + tid;
-        kn_f = drafted_len(prm, pf);
-        prev_f = prm.logw_prev ? prm.logw_prev[pf] : (float)(-log((double)N));
+        if (tid < N) {
+            kn_f0 = drafted_len(prm, pf);
+            prev_f0 = prm.logw_prev ? prm.logw_prev[pf] : nl;
+        }
+        if (H == 2 && tid + 32 < N) {
+            kn_f1 = drafted_len(prm, pf + 32);
+            prev_f1 = prm.logw_prev ? prm.logw_prev[pf + 32] : nl;
+        }
     }
-    double u = 0.0;
+    double u0 = 0.0, u1 = 0.0;
     float reset = 0.0f;
     if (crank == fin && tid < 64) {
         if (tid == 0) {
@@ -87,30 +101,51 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
                            prm.slot_src, prm.n_ties, prm.resampled, prm.eta, prm.N, prm.scheme};
             wts.st = 0u;
         }
-        if (resample_mode && tid < 32) u = tail_uniform(prm, p, lane);
+        if (resample_mode && tid < 32) {
+            u0 = tail_uniform(prm, p, lane);
+            if (H == 2) u1 = tail_uniform(prm, p, lane + 32);
+        }
         reset = (float)(-log((double)N));
     }
 
     // ---- S2: 4 lanes per row, 32 rows (16 target, 16 draft), polling K1's words
     bool late = false;
     {
-        const int l4 = tid & 3, lr = tid >> 2, qq = lr & (kTsPairs - 1);
-        float Ml = -INFINITY, Sl = 0.0f;
+        // lane li of a row merges virtual lanes v = li + LPR g (g < 4 / LPR): parts 4v .. 4v + 3
+        constexpr int kV = 4 / LPR;
+        const int li = tid & (LPR - 1), lr = tid / LPR, qq = lr & (kTsPairs - 1);
+        float Mv[kV], Sv[kV];
+#pragma unroll
+        for (int g = 0; g < kV; ++g) {
+            Mv[g] = -INFINITY;
+            Sv[g] = 0.0f;
+        }
         if (qq < nq) {
             const int64_t grow = (int64_t)p * rows + (int64_t)(lr / kTsPairs) * NK + q0 + qq;
-            float4 t[4];
-            late = lt_take4(prm.lt_words, 2ll * prm.P * NK, grow, 4 * l4, prm.nparts, t);
+            float4 t[4 * kV];
+            late = lt_take<kV>(prm.lt_words, 2ll * prm.P * NK, grow, 4 * li, 4 * LPR, prm.nparts, t);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) Ml = fmaxf(Ml, t[k].x);
+            for (int g = 0; g < kV; ++g) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) Sl = __fmaf_rn(t[k].y, t[k].x == Ml ? 1.0f : ex2_approx(t[k].x - Ml), Sl);
+                for (int k = 0; k < 4; ++k) Mv[g] = fmaxf(Mv[g], t[4 * g + k].x);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    Sv[g] = __fmaf_rn(t[4 * g + k].y, t[4 * g + k].x == Mv[g] ? 1.0f : ex2_approx(t[4 * g + k].x - Mv[g]), Sv[g]);
+            }
         }
-        float M = fmaxf(Ml, __shfl_xor_sync(0xffffffffu, Ml, 2));
+        // the 4-lane butterfly: M = max of all; S = (S0' + S2') + (S1' + S3'), Sv' = Sv 2^(Mv - M)
+        float M = kV == 2 ? fmaxf(Mv[0], Mv[kV - 1]) : fmaxf(Mv[0], __shfl_xor_sync(0xffffffffu, Mv[0], 2));
         M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 1));
-        float S = __fmul_rn(Sl, Ml == M ? 1.0f : ex2_approx(Ml - M));
-        S = __fadd_rn(S, __shfl_xor_sync(0xffffffffu, S, 2));
+        float S;
+        if (kV == 2) {
+            S = __fadd_rn(__fmul_rn(Sv[0], Mv[0] == M ? 1.0f : ex2_approx(Mv[0] - M)),
+                          __fmul_rn(Sv[kV - 1], Mv[kV - 1] == M ? 1.0f : ex2_approx(Mv[kV - 1] - M)));
+        } else {
+            S = __fmul_rn(Sv[0], Mv[0] == M ? 1.0f : ex2_approx(Mv[0] - M));
+            S = __fadd_rn(S, __shfl_xor_sync(0xffffffffu, S, 2));
+        }
         S = __fadd_rn(S, __shfl_xor_sync(0xffffffffu, S, 1));
-        if (l4 == 0) rs[lr] = make_float4(M, S, -INFINITY, 0.0f);
+        if (li == 0) rs[lr] = make_float4(M, S, -INFINITY, 0.0f);
     }
     const int any_late = __syncthreads_or(late);
     if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2053);      // chunk 0 S2 done
@@ -210,8 +245,7 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
         // S3 here: lam'_n = fl32(prev_n + sum_{j < k_n} term_{nK + j}) in j order
         if (tid < 32) {
             uint32_t st3 = 0;
-            if (tid < N) {
-                int kk = kn_f;
+            auto s3 = [&](int n, int kk, float pv) {
                 bool bad = false;
                 if (kk < 0 || kk > K) {
                     st3 |= ST_BAD_TOKEN;
@@ -219,24 +253,26 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
                     kk = 0;
                 }
                 double delta = 0.0;
-                for (int jj = 0; jj < kk; ++jj) delta = __dadd_rn(delta, s_term[tid * K + jj]);
+                for (int jj = 0; jj < kk; ++jj) delta = __dadd_rn(delta, s_term[n * K + jj]);
                 if (isnan(delta)) bad = true;
-                if (isnan(prev_f) || prev_f == INFINITY) {
+                if (isnan(pv) || pv == INFINITY) {
                     st3 |= ST_NONFINITE;
                     bad = true;
                 }
-                const float lm = bad ? -INFINITY : (float)__dadd_rn((double)prev_f, delta);
-                s_lam[tid] = lm;
-                const int64_t pf = (int64_t)p * N + tid;
+                const float lm = bad ? -INFINITY : (float)__dadd_rn((double)pv, delta);
+                s_lam[n] = lm;
+                const int64_t pf = (int64_t)p * N + n;
                 if (prm.logw_pre) prm.logw_pre[pf] = lm;
                 if (!resample_mode) prm.logw_out[pf] = lm;
-            }
+            };
+            if (tid < N) s3(tid, kn_f0, prev_f0);
+            if (H == 2 && tid + 32 < N) s3(tid + 32, kn_f1, prev_f1);
             st3 = __reduce_or_sync(0xffffffffu, st3);
             if (tid == 0 && st3) wts.st |= st3;                 // (role 1 sets only ST_DEGENERATE, later)
         }
         if (tid < 64) asm volatile("bar.sync 1, 64;" ::: "memory");     // s_lam for warp 1
     }
-    if (tid < 64) warp_tail<1>(tid >> 5, p, resample_mode, 0, s_lam, u, 0.0, reset, wts);
+    if (tid < 64) warp_tail<H>(tid >> 5, p, resample_mode, 0, s_lam, u0, u1, reset, wts);
     __syncthreads();
     if (tid == 64) prm.status[p] = f | wts.st;
     if (tid == 0 && p == 0) SMCSD_TRACE_AT(2052);               // S4-S7 done

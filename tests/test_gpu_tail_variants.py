@@ -64,6 +64,9 @@ def _run(smc, lt, mode, lp, lq, tok, ws, **kw):
     (1, 3, 5, 9000, torch.float32, {}),                                      # K = 5: S3 in the finisher
     (2, 6, 12, 30000, torch.bfloat16, {}),                                   # K = 12: S3 in the finisher
     (1, 8, 32, 50000, torch.bfloat16, {"scheme": 1}),                        # K = 32: 16 small CTAs
+    (1, 64, 8, 128256, torch.bfloat16, {}),                                  # N = 64: 2 lanes per row
+    (2, 40, 6, 30000, torch.float32, {"scheme": 1}),                         # S3 in the finisher, N > 32
+    (1, 48, 8, 20000, torch.bfloat16, {"eta": None}),
 ])
 @pytest.mark.parametrize("mode", ["step", "weights"])
 def test_tail_variants_bit_identical(smc, P, N, K, V, dtype, extra, mode):
