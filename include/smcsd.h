@@ -381,7 +381,7 @@ SMCSD_API smcsd_rc smcsd_tp_step(const void *logits_p, int64_t ld_p, int rows_pe
 SMCSD_API int smcsd_set_poll_tail(int enable);
 
 /* Small-tail switch (process-wide; default 1 = on).  Among the polling-tail calls, those with
- * N <= 32 and N*K <= 256 run the tail as 128-thread CTAs (16 pairs each, one
+ * N <= 64 and N*K <= 512 run the tail as 128-thread CTAs (16 or 32 pairs each, one
  * cluster per prompt) that fit beside K1's CTAs and are resident from the start of K1's stream
  * (paper_2604_15672_b200/csrc/smcsd_tail_small.cuh); results are bit-identical.  0 uses the
  * 256-thread tail for them.  Returns the previous setting. */
