@@ -10,6 +10,8 @@ import synth
 from paper_2604_15672_b200.dist import TPExchange
 
 dev = torch.device("cuda")
+if os.environ.get("SMCSD_SMALL") is not None:                 # small (K1-resident) tails on / off
+    smc.smcsd_set_small_tail(os.environ["SMCSD_SMALL"] == "1")
 P, N, K, V = 1, 64, 8, 128256
 ring = [synth.lm_logits(P, N, K, V, device=dev, seed=10 + r) for r in range(3)]
 
