@@ -71,7 +71,8 @@ typedef enum { SMCSD_SYSTEMATIC = 0, SMCSD_MULTINOMIAL = 1 } smcsd_scheme;
 #define SMCSD_ST_BAD_TOKEN   4u  /* drafted token outside [0,V), or n_drafted outside [0,K]         */
 #define SMCSD_ST_NONFINITE   8u  /* NaN/+inf logit or log-weight, or a row whose max is -inf        */
 #define SMCSD_ST_BAD_PAGE   16u  /* paged reindex: page id or ancestor out of range (entry skipped) */
-#define SMCSD_ST_EXCHANGE   32u  /* smcsd_tp_step: a peer's partials did not arrive within 20 s     */
+#define SMCSD_ST_EXCHANGE   32u  /* smcsd_tp_step: a peer's partials did not arrive within 20 s;   */
+                                 /* polling tails: K1's words of a row did not arrive within 20 s  */
 #define SMCSD_ST_BAD_INDEX  64u  /* kv reindex: src_index entry outside [0,N) (entry skipped), or an
                                     in-place index that is both a source and a destination (the
                                     prompt's in-place copies skipped)                              */
