@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
     }
     const int any_late = __syncthreads_or(late);
     if (tid == 0 && blockIdx.x == 0) SMCSD_TRACE_AT(2053);      // chunk 0 S2 done
+    if (tid == 0 && p == 0 && crank == fin) SMCSD_TRACE_AT(2054);   // finisher: its rows merged
     asm volatile("barrier.cluster.wait;" ::: "memory");         // phase 1 complete
 
     // ---- ell of both rows, the S3 term, S3 of whole particles (warp 0, lane = pair)
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
         }
         st = __reduce_or_sync(0xffffffffu, st);
         if (tid == 0) st_cluster_u32(&s_flags[crank], fin, st);
+        if (tid == 0 && p == 0 && crank == fin) SMCSD_TRACE_AT(2055);   // finisher: its S3 done
     }
     // ---- completion: the cluster barrier (release / acquire at cluster scope) hands every
     // chunk's lam' and bits to the finisher; this chunk's output stores go after the arrive

@@ -61,7 +61,8 @@ s = sorted(us(x) for x in starts)
 e = sorted(us(x) for x in ends)
 print(f"K1 CTAs {len(starts)}: start spread {s[-1]:.2f} us; done min {e[0]:.2f} median {e[len(e)//2]:.2f} "
       f"p90 {e[int(len(e)*0.9)]:.2f} max {e[-1]:.2f} us")
-names = {2060: "TP: last K1 CTA counted", 2061: "TP: system fence done", 2048: "tail CTA resident", 2049: "tail after pdl_wait", 2053: "chunk 0 S2+terms done", 2050: "last CTA of prompt 0", 2051: "after S3",
+names = {2060: "TP: last K1 CTA counted", 2061: "TP: system fence done", 2048: "tail CTA resident", 2049: "tail after pdl_wait", 2053: "chunk 0 S2+terms done",
+         2054: "finisher rows merged", 2055: "finisher S3 done", 2050: "last CTA of prompt 0", 2051: "after S3",
          2052: "after S4-S7", 2400: "LT CTA resident", 2401: "LT inputs+warm-up", 2402: "LT S2+S3 done",
          2403: "LT S4-S7 done"}
 for k, nm in names.items():

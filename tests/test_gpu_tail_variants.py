@@ -110,3 +110,20 @@ def test_tail_variant_staged_oracle_parity(smc, orc, variant):
     assert np.array_equal(np_(out.slot_src), staged["slot_src"])
     assert np.array_equal(np_(out.n_ties), staged["n_ties"])
     assert np.all(np_(out.status) == 0)
+
+
+def test_small_tail_many_prompts(smc, orc):
+    # thousands of one-CTA clusters (N K <= 16) queue behind the resident ones while K1 streams:
+    # bit-identical to the wait tail, staged oracle parity on every prompt
+    P, N, K, V = 3000, 2, 1, 100
+    dev = torch.device("cuda")
+    lp, lq, tok = synth.lm_logits(P, N, K, V, dtype=torch.float32, seed=77, bonus=False)
+    lp, lq, tok = lp.to(dev), lq.to(dev), tok.to(dev)
+    kw = dict(V=V, step=5, eta=math.inf)
+    ws = smc.Workspace(dev)
+    ref = _run(smc, "wait", "step", lp, lq, tok, ws, **kw)
+    got = _run(smc, "small", "step", lp, lq, tok, ws, **kw)
+    for f in ref:
+        assert torch.equal(_bits(ref[f]), _bits(got[f])), f
+    staged = orc.resample(np_(got["logw_pre"]), eta=math.inf, step=5)
+    assert np.array_equal(np_(got["ancestors"]), staged["ancestors"])
