@@ -11,7 +11,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libsmcsd.so")
 SOURCES = ["smcsd_api.cu"]
-DEPS = ["smcsd_api.cu", "smcsd_kernels.cuh", "smcsd_device.cuh", "smcsd_paged.cuh", "smcsd_tail_small.cuh", "smcsd_warp_tail.cuh"]
+DEPS = ["smcsd_api.cu", "smcsd_kernels.cuh", "smcsd_device.cuh", "smcsd_paged.cuh", "smcsd_tail_small.cuh", "smcsd_warp_tail.cuh", "smcsd_kv_tma.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -12,6 +12,7 @@
 #include "smcsd_kernels.cuh"
 #include "smcsd_paged.cuh"
 #include "smcsd_tail_small.cuh"
+#include "smcsd_kv_tma.cuh"
 
 using namespace smcsd;
 
@@ -540,6 +541,12 @@ smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
     KvParams prm;
     std::memset(&prm, 0, sizeof prm);
     prm.idx = src_index; prm.P = P; prm.N = N; prm.n_tensors = n_tensors; prm.status = status;
+    // bulk-copy kernel (smcsd_kv_tma.cuh) for N <= 256
+#ifndef SMCSD_NO_KV_TMA
+    const bool use_tma = N <= kKvTmaMaxN;
+#else
+    const bool use_tma = false;
+#endif
     int64_t items = 0;
     for (int k = 0; k < n_tensors; ++k) {
         const smcsd_kv_tensor &a = tensors[k];
@@ -561,10 +568,22 @@ smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
         t.in_place = a.dst == a.src;
         prm.any_in_place |= t.in_place;
         t.vecs = (uint64_t)a.seg_count * vps;
-        t.nchunks = (int64_t)cdiv((int64_t)t.vecs, kKvChunkVec);
+        t.nchunks = use_tma ? (int64_t)a.seg_count * cdiv(a.seg_bytes, kKvTmaChunk)
+                            : (int64_t)cdiv((int64_t)t.vecs, kKvChunkVec);
         items += a.n_outer * P * t.nchunks;
         if (items >= (1ll << 31)) return SMCSD_EINVAL;
         t.item_end = items;
+    }
+    if (use_tma) {
+        static bool attr_set[64] = {false};
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
+        if (!attr_set[dev]) {
+            if (cudaFuncSetAttribute(k_kv_reindex_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kKvTmaChunk) != cudaSuccess)
+                return SMCSD_ECUDA;
+            attr_set[dev] = true;
+        }
+        return launch_pdl(k_kv_reindex_tma, (unsigned)items, 2 * kKvTmaChunk, as_stream(stream), prm);
     }
     return launch_pdl(k_kv_reindex, (unsigned)items, 0, as_stream(stream), prm);
 }

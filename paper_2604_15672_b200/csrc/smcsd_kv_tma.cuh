@@ -1,0 +1,129 @@
+// smcsd_kv_tma.cuh -- K3 (S8/S9 source-major block gather) with bulk asynchronous copies.
+//
+// k_kv_reindex moves every 16-byte vector through registers: 256 threads x 4 loads of a 16 KB
+// chunk per source, then the stores to each destination.  Here one thread per CTA drives the
+// copy engine instead: cp.async.bulk loads a chunk of a source (up to kKvTmaChunk bytes of one
+// segment) into shared memory (mbarrier, complete_tx), and cp.async.bulk stores it from there to
+// every destination; two buffers, so the next source's load is in flight while the current
+// one's stores drain.  The copy plan and the ST_BAD_INDEX policy are k_kv_reindex's.
+#pragma once
+#include "smcsd_kernels.cuh"
+
+namespace smcsd {
+
+#ifndef SMCSD_KV_TMA_CHUNK
+#define SMCSD_KV_TMA_CHUNK 16384
+#endif
+constexpr int kKvTmaChunk = SMCSD_KV_TMA_CHUNK;             // bytes per chunk (within one segment)
+constexpr int kKvTmaMaxN = 256;                              // particles (plan arrays in smem)
+
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 :: "l"(dst), "r"(smem_u32(src_smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" :: "n"(N) : "memory"); }
+
+// grid = sum over tensors of n_outer * P * seg_count * ceil(seg_bytes / kKvTmaChunk) (item_end
+// holds the prefix; nchunks = chunks per block), block = kThreads, dynamic smem = 2 chunks.
+__global__ void __launch_bounds__(kThreads) k_kv_reindex_tma(const __grid_constant__ KvParams prm) {
+    extern __shared__ __align__(128) char kbuf[];                // [2][kKvTmaChunk]
+    __shared__ __align__(8) uint64_t full[2];
+    __shared__ int cnt[kKvTmaMaxN], start[kKvTmaMaxN], fill[kKvTmaMaxN], dsts[kKvTmaMaxN], srcs[kKvTmaMaxN];
+    __shared__ int wtot[kWarps + 1];
+    __shared__ int s_bad;
+    const int tid = threadIdx.x, N = prm.N;
+    int lo = 0, hi = prm.n_tensors - 1;                        // first tensor with item_end > item
+    const int64_t gitem = blockIdx.x;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (prm.t[mid].item_end > gitem) hi = mid; else lo = mid + 1;
+    }
+    const KvTensor &T = prm.t[lo];
+    const int64_t item = gitem - (lo > 0 ? prm.t[lo - 1].item_end : 0);
+    const int64_t chunk = item % T.nchunks;
+    const int64_t op = item / T.nchunks;
+    const int p = (int)(op % prm.P);
+    const int64_t o = op / prm.P;
+    const int in_place = T.in_place;
+    const int32_t *idx = prm.idx + (int64_t)p * N;
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
+        s_bad = 0;
+    }
+    pdl_wait();                                                // src_index from the tail kernel
+
+    // ---- copy plan for prompt p (k_kv_reindex's): destinations grouped by source
+    for (int n = tid; n < N; n += kThreads) {
+        cnt[n] = 0;
+        srcs[n] = idx[n];
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int n = tid; n < N; n += kThreads) {
+        const int s = srcs[n];
+        if ((unsigned)s >= (unsigned)N) bad |= 1;
+        else if (s != n && srcs[s] != s) bad |= 2;
+        if ((unsigned)s < (unsigned)N && (!in_place || s != n)) atomicAdd(&cnt[s], 1);
+    }
+    if (bad) atomicOr(&s_bad, bad);
+    __syncthreads();
+    const int pbad = s_bad;
+    if (prm.status && lo == 0 && o == 0 && chunk == 0 && tid == 0)
+        prm.status[p] = ((pbad & 1) || ((pbad & 2) && prm.any_in_place)) ? ST_BAD_INDEX : 0u;
+    if (in_place && (pbad & 2)) return;
+    for (int n = tid; n < N; n += kThreads) {
+        start[n] = cnt[n];
+        fill[n] = cnt[n] > 0;
+    }
+    __syncthreads();
+    block_exclusive_scan(start, N, wtot);
+    const int nsrc = block_exclusive_scan(fill, N, wtot);
+    for (int m = tid; m < N; m += kThreads)
+        if (cnt[m] > 0) srcs[fill[m]] = m;
+    __syncthreads();
+    for (int m = tid; m < N; m += kThreads) fill[m] = 0;
+    __syncthreads();
+    for (int n = tid; n < N; n += kThreads) {
+        const int s = idx[n];
+        if ((unsigned)s < (unsigned)N && (!in_place || s != n))
+            dsts[start[s] + atomicAdd(&fill[s], 1)] = n;
+    }
+    __syncthreads();
+    if (tid != 0) return;
+
+    // ---- this chunk: segment g, bytes [off, off + len) of it
+    const int64_t cps = ((int64_t)T.vps * 16 + kKvTmaChunk - 1) / kKvTmaChunk;   // chunks per segment
+    const int64_t g = chunk / cps;
+    const int64_t off = (chunk - g * cps) * kKvTmaChunk;
+    const uint32_t len = (uint32_t)min((int64_t)kKvTmaChunk, (int64_t)T.vps * 16 - off);
+    const int64_t base = o * T.outer_stride + (int64_t)p * T.prompt_stride + g * T.seg_stride + off;
+    // two buffers: source k+1 loads while source k's stores drain
+    auto load = [&](int k) {
+        const int b = k & 1;
+        mbar_arrive_expect_tx(&full[b], len);
+        bulk_g2s(kbuf + b * kKvTmaChunk, T.src + base + (int64_t)srcs[k] * T.particle_stride, len, &full[b]);
+    };
+    if (nsrc > 0) load(0);
+    for (int k = 0; k < nsrc; ++k) {
+        const int b = k & 1;
+        if (k + 1 < nsrc) {
+            // buffer 1 - b was last read by source k - 1's stores
+            bulk_wait_read<0>();
+            load(k + 1);
+        }
+        mbar_wait(&full[b], (uint32_t)((k >> 1) & 1));
+        const int s = srcs[k], c = cnt[s], st0 = start[s];
+        for (int q = 0; q < c; ++q)
+            bulk_s2g(T.dst + base + (int64_t)dsts[st0 + q] * T.particle_stride, kbuf + b * kKvTmaChunk, len);
+        bulk_commit();
+    }
+    bulk_wait_read<0>();                                       // (smem must outlive the stores' reads)
+}
+
+}  // namespace smcsd
