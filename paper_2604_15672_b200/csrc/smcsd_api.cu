@@ -579,11 +579,11 @@ smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
         int dev = 0;
         if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
         if (!attr_set[dev]) {
-            if (cudaFuncSetAttribute(k_kv_reindex_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kKvTmaChunk) != cudaSuccess)
+            if (cudaFuncSetAttribute(k_kv_reindex_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvTmaBufs * kKvTmaChunk) != cudaSuccess)
                 return SMCSD_ECUDA;
             attr_set[dev] = true;
         }
-        return launch_pdl(k_kv_reindex_tma, (unsigned)items, 2 * kKvTmaChunk, as_stream(stream), prm);
+        return launch_pdl(k_kv_reindex_tma, (unsigned)items, kKvTmaBufs * kKvTmaChunk, as_stream(stream), prm);
     }
     return launch_pdl(k_kv_reindex, (unsigned)items, 0, as_stream(stream), prm);
 }

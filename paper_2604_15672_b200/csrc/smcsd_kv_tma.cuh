@@ -4,7 +4,7 @@
 // chunk per source, then the stores to each destination.  Here one thread per CTA drives the
 // copy engine instead: cp.async.bulk loads a chunk of a source (up to kKvTmaChunk bytes of one
 // segment) into shared memory (mbarrier, complete_tx), and cp.async.bulk stores it from there to
-// every destination; two buffers, so the next source's load is in flight while the current
+// every destination; four buffers, so the next sources' loads are in flight while the current
 // one's stores drain.  The copy plan and the ST_BAD_INDEX policy are k_kv_reindex's.
 #pragma once
 #include "smcsd_kernels.cuh"
@@ -12,9 +12,13 @@
 namespace smcsd {
 
 #ifndef SMCSD_KV_TMA_CHUNK
-#define SMCSD_KV_TMA_CHUNK 16384
+#define SMCSD_KV_TMA_CHUNK 8192
 #endif
 constexpr int kKvTmaChunk = SMCSD_KV_TMA_CHUNK;             // bytes per chunk (within one segment)
+#ifndef SMCSD_KV_TMA_BUFS
+#define SMCSD_KV_TMA_BUFS 4
+#endif
+constexpr int kKvTmaBufs = SMCSD_KV_TMA_BUFS;               // chunk buffers (loads in flight + 1)
 constexpr int kKvTmaMaxN = 256;                              // particles (plan arrays in smem)
 
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
@@ -30,8 +34,8 @@ __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_g
 // grid = sum over tensors of n_outer * P * seg_count * ceil(seg_bytes / kKvTmaChunk) (item_end
 // holds the prefix; nchunks = chunks per block), block = kThreads, dynamic smem = 2 chunks.
 __global__ void __launch_bounds__(kThreads) k_kv_reindex_tma(const __grid_constant__ KvParams prm) {
-    extern __shared__ __align__(128) char kbuf[];                // [2][kKvTmaChunk]
-    __shared__ __align__(8) uint64_t full[2];
+    extern __shared__ __align__(128) char kbuf[];                // [kKvTmaBufs][kKvTmaChunk]
+    __shared__ __align__(8) uint64_t full[kKvTmaBufs];
     __shared__ int cnt[kKvTmaMaxN], start[kKvTmaMaxN], fill[kKvTmaMaxN], dsts[kKvTmaMaxN], srcs[kKvTmaMaxN];
     __shared__ int wtot[kWarps + 1];
     __shared__ int s_bad;
@@ -51,8 +55,7 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex_tma(const __grid_consta
     const int in_place = T.in_place;
     const int32_t *idx = prm.idx + (int64_t)p * N;
     if (tid == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
+        for (int b = 0; b < kKvTmaBufs; ++b) mbar_init(&full[b], 1);
         fence_mbar_init();
         s_bad = 0;
     }
@@ -103,21 +106,22 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex_tma(const __grid_consta
     const int64_t off = (chunk - g * cps) * kKvTmaChunk;
     const uint32_t len = (uint32_t)min((int64_t)kKvTmaChunk, (int64_t)T.vps * 16 - off);
     const int64_t base = o * T.outer_stride + (int64_t)p * T.prompt_stride + g * T.seg_stride + off;
-    // two buffers: source k+1 loads while source k's stores drain
+    // kKvTmaBufs buffers: the loads of sources k+1 .. k+B-1 are in flight while source k's
+    // stores drain (one bulk group per source)
     auto load = [&](int k) {
-        const int b = k & 1;
+        const int b = k % kKvTmaBufs;
         mbar_arrive_expect_tx(&full[b], len);
         bulk_g2s(kbuf + b * kKvTmaChunk, T.src + base + (int64_t)srcs[k] * T.particle_stride, len, &full[b]);
     };
-    if (nsrc > 0) load(0);
+    for (int k = 0; k < kKvTmaBufs - 1 && k < nsrc; ++k) load(k);
     for (int k = 0; k < nsrc; ++k) {
-        const int b = k & 1;
-        if (k + 1 < nsrc) {
-            // buffer 1 - b was last read by source k - 1's stores
+        const int b = k % kKvTmaBufs;
+        if (k + kKvTmaBufs - 1 < nsrc) {
+            // its buffer was last read by the stores of source k - 1 (the newest group)
             bulk_wait_read<0>();
-            load(k + 1);
+            load(k + kKvTmaBufs - 1);
         }
-        mbar_wait(&full[b], (uint32_t)((k >> 1) & 1));
+        mbar_wait(&full[b], (uint32_t)((k / kKvTmaBufs) & 1));
         const int s = srcs[k], c = cnt[s], st0 = start[s];
         for (int q = 0; q < c; ++q)
             bulk_s2g(T.dst + base + (int64_t)dsts[st0 + q] * T.particle_stride, kbuf + b * kKvTmaChunk, len);
