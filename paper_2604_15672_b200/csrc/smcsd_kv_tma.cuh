@@ -4,7 +4,7 @@
 // chunk per source, then the stores to each destination.  Here one thread per CTA drives the
 // copy engine instead: cp.async.bulk loads a chunk of a source (up to kKvTmaChunk bytes of one
 // segment) into shared memory (mbarrier, complete_tx), and cp.async.bulk stores it from there to
-// every destination; four buffers, so the next sources' loads are in flight while the current
+// every destination; eight buffers, so the next sources' loads are in flight while the current
 // one's stores drain.  The copy plan and the ST_BAD_INDEX policy are k_kv_reindex's.
 #pragma once
 #include "smcsd_kernels.cuh"
@@ -12,18 +12,37 @@
 namespace smcsd {
 
 #ifndef SMCSD_KV_TMA_CHUNK
-#define SMCSD_KV_TMA_CHUNK 8192
+#define SMCSD_KV_TMA_CHUNK 4096
 #endif
 constexpr int kKvTmaChunk = SMCSD_KV_TMA_CHUNK;             // bytes per chunk (within one segment)
 #ifndef SMCSD_KV_TMA_BUFS
-#define SMCSD_KV_TMA_BUFS 4
+#define SMCSD_KV_TMA_BUFS 8
 #endif
 constexpr int kKvTmaBufs = SMCSD_KV_TMA_BUFS;               // chunk buffers (loads in flight + 1)
 constexpr int kKvTmaMaxN = 256;                              // particles (plan arrays in smem)
 
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
+#ifdef SMCSD_KV_TMA_EVICT_FIRST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                 :: "l"(dst), "r"(smem_u32(src_smem)), "r"(bytes), "l"(pol) : "memory");
+#else
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
                  :: "l"(dst), "r"(smem_u32(src_smem)), "r"(bytes) : "memory");
+#endif
+}
+// global -> shared bulk load (k_kv_reindex_tma's sources), optionally with an L2 evict-first hint
+__device__ __forceinline__ void bulk_g2s_kv(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+#ifdef SMCSD_KV_TMA_EVICT_FIRST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
+#else
+    bulk_g2s(dst, src, bytes, bar);
+#endif
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
@@ -111,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex_tma(const __grid_consta
     auto load = [&](int k) {
         const int b = k % kKvTmaBufs;
         mbar_arrive_expect_tx(&full[b], len);
-        bulk_g2s(kbuf + b * kKvTmaChunk, T.src + base + (int64_t)srcs[k] * T.particle_stride, len, &full[b]);
+        bulk_g2s_kv(kbuf + b * kKvTmaChunk, T.src + base + (int64_t)srcs[k] * T.particle_stride, len, &full[b]);
     };
     for (int k = 0; k < kKvTmaBufs - 1 && k < nsrc; ++k) load(k);
     for (int k = 0; k < nsrc; ++k) {
