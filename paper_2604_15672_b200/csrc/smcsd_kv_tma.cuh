@@ -4,7 +4,7 @@
 // chunk per source, then the stores to each destination.  Here one thread per CTA drives the
 // copy engine instead: cp.async.bulk loads a chunk of a source (up to kKvTmaChunk bytes of one
 // segment) into shared memory (mbarrier, complete_tx), and cp.async.bulk stores it from there to
-// every destination; eight buffers, so the next sources' loads are in flight while the current
+// every destination; four buffers, so the next sources' loads are in flight while the current
 // one's stores drain.  The copy plan and the ST_BAD_INDEX policy are k_kv_reindex's.
 #pragma once
 #include "smcsd_kernels.cuh"
@@ -12,11 +12,11 @@
 namespace smcsd {
 
 #ifndef SMCSD_KV_TMA_CHUNK
-#define SMCSD_KV_TMA_CHUNK 4096
+#define SMCSD_KV_TMA_CHUNK 8192
 #endif
 constexpr int kKvTmaChunk = SMCSD_KV_TMA_CHUNK;             // bytes per chunk (within one segment)
 #ifndef SMCSD_KV_TMA_BUFS
-#define SMCSD_KV_TMA_BUFS 8
+#define SMCSD_KV_TMA_BUFS 4
 #endif
 constexpr int kKvTmaBufs = SMCSD_KV_TMA_BUFS;               // chunk buffers (loads in flight + 1)
 constexpr int kKvTmaMaxN = 256;                              // particles (plan arrays in smem)
