@@ -579,10 +579,15 @@ smcsd_rc smcsd_kv_reindex_multi(const smcsd_kv_tensor *tensors, int n_tensors,
         int dev = 0;
         if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SMCSD_ECUDA;
         if (!attr_set[dev]) {
-            if (cudaFuncSetAttribute(k_kv_reindex_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvTmaBufs * kKvTmaChunk) != cudaSuccess)
+            if (cudaFuncSetAttribute(k_kv_reindex_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvTmaBufs * kKvTmaChunk) != cudaSuccess ||
+                cudaFuncSetAttribute(k_kv_reindex_tma_w, cudaFuncAttributeMaxDynamicSharedMemorySize, kKvTmaBufs * kKvTmaChunk) != cudaSuccess)
                 return SMCSD_ECUDA;
             attr_set[dev] = true;
         }
+#ifndef SMCSD_NO_KV_TMA_WARP
+        if (N <= 32)
+            return launch_pdl_b(k_kv_reindex_tma_w, (unsigned)items, kKvTmaBufs * kKvTmaChunk, as_stream(stream), 32u, prm);
+#endif
         return launch_pdl(k_kv_reindex_tma, (unsigned)items, kKvTmaBufs * kKvTmaChunk, as_stream(stream), prm);
     }
     return launch_pdl(k_kv_reindex, (unsigned)items, 0, as_stream(stream), prm);

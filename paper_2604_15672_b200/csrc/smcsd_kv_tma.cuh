@@ -4,7 +4,7 @@
 // chunk per source, then the stores to each destination.  Here one thread per CTA drives the
 // copy engine instead: cp.async.bulk loads a chunk of a source (up to kKvTmaChunk bytes of one
 // segment) into shared memory (mbarrier, complete_tx), and cp.async.bulk stores it from there to
-// every destination; four buffers, so the next sources' loads are in flight while the current
+// every destination; eight buffers, so the next sources' loads are in flight while the current
 // one's stores drain.  The copy plan and the ST_BAD_INDEX policy are k_kv_reindex's.
 #pragma once
 #include "smcsd_kernels.cuh"
@@ -12,11 +12,11 @@
 namespace smcsd {
 
 #ifndef SMCSD_KV_TMA_CHUNK
-#define SMCSD_KV_TMA_CHUNK 8192
+#define SMCSD_KV_TMA_CHUNK 4096
 #endif
 constexpr int kKvTmaChunk = SMCSD_KV_TMA_CHUNK;             // bytes per chunk (within one segment)
 #ifndef SMCSD_KV_TMA_BUFS
-#define SMCSD_KV_TMA_BUFS 4
+#define SMCSD_KV_TMA_BUFS 8
 #endif
 constexpr int kKvTmaBufs = SMCSD_KV_TMA_BUFS;               // chunk buffers (loads in flight + 1)
 constexpr int kKvTmaMaxN = 256;                              // particles (plan arrays in smem)
@@ -147,6 +147,96 @@ __global__ void __launch_bounds__(kThreads) k_kv_reindex_tma(const __grid_consta
         bulk_commit();
     }
     bulk_wait_read<0>();                                       // (smem must outlive the stores' reads)
+}
+
+// The same copy with N <= 32 and one warp per CTA: lane n = particle n builds the plan with warp
+// votes and shared-memory counts (no block barriers), lane 0 drives the copy.  For small N the
+// per-CTA plan is what a CTA mostly does besides waiting on the copy engine; a warp builds it in
+// a few dozen instructions and more CTAs fit on an SM.
+__global__ void __launch_bounds__(32) k_kv_reindex_tma_w(const __grid_constant__ KvParams prm) {
+    extern __shared__ __align__(128) char kbuf[];                // [kKvTmaBufs][kKvTmaChunk]
+    __shared__ __align__(8) uint64_t full[kKvTmaBufs];
+    __shared__ int cnt[32], start[32], dsts[32], srcs[32];
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x, N = prm.N;
+    int lo = 0, hi = prm.n_tensors - 1;
+    const int64_t gitem = blockIdx.x;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (prm.t[mid].item_end > gitem) hi = mid; else lo = mid + 1;
+    }
+    const KvTensor &T = prm.t[lo];
+    const int64_t item = gitem - (lo > 0 ? prm.t[lo - 1].item_end : 0);
+    const int64_t chunk = item % T.nchunks;
+    const int64_t op = item / T.nchunks;
+    const int p = (int)(op % prm.P);
+    const int64_t o = op / prm.P;
+    const int in_place = T.in_place;
+    if (lane == 0) {
+        for (int b = 0; b < kKvTmaBufs; ++b) mbar_init(&full[b], 1);
+        fence_mbar_init();
+    }
+    cnt[lane] = 0;
+    pdl_wait();                                                // src_index from the tail kernel
+    // ---- copy plan (k_kv_reindex's): lane n holds src_index[n]
+    const bool act = lane < N;
+    const int s = act ? prm.idx[(int64_t)p * N + lane] : -1;
+    const bool inr = act && (unsigned)s < (unsigned)N;
+    const int s_of_s = __shfl_sync(FULL, s, inr ? s : 0);      // src_index[s]
+    int bad = 0;
+    if (act && !inr) bad |= 1;
+    if (inr && s != lane && s_of_s != s) bad |= 2;             // source s is itself overwritten
+    bad = __reduce_or_sync(FULL, bad);
+    if (prm.status && lo == 0 && o == 0 && chunk == 0 && lane == 0)
+        prm.status[p] = ((bad & 1) || ((bad & 2) && prm.any_in_place)) ? ST_BAD_INDEX : 0u;
+    if (in_place && (bad & 2)) return;
+    const bool valid = inr && (!in_place || s != lane);
+    __syncwarp();
+    if (valid) atomicAdd(&cnt[s], 1);
+    __syncwarp();
+    const int c = cnt[lane];
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned has = __ballot_sync(FULL, c > 0);
+    const int nsrc = __popc(has);
+    if (c > 0) srcs[__popc(has & lt)] = lane;
+    int x = c;                                                 // inclusive scan of the counts
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, d);
+        if (lane >= d) x += y;
+    }
+    start[lane] = x - c;
+    const unsigned grp = __match_any_sync(FULL, valid ? s : -1 - lane);
+    const int st_s = __shfl_sync(FULL, x - c, valid ? s : 0);  // start[s]
+    __syncwarp();
+    if (valid) dsts[st_s + __popc(grp & lt)] = lane;
+    __syncwarp();
+    if (lane != 0) return;
+
+    const int64_t cps = ((int64_t)T.vps * 16 + kKvTmaChunk - 1) / kKvTmaChunk;   // chunks per segment
+    const int64_t g = chunk / cps;
+    const int64_t off = (chunk - g * cps) * kKvTmaChunk;
+    const uint32_t len = (uint32_t)min((int64_t)kKvTmaChunk, (int64_t)T.vps * 16 - off);
+    const int64_t base = o * T.outer_stride + (int64_t)p * T.prompt_stride + g * T.seg_stride + off;
+    auto load = [&](int k) {
+        const int b = k % kKvTmaBufs;
+        mbar_arrive_expect_tx(&full[b], len);
+        bulk_g2s_kv(kbuf + b * kKvTmaChunk, T.src + base + (int64_t)srcs[k] * T.particle_stride, len, &full[b]);
+    };
+    for (int k = 0; k < kKvTmaBufs - 1 && k < nsrc; ++k) load(k);
+    for (int k = 0; k < nsrc; ++k) {
+        const int b = k % kKvTmaBufs;
+        if (k + kKvTmaBufs - 1 < nsrc) {
+            bulk_wait_read<0>();
+            load(k + kKvTmaBufs - 1);
+        }
+        mbar_wait(&full[b], (uint32_t)((k / kKvTmaBufs) & 1));
+        const int sk = srcs[k], ck = cnt[sk], s0 = start[sk];
+        for (int q = 0; q < ck; ++q)
+            bulk_s2g(T.dst + base + (int64_t)dsts[s0 + q] * T.particle_stride, kbuf + b * kKvTmaChunk, len);
+        bulk_commit();
+    }
+    bulk_wait_read<0>();
 }
 
 }  // namespace smcsd
