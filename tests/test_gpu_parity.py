@@ -453,6 +453,14 @@ def test_kv_reindex_ragged(smc, orc, in_place):
     _kv_case(smc, orc, L=1, P=2, N=1024, H=1, S=8, d=8, seq_len=8, in_place=in_place, seed=3)
 
 
+@pytest.mark.parametrize("N", [1, 2, 31, 32, 33, 256, 257])
+@pytest.mark.parametrize("in_place", [False, True])
+def test_kv_reindex_kernel_boundaries(smc, orc, N, in_place):
+    # the three K3 kernels' ranges (one-warp bulk copy N <= 32, 256-thread bulk copy N <= 256,
+    # register path above), segments of 4 KB + a ragged part (seq_len < S: non-contiguous)
+    _kv_case(smc, orc, L=2, P=2, N=N, H=3, S=48, d=64, seq_len=40, in_place=in_place, seed=50 + N)
+
+
 def test_token_history_reindex(smc, orc):
     # S9: tok'[p][n][:] = tok[p][a_n][:], int32 rows through the same entry point
     dev = torch.device("cuda")
