@@ -125,6 +125,9 @@ def dist_env(args):
         backend = os.environ.get("SMCSD_BENCH_BACKEND", "nccl")   # gloo: functional test only
         if args.impl == "reference" or backend == "gloo":
             if args.impl != "reference":
+                if torch.cuda.device_count() == 0:
+                    raise SystemExit("bench.py: our arm runs the CUDA path and this box has no GPU "
+                                     "(--impl reference runs the CPU oracle arm)")
                 torch.cuda.set_device(local % torch.cuda.device_count())
             dist.init_process_group("gloo")
         else:
