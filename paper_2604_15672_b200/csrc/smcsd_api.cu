@@ -234,7 +234,12 @@ smcsd_rc launch_tail_small(const Params &prm, int resample_mode, int chunks, cud
     const int64_t nk = (int64_t)prm.N * prm.K;
     const bool l4 = nk <= 16ll * kTsMaxChunks, h1 = prm.N <= 32;
     auto *k = l4 ? (h1 ? k_tail_small<4, 1> : k_tail_small<4, 2>) : (h1 ? k_tail_small<2, 1> : k_tail_small<2, 2>);
-    return cudaLaunchKernelEx(&cfg, k, prm, resample_mode, chunks) == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
+    // the CTAs poll K1's words only once K1's work counter shows every item claimed (gate_ctr)
+    Params p2 = prm;
+    const int64_t ctas = prm.dtype == SMCSD_BF16 ? k1_ctas<1, 0>() : k1_ctas<0, 0>();
+    const int64_t items = prm.main_items + prm.bonus_items, k1_grid = items < ctas ? items : ctas;
+    p2.gate_ctr = (unsigned)(items - k1_grid);
+    return cudaLaunchKernelEx(&cfg, k, p2, resample_mode, chunks) == cudaSuccess ? SMCSD_OK : SMCSD_ECUDA;
 }
 
 smcsd_rc launch_tail(const Params &prm, int resample_mode, cudaStream_t st) {

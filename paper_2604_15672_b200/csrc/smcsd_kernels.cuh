@@ -96,6 +96,7 @@ struct Params {
     int32_t *selected;                          // smcsd_select output [P]
     int x_from_logits;                          // 1: tail loads t_d from the logits; 0: from parts
     int late_claim;                             // K1: claim items only when a ring slot is free
+    unsigned gate_ctr;                          // k_tail_small: work_ctr once every K1 item is claimed
     unsigned *work_ctr;                         // K1 dynamic work counter (re-armed by K2)
     unsigned *prompt_ctr;                       // [P] K2 chunk completion counters
     uint32_t *st_ws;                            // [P] K2 status accumulation

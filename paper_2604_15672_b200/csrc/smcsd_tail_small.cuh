@@ -9,9 +9,9 @@
 // row, or 32 with 2 lanes per row for N K up to 512, a prompt's CTAs one thread-block cluster
 // (<= 16), N <= 64.  S3 runs in the chunk CTAs when K divides 16, else in
 // the finisher from the terms the chunks push to it.  K1 launches it at once (polling tail), so its CTAs
-// are resident from the start of K1's stream: they read their inputs and poll K1's {m, s}
-// words while K1 runs, and the finishing CTA runs S4-S7 (warp_tail) once every chunk has
-// pushed its lam' over DSMEM.
+// are resident from the start of K1's stream: they read their inputs while K1 runs, poll K1's
+// {m, s} words once K1's work counter shows every item claimed, and the finishing CTA runs
+// S4-S7 (warp_tail) once every chunk has pushed its lam' over DSMEM.
 //
 // Arithmetic and order are k_tail's (so the outputs are bit-identical): S2 4-lane merge of a
 // row's 16 parts (lane l4: parts 4 l4 .. 4 l4 + 3, then the xor-2 / xor-1 butterfly), ell =
@@ -108,6 +108,16 @@ __global__ void __launch_bounds__(kTsThreads, 8) k_tail_small(const __grid_const
         reset = (float)(-log((double)N));
     }
 
+    // ---- gate: one thread watches K1's work counter (sleeping ~1 us between reads) until every
+    // K1 item is claimed; only then do the CTA's lanes poll their words.  Polls in flight beside
+    // K1's stream slow it (profiles/r02j_ab_poll_shape_rejected.txt); the gate took cfg2 -0.1 us
+    // and N = 64 -0.3 us (profiles/r02j_ab_tail_small_gate.txt).  Bounded like the polls.
+    if (tid == 0 && prm.work_ctr) {
+        const uint64_t g0 = globaltimer_ns();
+        while (*reinterpret_cast<volatile unsigned *>(prm.work_ctr) < prm.gate_ctr && globaltimer_ns() - g0 < kXTimeoutNs)
+            __nanosleep(1000);
+    }
+    __syncthreads();
     // ---- S2: 4 lanes per row, 32 rows (16 target, 16 draft), polling K1's words
     bool late = false;
     {

@@ -19,6 +19,7 @@
 // source m repeated o_m - 1 times in ascending m).  PAPER.md:316-331 (Alg. 1, lines 9-14).
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include "smcsd_device.cuh"
 
@@ -38,6 +39,7 @@ struct WtArgs {
 struct WtSmem {
     WtArgs a;
     alignas(16) double eb[2][64];   // e of each role (16-byte broadcast reads), then C (role 0)
+    double pb[64];                  // role 0: the prefix sums P_m
     alignas(16) int ib[64];         // a_n
     int ex[64];                     // source of the i-th extra copy
     uint32_t st;                    // ST_DEGENERATE (role 1); the caller ORs it into the status
@@ -116,13 +118,14 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
     if (H == 1) eb[lane + 32] = 0.0;                            // (N8 may reach past 32: never with H = 1)
     __syncwarp();
     // sequential fp64 sums over e_0 .. e_{N-1} in particle order (reading G6), run by every
-    // lane from 16-byte broadcast shared loads; lane l keeps P_l (and P_{l+32})
+    // lane from 16-byte broadcast shared loads.  Role 0 records each P_m in shared memory (one
+    // store; lane l then reads P_l, P_{l+32}) and skips sum e^2 when eta = +inf (S5 does not
+    // read it); role 1 needs sum e^2 (ESS) but not P.
     const int N8 = (N + 7) & ~7;
-    double S, sq, Pm[H];
-    {
-        double acc = 0.0, q = 0.0, pm[H];
-#pragma unroll
-        for (int h = 0; h < H; ++h) pm[h] = 0.0;
+    double S, sq = 0.0, Pm[H];
+    auto sums = [&](auto cap_t, auto sq_t) {
+        constexpr bool kCap = decltype(cap_t)::value, kSq = decltype(sq_t)::value;
+        double acc = 0.0, q = 0.0;
         for (int m0 = 0; m0 < N8; m0 += 8) {
             double2 v[4];
 #pragma unroll
@@ -131,15 +134,22 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
             for (int k = 0; k < 8; ++k) {
                 const double em = (k & 1) ? v[k >> 1].y : v[k >> 1].x;
                 acc = __dadd_rn(acc, em);
-                q = __dadd_rn(q, __dmul_rn(em, em));
-#pragma unroll
-                for (int h = 0; h < H; ++h) pm[h] = m0 + k == lane + 32 * h ? acc : pm[h];
+                if (kSq) q = __dadd_rn(q, __dmul_rn(em, em));
+                if (kCap) ws.pb[m0 + k] = acc;
             }
         }
         S = acc;
         sq = q;
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    if (role == 1) sums(F_{}, T_{});
+    else if (A.eta == (double)INFINITY && !dry) sums(T_{}, F_{});
+    else sums(T_{}, T_{});
+    if (role == 0) {
+        __syncwarp();
 #pragma unroll
-        for (int h = 0; h < H; ++h) Pm[h] = pm[h];
+        for (int h = 0; h < H; ++h) Pm[h] = ws.pb[lane + 32 * h];
     }
     if (role == 1) {
         // ---- S4 outputs, off the ancestors' path
@@ -218,19 +228,23 @@ __device__ __noinline__ void warp_tail(int role, int p, int resample_mode, int d
             }
         }
     } else {
-        // 32 < N <= 64: binary search of C, then the tie run around the boundary (an O(log N)
-        // chain instead of 2 x N broadcast compares per lane)
+        // 32 < N <= 64: branchless binary search of the 64 entries of C (entries >= N are +inf,
+        // C is nondecreasing), both particles' searches interleaved; then the tie run around
+        // the boundary (an O(log N) chain instead of 2 x N broadcast compares per lane)
+        int lo[H];
+#pragma unroll
+        for (int h = 0; h < H; ++h) lo[h] = 0;
+#pragma unroll
+        for (int st = 32; st >= 1; st >>= 1) {
+#pragma unroll
+            for (int h = 0; h < H; ++h) lo[h] += eb[lo[h] + st - 1] <= u[h] ? st : 0;
+        }
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-            int lo = 0, hi = N;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (eb[mid] <= u[h]) lo = mid + 1; else hi = mid;
-            }
-            a[h] = lo;
+            a[h] = lo[h];
             if (act[h] && need_ties) {
-                for (int m = lo - 1; m >= 0 && fabs(__dsub_rn(u[h], eb[m])) <= tie; --m) ++ties;
-                for (int m = lo; m < N && fabs(__dsub_rn(u[h], eb[m])) <= tie; ++m) ++ties;
+                for (int m = lo[h] - 1; m >= 0 && fabs(__dsub_rn(u[h], eb[m])) <= tie; --m) ++ties;
+                for (int m = lo[h]; m < N && fabs(__dsub_rn(u[h], eb[m])) <= tie; ++m) ++ties;
             }
         }
     }

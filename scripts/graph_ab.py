@@ -2,7 +2,7 @@
 """Host cost per smcsd_step call, and cfg2 / N=64 device time per step eager vs CUDA-graph
 replay (removes the host from the loop).  SMCSD_LIB_OVERRIDE selects a library variant.
 Usage (GPU): python scripts/graph_ab.py"""
-import os, sys, time
+import math, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2604_15672_b200 as smc
@@ -18,10 +18,15 @@ if os.environ.get("SMCSD_POLL") is not None:                  # polling tail on 
     name += " poll=" + os.environ["SMCSD_POLL"]
 
 
+ETA = {"eta": math.inf} if os.environ.get("ETA_INF") else {}      # default eta = N/2
+if ETA:
+    name += " eta=inf"
+
+
 def case(label, N, ring_n=6, reps=20, P=1):
     ring = [synth.lm_logits(P, N, 8, 128256, device=dev, seed=10 + r) for r in range(ring_n)]
     ws, out = smc.Workspace(dev), smc.Outputs()
-    call = lambda i: smc.smcsd_step(*ring[i % ring_n], V=128256, step=i, out=out, fields=(), workspace=ws)
+    call = lambda i: smc.smcsd_step(*ring[i % ring_n], V=128256, step=i, out=out, fields=(), workspace=ws, **ETA)
     for i in range(3):
         call(i)
     torch.cuda.synchronize()
@@ -43,11 +48,11 @@ def case(label, N, ring_n=6, reps=20, P=1):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(s):
         for i in range(ring_n):
-            smc.smcsd_step(*ring[i], V=128256, step=i, out=out, fields=(), workspace=ws, stream=s)
+            smc.smcsd_step(*ring[i], V=128256, step=i, out=out, fields=(), workspace=ws, stream=s, **ETA)
         torch.cuda.synchronize()
         with torch.cuda.graph(g, stream=s):
             for i in range(ring_n):
-                smc.smcsd_step(*ring[i], V=128256, step=i, out=out, fields=(), workspace=ws, stream=s)
+                smc.smcsd_step(*ring[i], V=128256, step=i, out=out, fields=(), workspace=ws, stream=s, **ETA)
     g.replay()
     torch.cuda.synchronize()
     a.record()
