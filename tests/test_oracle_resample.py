@@ -42,6 +42,11 @@ def test_tie_counts(orc):
     * (0, 0, 1, 1), x = 0: C = (0, 0, .5, 1); u_0 = 0 meets C_0 = C_1 (2 ties), u_2 = .5 meets
       C_2 (1 tie): 3.  a = (2, 2, 3, 3): the plateau at zero is never chosen even at u = 0.
     * N = 4 equal, x = 1: u_n - C_{n-1} = 2^-32/4 = 2^-34 > 2^-40: no tie.
+    * N = 48 and 64 equal, x = 0: as above, N-1 ties (the GPU's two-particles-per-lane S6);
+      N = 64, x = 1: none.
+    * (.5, 0 x 38, .5), N = 40, x = 0: e = (1, 0, ..., 0, 1), C_0..C_38 = .5, C_39 = 1,
+      u_n = n/40.  u_20 = .5 meets the 39-entry plateau: 39 ties.  a_n = 0 for n < 20 (u < .5)
+      and 39 from n = 20 on (all 39 plateau entries are <= u): offspring 20 and 20.
     """
     for line in read_golden("systematic_ties.txt"):
         w, x, anc, off, ties = [s.strip() for s in line.split(";")]
