@@ -127,3 +127,46 @@ def test_small_tail_many_prompts(smc, orc):
         assert torch.equal(_bits(ref[f]), _bits(got[f])), f
     staged = orc.resample(np_(got["logw_pre"]), eta=math.inf, step=5)
     assert np.array_equal(np_(got["ancestors"]), staged["ancestors"])
+
+
+@pytest.mark.parametrize("N,K,variant", [(16, 8, "small"), (64, 8, "small"), (12, 12, "small"),
+                                         (16, 8, "poll256")])
+def test_polling_tail_graph_replay_stress(smc, N, K, variant):
+    """Back-to-back steps under CUDA-graph replay: a ring of 6 steps (each with its own inputs,
+    step counter and outputs) captured once and replayed 150 times (900 steps, PDL-chained, the
+    tail of one step overlapping the next step's K1 launch).  Each step's outputs after the last
+    replay are bit-identical to the same step run eagerly: the work-counter gate, the word array
+    zeroing and the counter re-arm carry no state from one step into the next."""
+    dev = torch.device("cuda")
+    V, R = 128256, 6
+    ring = [synth.lm_logits(1, N, K, V, device=dev, seed=900 + 17 * r) for r in range(R)]
+    _set(smc, variant)
+    try:
+        ws = smc.Workspace(dev)
+        outs = [smc.Outputs() for _ in range(R)]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+
+        def steps():
+            for i in range(R):
+                smc.smcsd_step(*ring[i], V=V, eta=math.inf, step=i, out=outs[i], workspace=ws, stream=s)
+
+        with torch.cuda.stream(s):
+            steps()
+        torch.cuda.synchronize()
+        ref = [{f: getattr(o, f).clone() for f in FIELDS if getattr(o, f, None) is not None} for o in outs]
+        for o in outs:                                          # poison: the replays must rewrite
+            for f in ref[0]:
+                getattr(o, f).fill_(7)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            steps()
+        for _ in range(150):
+            g.replay()
+        torch.cuda.synchronize()
+    finally:
+        _set(smc, "small")
+    for i, o in enumerate(outs):
+        assert int(o.status.max()) == 0, i
+        for f, t in ref[i].items():
+            assert torch.equal(_bits(getattr(o, f)), _bits(t)), (i, f)
