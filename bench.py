@@ -428,6 +428,7 @@ def summarize(per_kernel_ms, sharded, secondary, world):
     out["cfg5_tp_ms_per_step"] = c5.get("ms_per_step")
     out["cfg5_tp_path"] = "fused" if "fused_exchange" in c5 and "error" not in c5["fused_exchange"] else (
         "allgather" if c5 else None)
+    out["cfg5_tp_overhead_vs_plain"] = g(c5, "fused_exchange", "overhead_vs_plain")
     out["cfg2_verify_graph_us"] = g(secondary, "cfg2_verify", "plain", "graph_us_per_step")
     out["cfg2_verify_graph_frac_of_cold_floor"] = g(secondary, "cfg2_verify", "plain", "graph_frac_of_cold_floor")
     out["cfg3_in_place_frac"] = g(secondary, "cfg3", "in_place", "frac_of_measured")
@@ -791,6 +792,15 @@ def measure_cfg5(dev, rank, world, hbm_peak, steps=20, warmup=3):
                                  "path": "smcsd_tp_step: K1 pushes each partial to every rank as "
                                          "two tagged 8-byte words (P2P relaxed stores, no fence or "
                                          "flag); the tail polls them + S2-S7"}
+        if world == 1:
+            # one rank holds the whole vocabulary: the plain smcsd_step on the same inputs, so
+            # the line shows what the fused exchange costs (profiles/r02k_tp_overhead_decomposition.txt)
+            op, wsq = smc.Outputs(logw=logw), smc.Workspace(dev)
+            fnq = lambda i: smc.smcsd_step(sp, sq, tok, V=V, logw_prev=logw, eta=math.inf, step=i,
+                                           out=op, fields=(), workspace=wsq)
+            msq = _time_steps(fnq, steps, warmup, world, dev)
+            res["fused_exchange"]["plain_step_ms"] = round(msq, 4)
+            res["fused_exchange"]["overhead_vs_plain"] = round(msf / msq - 1.0, 4)
         # the product path is the line's cfg5 figure
         res["ms_per_step"] = round(msf, 4)
         res["steps_per_s"] = round(1e3 / msf, 1)
