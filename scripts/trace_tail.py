@@ -74,6 +74,11 @@ if ck[0]:
     print("chunk 0 clocks after pdl_wait: " + "  ".join(
         f"{nm} {ck[i] - ck[0]}" for i, nm in enumerate(["wait", "flags", "S2 merge", "ell", "terms", "fence", "counter"]) if ck[i]))
 
+fc = t[2210:2216]
+if fc[0] and fc[5]:
+    print("finisher clocks from rows merged: " + "  ".join(
+        f"{nm} {fc[i] - fc[0]}" for i, nm in enumerate(["merged", "phase1 wait", "ell+terms", "S3+push", "arrive+stores", "barrier"]) if fc[i]))
+
 ph = t[2300:2309]
 PHASES = (["start", "exp", "prefix+ess", "anc+ties", "offspring+plan", "S7 stores", "ess/lse/wnorm"] if t[2400] else
           ["start", "M", "exp", "prefix+ess", "wnorm", "C", "u+search", "plan", "S7"])
